@@ -1,0 +1,179 @@
+/* qldpc_b200.h — the C-ABI boundary of the B200-native min-sum decoder.
+ *
+ * This is the drop-in boundary for ONE path of the reference: the scaled
+ * min-sum syndrome decoder behind `class qldpc::Decoder` and the free functions
+ * `decode`, `decode_batch`, `decode_css`
+ * (reference: proj/include/qldpc/decoder.hpp:77-129, proj/src/decoder.cpp).
+ * Plain pointers and sizes only; no C++ or torch types cross this line.
+ *
+ * Conventions shared with the reference:
+ *   - a packed bit vector of L bits is ceil(L/64) uint64 words, bit i at
+ *     (words[i >> 6] >> (i & 63)) & 1   (proj/include/qldpc/gf2.hpp:26), so
+ *     `Gf2Vector::words()` can be passed straight through;
+ *   - edges are numbered check-major, `var_edges` ascending per variable
+ *     (proj/include/qldpc/tanner_graph.hpp:15-48);
+ *   - a decoder over S segments (1 for a plain graph, 2 = X,Z for a CssCode,
+ *     proj/src/decoder.cpp:406-424) reports `converged` and `iterations` PER
+ *     SEGMENT; `decode_into` semantics are AND / MAX over segments
+ *     (decoder.cpp:204-213), `decode_css_into` semantics are the per-segment
+ *     values themselves (decoder.cpp:194-202).
+ *
+ * Every function returns a qb_status.  QB_INVALID_ARGUMENT marks exactly the
+ * conditions for which the reference throws std::invalid_argument; any CUDA
+ * failure is QB_RUNTIME_ERROR.  The message is available from
+ * qb_last_error(handle) (or qb_last_error(NULL) for a failed create).
+ * There is NO CPU fallback: without a usable CUDA device every compute entry
+ * point fails with QB_RUNTIME_ERROR.
+ */
+#ifndef QLDPC_B200_H_
+#define QLDPC_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  QB_OK = 0,
+  QB_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+  QB_RUNTIME_ERROR = 2     /* CUDA / resource failure: std::runtime_error */
+} qb_status;
+
+/* reference: enum class Arithmetic (decoder.hpp:16).  QB_ARITH_HALF is an
+ * extension with no reference counterpart (fp16 messages, fp32 arithmetic). */
+typedef enum {
+  QB_ARITH_FLOAT = 0,
+  QB_ARITH_INT8 = 1,
+  QB_ARITH_INT16 = 2,
+  QB_ARITH_HALF = 3
+} qb_arithmetic;
+
+/* reference: struct TannerGraph (tanner_graph.hpp:15-48). */
+typedef struct {
+  uint32_t num_checks;
+  uint32_t num_vars;
+  uint32_t num_edges;
+  const uint32_t* edge_var;      /* [num_edges] */
+  const uint32_t* check_offsets; /* [num_checks + 1] */
+  const uint32_t* var_offsets;   /* [num_vars + 1] */
+  const uint32_t* var_edges;     /* [num_edges] */
+} qb_graph;
+
+/* reference: struct Segment (decoder.cpp:25-30).  Segments must tile the
+ * graph block-diagonally: every edge of a check in [check_begin, check_end)
+ * ends at a variable in [var_begin, var_end). */
+typedef struct {
+  uint32_t check_begin, check_end, var_begin, var_end;
+} qb_segment;
+
+/* reference: struct DecoderConfig (decoder.hpp:23-38). */
+typedef struct {
+  uint64_t max_iterations;   /* >= 1 */
+  double alpha;              /* (0, 1] */
+  int32_t early_termination; /* 0 / 1 */
+  int32_t arithmetic;        /* qb_arithmetic */
+  double quant_scale;        /* 0 = mode default (8 for int8, 256 for int16) */
+  const double* priors;      /* NULL or num_priors == 0: uniform prior 1 */
+  uint64_t num_priors;       /* 0 or num_vars */
+} qb_config;
+
+typedef struct qb_decoder qb_decoder;
+
+/* Kernel selection and I/O policy knobs (qb_set_option). */
+typedef enum {
+  /* 0 = auto, 1 = generic CSR kernel, 2 = regular (ELL, register-resident
+   * tables) kernel.  Selecting 2 on a graph it cannot run is an error. */
+  QB_OPT_KERNEL = 0,
+  /* Single-shot I/O: 0 = mapped pinned host memory + completion flag (no
+   * memcpy, no stream sync), 1 = cudaMemcpyAsync H2D / kernel / D2H + stream
+   * synchronize (the reference paper's protocol). */
+  QB_OPT_LATENCY_IO = 1,
+  /* Single-shot launch shape: 0 = auto, 1 = one CTA per shot, 2 = one thread
+   * block cluster per shot (one CTA per segment, results merged over DSMEM). */
+  QB_OPT_LATENCY_SHAPE = 2,
+  /* Threads per segment group (0 = auto). */
+  QB_OPT_GROUP_THREADS = 3,
+  /* CTAs per SM for the persistent batch kernel (0 = auto). */
+  QB_OPT_BATCH_CTAS_PER_SM = 4
+} qb_option;
+
+/* Builds a decoder: validates like Decoder::Decoder (decoder.cpp:373-404,
+ * :83-131), uploads the code tables and allocates every device / pinned
+ * buffer, so decode calls are allocation-free.  The graph arrays are copied;
+ * they need not outlive the call.  `device` is the CUDA ordinal. */
+qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
+                            uint32_t num_segments, const qb_config* config,
+                            int device, qb_decoder** out);
+
+void qb_decoder_destroy(qb_decoder* h);
+
+/* Thread-local for h == NULL (create failures), else the handle's. */
+const char* qb_last_error(const qb_decoder* h);
+
+qb_status qb_set_option(qb_decoder* h, int option, int64_t value);
+int64_t qb_get_option(const qb_decoder* h, int option);
+
+uint32_t qb_num_checks(const qb_decoder* h);
+uint32_t qb_num_vars(const qb_decoder* h);
+uint32_t qb_num_segments(const qb_decoder* h);
+
+/* Decoder::decode_into / decode_css_into (decoder.cpp:551-591) for ONE
+ * syndrome, latency path.  All pointers are HOST memory.
+ *   syndrome   ceil(M/64) words      estimate  ceil(N/64) words (out)
+ *   residual   ceil(M/64) words (out, may be NULL)
+ *   converged  [num_segments] (out)  iterations [num_segments] (out) */
+qb_status qb_decode(qb_decoder* h, const uint64_t* syndrome,
+                    uint64_t* estimate, uint64_t* residual, uint8_t* converged,
+                    uint32_t* iterations);
+
+/* decode_batch (decoder.cpp:604-655) for `shots` syndromes held in HOST
+ * memory (pinned memory from qb_host_alloc makes the copies asynchronous):
+ * H2D, persistent decode kernel, D2H, all inside the call.  Strides are the
+ * packed word counts above; converged / iterations are [shots][num_segments].
+ * Results are elementwise identical to `shots` qb_decode calls. */
+qb_status qb_decode_batch(qb_decoder* h, uint64_t shots,
+                          const uint64_t* syndromes, uint64_t* estimates,
+                          uint64_t* residuals /* may be NULL */,
+                          uint8_t* converged, uint32_t* iterations);
+
+/* Same, with every buffer already resident in DEVICE memory (16-byte aligned)
+ * and the launch enqueued on `stream` (a cudaStream_t, NULL = default). */
+qb_status qb_decode_batch_device(qb_decoder* h, uint64_t shots,
+                                 const uint64_t* d_syndromes,
+                                 uint64_t* d_estimates,
+                                 uint64_t* d_residuals /* may be NULL */,
+                                 uint8_t* d_converged, uint32_t* d_iterations,
+                                 void* stream);
+
+/* Debug / parity: decode one syndrome and also return the final edge messages
+ * q (variable->check) and r (check->variable) in reference edge order, as
+ * float for QB_ARITH_FLOAT / QB_ARITH_HALF and int32 for the integer modes
+ * (pass the matching pair, NULL for the other). */
+qb_status qb_decode_debug(qb_decoder* h, const uint64_t* syndrome,
+                          uint64_t* estimate, uint64_t* residual,
+                          uint8_t* converged, uint32_t* iterations,
+                          float* q_f32, float* r_f32, int32_t* q_i32,
+                          int32_t* r_i32);
+
+/* Decoder::last_kernel_ns (decoder.cpp:593-596): device-side %globaltimer
+ * span of the most recent qb_decode (first instruction to last store). */
+uint64_t qb_last_kernel_ns(const qb_decoder* h);
+
+/* Number of kernels this handle has launched since creation. */
+uint64_t qb_launch_count(const qb_decoder* h);
+
+/* Pinned (page-locked, device-mapped) host memory for batch I/O. */
+qb_status qb_host_alloc(void** out, size_t bytes);
+void qb_host_free(void* p);
+
+/* Library / device description, e.g. for bench logs. */
+const char* qb_version(void);
+qb_status qb_device_info(int device, char* name, size_t name_len,
+                         int* sm_count, int* cc_major, int* cc_minor);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QLDPC_B200_H_ */

@@ -1,0 +1,130 @@
+// Shared device-side definitions for the sm_100a min-sum decoder kernels.
+//
+// Terminology follows the reference's domain (proj/src/decoder.cpp): a SHOT is
+// one syndrome to decode; a SEGMENT is an independent block of the Tanner
+// graph (1 for a plain graph, 2 = X and Z for a CssCode); q are
+// variable->check messages, r are check->variable messages, gamma the priors.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace qb {
+
+constexpr int kMaxSegments = 8;
+constexpr int kWarp = 32;
+
+struct SegmentDev {
+  uint32_t c0, c1;  // checks [c0, c1)
+  uint32_t v0, v1;  // variables [v0, v1)
+  uint32_t e0, e1;  // edges [e0, e1) (check-major numbering => contiguous)
+};
+
+// Everything a kernel needs to know about one decoder (code tables + config).
+// Passed by value as a kernel parameter (__grid_constant__), so it sits in
+// constant bank 0 and costs no loads from global memory.
+struct DecodeParams {
+  uint32_t M, N, E, nseg;
+  uint32_t syn_w32;  // 2 * ceil(M / 64): 32-bit words per packed syndrome
+  uint32_t est_w32;  // 2 * ceil(N / 64): 32-bit words per packed estimate
+  uint32_t max_iter;
+  int32_t early;
+  uint32_t ngroups;        // warp groups per CTA (<= nseg)
+  uint32_t group_threads;  // threads per group, multiple of 32
+  // arithmetic constants
+  double alpha;       // float mode: fp64 multiply, one rounding (decoder.cpp:302-307)
+  float alpha_f;      // half mode
+  float deg1_f;       // float(alpha * 64)           (decoder.cpp:256)
+  float clamp_f;      // float(1e30)                 (decoder.cpp:23, :238-241)
+  uint32_t alpha_fx;  // lround(alpha * 65536)       (decoder.cpp:89)
+  int32_t kmax;       // 127 / 32767                 (decoder.cpp:50, :59)
+  int32_t deg1_i;     // scale_q16(kmax)             (decoder.cpp:253)
+  // CSR tables (device global memory, read-only)
+  const uint32_t* check_off;   // [M + 1]
+  const uint32_t* var_off;     // [N + 1]
+  const uint32_t* var_edges;   // [E]
+  const uint32_t* edge_var;    // [E]
+  const uint32_t* edge_check;  // [E]
+  const void* gamma;           // [N] float (float/half modes) or int32 (int modes)
+  SegmentDev segs[kMaxSegments];
+};
+
+// Per-launch I/O description.  All pointers are device-accessible (device
+// memory, or mapped pinned host memory on the single-shot path).
+struct ShotIO {
+  uint64_t nshots;
+  const uint32_t* syn;  // [nshots][syn_w32]
+  uint32_t* est;        // [nshots][est_w32]
+  uint32_t* resid;      // [nshots][syn_w32] or nullptr
+  uint8_t* conv;        // [nshots][nseg]
+  uint32_t* iters;      // [nshots][nseg]
+  unsigned int* sched;  // [0] next-shot ticket, [1] finished-CTA count
+  // single-shot completion (nullptr on the batch path)
+  uint64_t* kernel_ns;       // %globaltimer span, written before the flag
+  volatile uint32_t* flag;   // receives `seq` after every result is visible
+  uint32_t seq;
+  // debug dumps of the final edge messages (nullptr unless qb_decode_debug)
+  void* q_dump;
+  void* r_dump;
+};
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Named barrier over one warp group (ids 1..15; id 0 is __syncthreads()).
+__device__ __forceinline__ void group_barrier(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Bits i of 32-bit word w whose global index 32*w + i lies in [lo, hi).
+__device__ __forceinline__ uint32_t range_mask(uint32_t w, uint32_t lo, uint32_t hi) {
+  const uint32_t base = w * 32u;
+  if (hi <= base || lo >= base + 32u) return 0u;
+  const uint32_t a = lo > base ? lo - base : 0u;
+  const uint32_t b = hi < base + 32u ? hi - base : 32u;
+  const uint32_t upto_b = b >= 32u ? 0xffffffffu : ((1u << b) - 1u);
+  const uint32_t below_a = (1u << a) - 1u;  // a < 32 here
+  return upto_b & ~below_a;
+}
+
+// ---------------------------------------------------------------------------
+// Arithmetic traits.  Each mode defines the stored message type, the prior
+// type, and the two node updates' scalar pieces.
+// ---------------------------------------------------------------------------
+
+struct ArithF32 {
+  using Msg = float;
+  using Gam = float;
+  static constexpr bool kInt = false;
+};
+struct ArithF16 {
+  using Msg = __half;
+  using Gam = float;
+  static constexpr bool kInt = false;
+};
+struct ArithI8 {
+  using Msg = int8_t;
+  using Gam = int32_t;
+  static constexpr bool kInt = true;
+};
+struct ArithI16 {
+  using Msg = int16_t;
+  using Gam = int32_t;
+  static constexpr bool kInt = true;
+};
+
+// Q16 scaling of a non-negative magnitude (decoder.cpp:226-229).  mag <= 32767
+// and alpha_fx <= 65536, so the product fits 32 unsigned bits.
+__device__ __forceinline__ int32_t scale_q16(uint32_t mag, uint32_t alpha_fx) {
+  return static_cast<int32_t>((mag * alpha_fx + 32768u) >> 16);
+}
+
+// Half-mode symmetric clamp keeps stored messages finite in fp16 (the analogue
+// of the reference's 1e30 clamp for fp32 storage).
+constexpr float kHalfClamp = 60000.0f;
+
+}  // namespace qb

@@ -1,0 +1,762 @@
+// C-ABI implementation (include/qldpc_b200.h): validation, the code loader
+// that turns a Tanner graph into device tables, and the kernel launches.
+//
+// Reference behaviour mirrored here: Decoder construction + validation
+// (proj/src/decoder.cpp:73-140, :373-404), decode_into / decode_css_into
+// (:551-591), decode_batch (:604-655), last_kernel_ns (:593-596).
+#include "../../include/qldpc_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernel_generic.cuh"
+
+using namespace qb;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct StatusError {
+  qb_status code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(qb_status code, std::string msg) { throw StatusError{code, std::move(msg)}; }
+
+#define CUDA_TRY(expr)                                                               \
+  do {                                                                               \
+    cudaError_t err__ = (expr);                                                      \
+    if (err__ != cudaSuccess) {                                                      \
+      fail(QB_RUNTIME_ERROR, std::string("CUDA error in " #expr ": ") +              \
+                                 cudaGetErrorName(err__) + " (" +                    \
+                                 cudaGetErrorString(err__) + ")");                   \
+    }                                                                                \
+  } while (0)
+
+template <typename T>
+T* dev_upload(const std::vector<T>& host) {
+  T* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, std::max<size_t>(host.size(), 1) * sizeof(T)));
+  if (!host.empty()) {
+    CUDA_TRY(cudaMemcpy(d, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  return d;
+}
+
+// round(value * scale) clamped to [-limit, limit] (decoder.cpp:500-509).
+int32_t quantize_saturate(double value, double scale, int32_t limit) {
+  const double scaled = value * scale;
+  if (std::isnan(scaled)) fail(QB_INVALID_ARGUMENT, "quantize_saturate: value is NaN");
+  if (scaled >= static_cast<double>(limit)) return limit;
+  if (scaled <= static_cast<double>(-limit)) return -limit;
+  return static_cast<int32_t>(std::llround(scaled));
+}
+
+size_t msg_bytes_of(int arith) {
+  switch (arith) {
+    case QB_ARITH_FLOAT: return 4;
+    case QB_ARITH_INT8: return 1;
+    case QB_ARITH_INT16: return 2;
+    default: return 2;  // half
+  }
+}
+
+}  // namespace
+
+struct qb_decoder {
+  int device = 0;
+  int sm_count = 0;
+  int max_smem_optin = 0;
+  cudaStream_t stream = nullptr;
+  DecodeParams P{};
+  int arith = 0;
+  std::vector<void*> dev_allocs;  // tables, freed in the destructor
+  unsigned int* d_sched = nullptr;
+
+  // single-shot staging: mapped pinned host memory (+ device mirrors for the
+  // memcpy protocol)
+  uint32_t* h_in = nullptr;   // [syn_w32]
+  uint32_t* d_in_map = nullptr;
+  unsigned char* h_out = nullptr;
+  unsigned char* d_out_map = nullptr;
+  size_t out_bytes = 0, off_res = 0, off_conv = 0, off_iters = 0, off_ns = 0, off_flag = 0;
+  uint32_t* d_in_dev = nullptr;
+  unsigned char* d_out_dev = nullptr;
+  uint32_t seq = 0;
+  uint64_t last_kernel_ns = 0;
+
+  // batch buffers (device), grown on demand
+  uint64_t batch_cap = 0;
+  uint32_t *b_syn = nullptr, *b_est = nullptr, *b_res = nullptr, *b_iters = nullptr;
+  uint8_t* b_conv = nullptr;
+  // debug dumps
+  void *d_qdump = nullptr, *d_rdump = nullptr;
+
+  // options
+  int64_t opt_kernel = 0, opt_latency_io = 0, opt_latency_shape = 0, opt_group_threads = 0,
+          opt_batch_ctas = 0;
+
+  uint64_t launches = 0;
+  std::string err;
+  size_t smem_bytes = 0;
+};
+
+namespace {
+
+void free_batch(qb_decoder* h) {
+  cudaFree(h->b_syn);
+  cudaFree(h->b_est);
+  cudaFree(h->b_res);
+  cudaFree(h->b_iters);
+  cudaFree(h->b_conv);
+  h->b_syn = h->b_est = h->b_res = h->b_iters = nullptr;
+  h->b_conv = nullptr;
+  h->batch_cap = 0;
+}
+
+void destroy(qb_decoder* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (void* p : h->dev_allocs) cudaFree(p);
+  cudaFree(h->d_sched);
+  cudaFree(h->d_in_dev);
+  cudaFree(h->d_out_dev);
+  cudaFree(h->d_qdump);
+  cudaFree(h->d_rdump);
+  if (h->h_in) cudaFreeHost(h->h_in);
+  if (h->h_out) cudaFreeHost(h->h_out);
+  free_batch(h);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+// ---- validation -----------------------------------------------------------
+
+void validate_graph(const qb_graph* g) {
+  if (!g) fail(QB_INVALID_ARGUMENT, "graph is NULL");
+  if (g->num_checks == 0 || g->num_vars == 0 || g->num_edges == 0) {
+    fail(QB_INVALID_ARGUMENT, "graph must have checks, variables and at least one edge");
+  }
+  if (!g->edge_var || !g->check_offsets || !g->var_offsets || !g->var_edges) {
+    fail(QB_INVALID_ARGUMENT, "graph arrays must not be NULL");
+  }
+  const uint32_t M = g->num_checks, N = g->num_vars, E = g->num_edges;
+  if (g->check_offsets[0] != 0 || g->check_offsets[M] != E) {
+    fail(QB_INVALID_ARGUMENT, "check_offsets must run from 0 to num_edges");
+  }
+  for (uint32_t m = 0; m < M; ++m) {
+    if (g->check_offsets[m + 1] < g->check_offsets[m]) {
+      fail(QB_INVALID_ARGUMENT, "check_offsets must be non-decreasing");
+    }
+  }
+  if (g->var_offsets[0] != 0 || g->var_offsets[N] != E) {
+    fail(QB_INVALID_ARGUMENT, "var_offsets must run from 0 to num_edges");
+  }
+  for (uint32_t e = 0; e < E; ++e) {
+    if (g->edge_var[e] >= N) fail(QB_INVALID_ARGUMENT, "edge_var entry out of range");
+  }
+  std::vector<uint8_t> seen(E, 0);
+  for (uint32_t n = 0; n < N; ++n) {
+    if (g->var_offsets[n + 1] < g->var_offsets[n]) {
+      fail(QB_INVALID_ARGUMENT, "var_offsets must be non-decreasing");
+    }
+    for (uint32_t i = g->var_offsets[n]; i < g->var_offsets[n + 1]; ++i) {
+      const uint32_t e = g->var_edges[i];
+      if (e >= E || seen[e] || g->edge_var[e] != n) {
+        fail(QB_INVALID_ARGUMENT, "var_edges is not a permutation consistent with edge_var");
+      }
+      if (i > g->var_offsets[n] && g->var_edges[i - 1] >= e) {
+        fail(QB_INVALID_ARGUMENT, "var_edges must be ascending within each variable");
+      }
+      seen[e] = 1;
+    }
+  }
+}
+
+// Mirrors validate_common (decoder.cpp:373-387).
+void validate_config_common(const qb_graph* g, const qb_config* c) {
+  if (!c) fail(QB_INVALID_ARGUMENT, "config is NULL");
+  if (c->max_iterations < 1) {
+    fail(QB_INVALID_ARGUMENT, "DecoderConfig: max_iterations must be at least 1");
+  }
+  if (c->max_iterations > 0x7fffffffull) {
+    fail(QB_INVALID_ARGUMENT, "DecoderConfig: max_iterations exceeds the device counter range");
+  }
+  if (!(c->alpha > 0.0 && c->alpha <= 1.0)) {
+    fail(QB_INVALID_ARGUMENT, "DecoderConfig: alpha must lie in (0, 1]");
+  }
+  const bool has = c->priors != nullptr && c->num_priors != 0;
+  if (c->num_priors != 0 && c->priors == nullptr) {
+    fail(QB_INVALID_ARGUMENT, "DecoderConfig: num_priors given but priors is NULL");
+  }
+  if (has && c->num_priors != g->num_vars) {
+    fail(QB_INVALID_ARGUMENT, "DecoderConfig: " + std::to_string(c->num_priors) +
+                                  " priors given but the graph has " +
+                                  std::to_string(g->num_vars) + " variables");
+  }
+  if (c->arithmetic < QB_ARITH_FLOAT || c->arithmetic > QB_ARITH_HALF) {
+    fail(QB_INVALID_ARGUMENT, "DecoderConfig: unknown arithmetic mode");
+  }
+}
+
+// ---- kernel dispatch ------------------------------------------------------
+
+template <class A>
+void launch_generic_t(qb_decoder* h, const ShotIO& io, unsigned grid, cudaStream_t stream) {
+  auto kern = decode_generic_kernel<A>;
+  static thread_local const void* configured = nullptr;
+  (void)configured;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(h->smem_bytes)));
+  const unsigned block = h->P.ngroups * h->P.group_threads;
+  kern<<<grid, block, h->smem_bytes, stream>>>(h->P, io);
+  CUDA_TRY(cudaGetLastError());
+  ++h->launches;
+}
+
+void launch_generic(qb_decoder* h, const ShotIO& io, unsigned grid, cudaStream_t stream) {
+  switch (h->arith) {
+    case QB_ARITH_FLOAT: launch_generic_t<ArithF32>(h, io, grid, stream); break;
+    case QB_ARITH_INT8: launch_generic_t<ArithI8>(h, io, grid, stream); break;
+    case QB_ARITH_INT16: launch_generic_t<ArithI16>(h, io, grid, stream); break;
+    default: launch_generic_t<ArithF16>(h, io, grid, stream); break;
+  }
+}
+
+template <class A>
+int occupancy_generic_t(qb_decoder* h) {
+  int n = 0;
+  auto kern = decode_generic_kernel<A>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(h->smem_bytes)));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &n, kern, static_cast<int>(h->P.ngroups * h->P.group_threads), h->smem_bytes));
+  return n;
+}
+
+int occupancy_generic(qb_decoder* h) {
+  switch (h->arith) {
+    case QB_ARITH_FLOAT: return occupancy_generic_t<ArithF32>(h);
+    case QB_ARITH_INT8: return occupancy_generic_t<ArithI8>(h);
+    case QB_ARITH_INT16: return occupancy_generic_t<ArithI16>(h);
+    default: return occupancy_generic_t<ArithF16>(h);
+  }
+}
+
+void choose_shape(qb_decoder* h) {
+  DecodeParams& P = h->P;
+  P.ngroups = std::min<uint32_t>(P.nseg, 8);
+  uint32_t want = 32;
+  for (uint32_t s = 0; s < P.nseg; ++s) {
+    const uint32_t ms = P.segs[s].c1 - P.segs[s].c0;
+    const uint32_t ns = P.segs[s].v1 - P.segs[s].v0;
+    want = std::max(want, std::max(ms, (ns + 1) / 2));
+  }
+  uint32_t T = h->opt_group_threads > 0 ? static_cast<uint32_t>(h->opt_group_threads) : want;
+  T = (T + 31u) & ~31u;
+  const uint32_t cap = (1024u / P.ngroups) & ~31u;
+  T = std::max(32u, std::min(T, cap));
+  P.group_threads = T;
+}
+
+void ensure_batch(qb_decoder* h, uint64_t shots, bool want_resid) {
+  if (shots <= h->batch_cap && (!want_resid || h->b_res)) return;
+  const uint64_t cap = std::max<uint64_t>(shots, h->batch_cap);
+  free_batch(h);
+  const DecodeParams& P = h->P;
+  CUDA_TRY(cudaMalloc(&h->b_syn, cap * P.syn_w32 * 4));
+  CUDA_TRY(cudaMalloc(&h->b_est, cap * P.est_w32 * 4));
+  CUDA_TRY(cudaMalloc(&h->b_res, cap * P.syn_w32 * 4));
+  CUDA_TRY(cudaMalloc(&h->b_iters, cap * P.nseg * 4));
+  CUDA_TRY(cudaMalloc(&h->b_conv, cap * P.nseg));
+  h->batch_cap = cap;
+}
+
+unsigned batch_grid(qb_decoder* h, uint64_t shots) {
+  int per_sm = occupancy_generic(h);
+  if (per_sm < 1) fail(QB_RUNTIME_ERROR, "decode kernel does not fit on an SM");
+  if (h->opt_batch_ctas > 0) per_sm = std::min<int>(per_sm, static_cast<int>(h->opt_batch_ctas));
+  const uint64_t resident = static_cast<uint64_t>(per_sm) * h->sm_count;
+  return static_cast<unsigned>(std::min<uint64_t>(shots, resident));
+}
+
+void run_batch_device(qb_decoder* h, uint64_t shots, const uint32_t* d_syn, uint32_t* d_est,
+                      uint32_t* d_res, uint8_t* d_conv, uint32_t* d_iters, cudaStream_t stream) {
+  if (shots == 0) return;
+  if (shots > 0x7fff0000ull) fail(QB_INVALID_ARGUMENT, "too many shots for one launch");
+  ShotIO io{};
+  io.nshots = shots;
+  io.syn = d_syn;
+  io.est = d_est;
+  io.resid = d_res;
+  io.conv = d_conv;
+  io.iters = d_iters;
+  io.sched = h->d_sched;
+  launch_generic(h, io, batch_grid(h, shots), stream);
+}
+
+template <typename F>
+qb_status guarded(qb_decoder* h, F&& f) {
+  try {
+    if (h) {
+      cudaError_t e = cudaSetDevice(h->device);
+      if (e != cudaSuccess) fail(QB_RUNTIME_ERROR, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    }
+    f();
+    return QB_OK;
+  } catch (const StatusError& e) {
+    (h ? h->err : g_create_error) = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    (h ? h->err : g_create_error) = e.what();
+    return QB_RUNTIME_ERROR;
+  }
+}
+
+void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, uint64_t* residual,
+                 uint8_t* converged, uint32_t* iterations, bool debug) {
+  const DecodeParams& P = h->P;
+  if (!syndrome || !estimate || !converged || !iterations) {
+    fail(QB_INVALID_ARGUMENT, "decode: NULL buffer");
+  }
+  std::memcpy(h->h_in, syndrome, P.syn_w32 * 4);
+  const uint32_t seq = ++h->seq;
+  ShotIO io{};
+  io.nshots = 1;
+  io.sched = h->d_sched;
+  io.seq = seq;
+  if (debug) {
+    io.q_dump = h->d_qdump;
+    io.r_dump = h->d_rdump;
+  }
+  volatile uint32_t* h_flag = reinterpret_cast<volatile uint32_t*>(h->h_out + h->off_flag);
+  const bool mapped = h->opt_latency_io == 0;
+  unsigned char* out = mapped ? h->d_out_map : h->d_out_dev;
+  io.syn = mapped ? h->d_in_map : h->d_in_dev;
+  io.est = reinterpret_cast<uint32_t*>(out);
+  io.resid = reinterpret_cast<uint32_t*>(out + h->off_res);
+  io.conv = out + h->off_conv;
+  io.iters = reinterpret_cast<uint32_t*>(out + h->off_iters);
+  io.kernel_ns = reinterpret_cast<uint64_t*>(out + h->off_ns);
+  io.flag = reinterpret_cast<volatile uint32_t*>(out + h->off_flag);
+
+  if (mapped) {
+    launch_generic(h, io, 1, h->stream);
+    // Spin on the completion word the kernel writes last; no stream sync on
+    // the fast path.  A watchdog falls back to the runtime for diagnosis.
+    const auto t0 = std::chrono::steady_clock::now();
+    uint64_t spins = 0;
+    while (*h_flag != seq) {
+      if ((++spins & 0xffff) == 0) {
+        if (cudaStreamQuery(h->stream) != cudaErrorNotReady) {
+          CUDA_TRY(cudaStreamSynchronize(h->stream));
+          if (*h_flag == seq) break;
+          fail(QB_RUNTIME_ERROR, "decode kernel finished without signalling completion");
+        }
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20)) {
+          fail(QB_RUNTIME_ERROR, "decode kernel timed out");
+        }
+      }
+    }
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(h->d_in_dev, h->h_in, P.syn_w32 * 4, cudaMemcpyHostToDevice,
+                             h->stream));
+    launch_generic(h, io, 1, h->stream);
+    CUDA_TRY(cudaMemcpyAsync(h->h_out, h->d_out_dev, h->out_bytes, cudaMemcpyDeviceToHost,
+                             h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+  }
+  std::memcpy(estimate, h->h_out, P.est_w32 * 4);
+  if (residual) std::memcpy(residual, h->h_out + h->off_res, P.syn_w32 * 4);
+  std::memcpy(converged, h->h_out + h->off_conv, P.nseg);
+  std::memcpy(iterations, h->h_out + h->off_iters, P.nseg * 4);
+  std::memcpy(&h->last_kernel_ns, h->h_out + h->off_ns, 8);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* qb_version(void) { return "qldpc_b200 0.1 (sm_100a)"; }
+
+const char* qb_last_error(const qb_decoder* h) {
+  return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+qb_status qb_device_info(int device, char* name, size_t name_len, int* sm_count, int* cc_major,
+                         int* cc_minor) {
+  return guarded(nullptr, [&] {
+    cudaDeviceProp prop{};
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (name && name_len) {
+      std::strncpy(name, prop.name, name_len - 1);
+      name[name_len - 1] = 0;
+    }
+    if (sm_count) *sm_count = prop.multiProcessorCount;
+    if (cc_major) *cc_major = prop.major;
+    if (cc_minor) *cc_minor = prop.minor;
+  });
+}
+
+qb_status qb_host_alloc(void** out, size_t bytes) {
+  return guarded(nullptr, [&] {
+    if (!out) fail(QB_INVALID_ARGUMENT, "qb_host_alloc: NULL out");
+    CUDA_TRY(cudaHostAlloc(out, std::max<size_t>(bytes, 1), cudaHostAllocPortable));
+  });
+}
+
+void qb_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
+                            uint32_t num_segments, const qb_config* config, int device,
+                            qb_decoder** out) {
+  qb_decoder* h = nullptr;
+  const qb_status st = guarded(nullptr, [&] {
+    if (!out) fail(QB_INVALID_ARGUMENT, "out handle is NULL");
+    *out = nullptr;
+    validate_graph(graph);
+    validate_config_common(graph, config);
+    const uint32_t M = graph->num_checks, N = graph->num_vars, E = graph->num_edges;
+    const bool has_priors = config->priors != nullptr && config->num_priors != 0;
+    const int arith = config->arithmetic;
+
+    // ---- priors (decoder.cpp:82-132)
+    std::vector<float> gamma_f;
+    std::vector<int32_t> gamma_i;
+    uint32_t alpha_fx = 0;
+    int32_t kmax = 0;
+    if (arith == QB_ARITH_INT8 || arith == QB_ARITH_INT16) {
+      kmax = arith == QB_ARITH_INT8 ? 127 : 32767;
+      const double scale = config->quant_scale != 0.0 ? config->quant_scale
+                                                      : (arith == QB_ARITH_INT8 ? 8.0 : 256.0);
+      if (!(scale > 0.0) || !std::isfinite(scale)) {
+        fail(QB_INVALID_ARGUMENT, "DecoderConfig: quant_scale must be positive and finite");
+      }
+      alpha_fx = static_cast<uint32_t>(std::lround(config->alpha * 65536.0));
+      if (alpha_fx == 0) {
+        fail(QB_INVALID_ARGUMENT,
+             "DecoderConfig: alpha is too small for the fixed-point message scaling");
+      }
+      uint64_t max_degree = 0;
+      for (uint32_t n = 0; n < N; ++n) {
+        max_degree = std::max<uint64_t>(max_degree,
+                                        graph->var_offsets[n + 1] - graph->var_offsets[n]);
+      }
+      if (max_degree + 1 > static_cast<uint64_t>(std::numeric_limits<int32_t>::max() / kmax)) {
+        fail(QB_INVALID_ARGUMENT,
+             "DecoderConfig: variable degree too large for 32-bit accumulation in this "
+             "integer mode");
+      }
+      gamma_i.resize(N);
+      for (uint32_t n = 0; n < N; ++n) {
+        const double p = has_priors ? config->priors[n] : 1.0;
+        if (!std::isfinite(p)) {
+          fail(QB_INVALID_ARGUMENT,
+               "DecoderConfig: prior at variable " + std::to_string(n) + " is not finite");
+        }
+        const int32_t qv = quantize_saturate(p, scale, kmax);
+        if (qv == 0) {
+          fail(QB_INVALID_ARGUMENT, "DecoderConfig: prior at variable " + std::to_string(n) +
+                                        " quantizes to 0 and would make the decoder inert; "
+                                        "increase quant_scale");
+        }
+        gamma_i[n] = qv;
+      }
+    } else {
+      gamma_f.resize(N);
+      for (uint32_t n = 0; n < N; ++n) {
+        const double p = has_priors ? config->priors[n] : 1.0;
+        if (!std::isfinite(p)) {
+          fail(QB_INVALID_ARGUMENT,
+               "DecoderConfig: prior at variable " + std::to_string(n) + " is not finite");
+        }
+        gamma_f[n] = static_cast<float>(p);
+      }
+    }
+
+    // ---- segments (decoder.cpp:406-424)
+    std::vector<qb_segment> segs;
+    if (segments == nullptr || num_segments == 0) {
+      segs.push_back({0, M, 0, N});
+    } else {
+      segs.assign(segments, segments + num_segments);
+    }
+    if (segs.size() > static_cast<size_t>(kMaxSegments)) {
+      fail(QB_INVALID_ARGUMENT, "at most " + std::to_string(kMaxSegments) + " segments");
+    }
+    std::vector<uint32_t> edge_check(E);
+    for (uint32_t m = 0; m < M; ++m) {
+      for (uint32_t e = graph->check_offsets[m]; e < graph->check_offsets[m + 1]; ++e) {
+        edge_check[e] = m;
+      }
+    }
+    uint32_t next_c = 0, next_v = 0;
+    for (const qb_segment& s : segs) {
+      if (s.check_begin != next_c || s.var_begin != next_v || s.check_end <= s.check_begin ||
+          s.var_end <= s.var_begin || s.check_end > M || s.var_end > N) {
+        fail(QB_INVALID_ARGUMENT, "segments must tile the checks and variables in order");
+      }
+      for (uint32_t e = graph->check_offsets[s.check_begin];
+           e < graph->check_offsets[s.check_end]; ++e) {
+        const uint32_t v = graph->edge_var[e];
+        if (v < s.var_begin || v >= s.var_end) {
+          fail(QB_INVALID_ARGUMENT, "segments are not block-diagonal: an edge leaves its block");
+        }
+      }
+      next_c = s.check_end;
+      next_v = s.var_end;
+    }
+    if (next_c != M || next_v != N) {
+      fail(QB_INVALID_ARGUMENT, "segments must cover every check and variable");
+    }
+
+    // ---- device
+    CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    h = new qb_decoder();
+    h->device = device;
+    h->sm_count = prop.multiProcessorCount;
+    h->max_smem_optin = static_cast<int>(prop.sharedMemPerBlockOptin);
+    h->arith = arith;
+    int lo = 0, hi = 0;
+    CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUDA_TRY(cudaStreamCreateWithPriority(&h->stream, cudaStreamNonBlocking, hi));
+
+    DecodeParams& P = h->P;
+    P.M = M;
+    P.N = N;
+    P.E = E;
+    P.nseg = static_cast<uint32_t>(segs.size());
+    P.syn_w32 = 2 * ((M + 63) / 64);
+    P.est_w32 = 2 * ((N + 63) / 64);
+    P.max_iter = static_cast<uint32_t>(config->max_iterations);
+    P.early = config->early_termination ? 1 : 0;
+    P.alpha = config->alpha;
+    P.alpha_f = static_cast<float>(config->alpha);
+    P.deg1_f = static_cast<float>(config->alpha * 64.0);
+    P.clamp_f = static_cast<float>(1e30);
+    P.alpha_fx = alpha_fx;
+    P.kmax = kmax;
+    P.deg1_i = kmax ? static_cast<int32_t>((static_cast<int64_t>(kmax) * alpha_fx + 32768) >> 16) : 0;
+    for (size_t s = 0; s < segs.size(); ++s) {
+      P.segs[s] = {segs[s].check_begin, segs[s].check_end, segs[s].var_begin, segs[s].var_end,
+                   graph->check_offsets[segs[s].check_begin],
+                   graph->check_offsets[segs[s].check_end]};
+    }
+
+    auto keep = [&](auto* p) {
+      h->dev_allocs.push_back(const_cast<void*>(static_cast<const void*>(p)));
+      return p;
+    };
+    P.check_off = keep(dev_upload(std::vector<uint32_t>(graph->check_offsets, graph->check_offsets + M + 1)));
+    P.var_off = keep(dev_upload(std::vector<uint32_t>(graph->var_offsets, graph->var_offsets + N + 1)));
+    P.var_edges = keep(dev_upload(std::vector<uint32_t>(graph->var_edges, graph->var_edges + E)));
+    P.edge_var = keep(dev_upload(std::vector<uint32_t>(graph->edge_var, graph->edge_var + E)));
+    P.edge_check = keep(dev_upload(edge_check));
+    P.gamma = gamma_f.empty() ? static_cast<const void*>(keep(dev_upload(gamma_i)))
+                              : static_cast<const void*>(keep(dev_upload(gamma_f)));
+
+    h->smem_bytes = generic_smem_bytes(E, P.syn_w32, P.est_w32, P.nseg, msg_bytes_of(arith));
+    if (h->smem_bytes > static_cast<size_t>(h->max_smem_optin)) {
+      fail(QB_INVALID_ARGUMENT, "graph needs " + std::to_string(h->smem_bytes) +
+                                    " bytes of shared memory per shot; the device offers " +
+                                    std::to_string(h->max_smem_optin));
+    }
+    choose_shape(h);
+
+    CUDA_TRY(cudaMalloc(&h->d_sched, 2 * sizeof(unsigned int)));
+    CUDA_TRY(cudaMemset(h->d_sched, 0, 2 * sizeof(unsigned int)));
+
+    // ---- single-shot staging
+    auto align8 = [](size_t x) { return (x + 7) & ~static_cast<size_t>(7); };
+    h->off_res = align8(P.est_w32 * 4);
+    h->off_conv = h->off_res + align8(P.syn_w32 * 4);
+    h->off_iters = h->off_conv + align8(P.nseg);
+    h->off_ns = h->off_iters + align8(P.nseg * 4);
+    h->off_flag = h->off_ns + 8;
+    h->out_bytes = h->off_flag + 8;
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h->h_in), P.syn_w32 * 4,
+                           cudaHostAllocMapped | cudaHostAllocWriteCombined));
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h->h_out), h->out_bytes, cudaHostAllocMapped));
+    std::memset(h->h_out, 0, h->out_bytes);
+    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_in_map), h->h_in, 0));
+    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_out_map), h->h_out, 0));
+    CUDA_TRY(cudaMalloc(&h->d_in_dev, P.syn_w32 * 4));
+    CUDA_TRY(cudaMalloc(&h->d_out_dev, h->out_bytes));
+    CUDA_TRY(cudaMemset(h->d_out_dev, 0, h->out_bytes));
+    CUDA_TRY(cudaMalloc(&h->d_qdump, static_cast<size_t>(E) * 4));
+    CUDA_TRY(cudaMalloc(&h->d_rdump, static_cast<size_t>(E) * 4));
+    CUDA_TRY(cudaDeviceSynchronize());
+    *out = h;
+  });
+  if (st != QB_OK && h) destroy(h);
+  return st;
+}
+
+void qb_decoder_destroy(qb_decoder* h) { destroy(h); }
+
+qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
+  if (!h) return QB_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    switch (option) {
+      case QB_OPT_KERNEL:
+        if (value < 0 || value > 2) fail(QB_INVALID_ARGUMENT, "QB_OPT_KERNEL: 0, 1 or 2");
+        if (value == 2) fail(QB_INVALID_ARGUMENT, "regular kernel not available for this graph");
+        h->opt_kernel = value;
+        break;
+      case QB_OPT_LATENCY_IO:
+        if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_LATENCY_IO: 0 or 1");
+        h->opt_latency_io = value;
+        break;
+      case QB_OPT_LATENCY_SHAPE:
+        if (value < 0 || value > 2) fail(QB_INVALID_ARGUMENT, "QB_OPT_LATENCY_SHAPE: 0, 1 or 2");
+        h->opt_latency_shape = value;
+        break;
+      case QB_OPT_GROUP_THREADS:
+        if (value < 0 || value > 1024) fail(QB_INVALID_ARGUMENT, "QB_OPT_GROUP_THREADS: 0..1024");
+        h->opt_group_threads = value;
+        choose_shape(h);
+        break;
+      case QB_OPT_BATCH_CTAS_PER_SM:
+        if (value < 0 || value > 32) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_CTAS_PER_SM: 0..32");
+        h->opt_batch_ctas = value;
+        break;
+      default:
+        fail(QB_INVALID_ARGUMENT, "unknown option");
+    }
+  });
+}
+
+int64_t qb_get_option(const qb_decoder* h, int option) {
+  if (!h) return -1;
+  switch (option) {
+    case QB_OPT_KERNEL: return h->opt_kernel;
+    case QB_OPT_LATENCY_IO: return h->opt_latency_io;
+    case QB_OPT_LATENCY_SHAPE: return h->opt_latency_shape;
+    case QB_OPT_GROUP_THREADS: return h->P.group_threads;
+    case QB_OPT_BATCH_CTAS_PER_SM: return h->opt_batch_ctas;
+    default: return -1;
+  }
+}
+
+uint32_t qb_num_checks(const qb_decoder* h) { return h ? h->P.M : 0; }
+uint32_t qb_num_vars(const qb_decoder* h) { return h ? h->P.N : 0; }
+uint32_t qb_num_segments(const qb_decoder* h) { return h ? h->P.nseg : 0; }
+uint64_t qb_last_kernel_ns(const qb_decoder* h) { return h ? h->last_kernel_ns : 0; }
+uint64_t qb_launch_count(const qb_decoder* h) { return h ? h->launches : 0; }
+
+qb_status qb_decode(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate,
+                    uint64_t* residual, uint8_t* converged, uint32_t* iterations) {
+  if (!h) return QB_INVALID_ARGUMENT;
+  return guarded(h, [&] { single_shot(h, syndrome, estimate, residual, converged, iterations, false); });
+}
+
+qb_status qb_decode_debug(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate,
+                          uint64_t* residual, uint8_t* converged, uint32_t* iterations,
+                          float* q_f32, float* r_f32, int32_t* q_i32, int32_t* r_i32) {
+  if (!h) return QB_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    single_shot(h, syndrome, estimate, residual, converged, iterations, true);
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    const size_t bytes = static_cast<size_t>(h->P.E) * 4;
+    const bool is_int = h->arith == QB_ARITH_INT8 || h->arith == QB_ARITH_INT16;
+    void* qdst = is_int ? static_cast<void*>(q_i32) : static_cast<void*>(q_f32);
+    void* rdst = is_int ? static_cast<void*>(r_i32) : static_cast<void*>(r_f32);
+    if (!qdst || !rdst) fail(QB_INVALID_ARGUMENT, "decode_debug: message buffers of the wrong type");
+    CUDA_TRY(cudaMemcpy(qdst, h->d_qdump, bytes, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(rdst, h->d_rdump, bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
+qb_status qb_decode_batch_device(qb_decoder* h, uint64_t shots, const uint64_t* d_syndromes,
+                                 uint64_t* d_estimates, uint64_t* d_residuals,
+                                 uint8_t* d_converged, uint32_t* d_iterations, void* stream) {
+  if (!h) return QB_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    if (shots == 0) return;
+    if (!d_syndromes || !d_estimates || !d_converged || !d_iterations) {
+      fail(QB_INVALID_ARGUMENT, "decode_batch_device: NULL buffer");
+    }
+    run_batch_device(h, shots, reinterpret_cast<const uint32_t*>(d_syndromes),
+                     reinterpret_cast<uint32_t*>(d_estimates),
+                     reinterpret_cast<uint32_t*>(d_residuals), d_converged, d_iterations,
+                     static_cast<cudaStream_t>(stream));
+  });
+}
+
+qb_status qb_decode_batch(qb_decoder* h, uint64_t shots, const uint64_t* syndromes,
+                          uint64_t* estimates, uint64_t* residuals, uint8_t* converged,
+                          uint32_t* iterations) {
+  if (!h) return QB_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    if (shots == 0) return;
+    if (!syndromes || !estimates || !converged || !iterations) {
+      fail(QB_INVALID_ARGUMENT, "decode_batch: NULL buffer");
+    }
+    const DecodeParams& P = h->P;
+    // Chunked so that H2D of chunk i+1, the kernel of chunk i and D2H of
+    // chunk i-1 overlap when the host buffers are pinned.
+    const uint64_t kMaxChunk = 1ull << 18;
+    const uint64_t chunk = std::min<uint64_t>(shots, kMaxChunk);
+    ensure_batch(h, chunk * 2, residuals != nullptr);
+    cudaStream_t st = h->stream;
+    uint64_t done = 0;
+    int slot = 0;
+    cudaEvent_t ev[2];
+    CUDA_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    bool used[2] = {false, false};
+    try {
+      while (done < shots) {
+        const uint64_t n = std::min<uint64_t>(chunk, shots - done);
+        const uint64_t off = static_cast<uint64_t>(slot) * chunk;
+        if (used[slot]) CUDA_TRY(cudaEventSynchronize(ev[slot]));
+        uint32_t* d_syn = h->b_syn + off * P.syn_w32;
+        uint32_t* d_est = h->b_est + off * P.est_w32;
+        uint32_t* d_res = h->b_res + off * P.syn_w32;
+        uint8_t* d_conv = h->b_conv + off * P.nseg;
+        uint32_t* d_it = h->b_iters + off * P.nseg;
+        CUDA_TRY(cudaMemcpyAsync(d_syn, reinterpret_cast<const uint32_t*>(syndromes) + done * P.syn_w32,
+                                 n * P.syn_w32 * 4, cudaMemcpyHostToDevice, st));
+        run_batch_device(h, n, d_syn, d_est, residuals ? d_res : nullptr, d_conv, d_it, st);
+        CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(estimates) + done * P.est_w32, d_est,
+                                 n * P.est_w32 * 4, cudaMemcpyDeviceToHost, st));
+        if (residuals) {
+          CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(residuals) + done * P.syn_w32, d_res,
+                                   n * P.syn_w32 * 4, cudaMemcpyDeviceToHost, st));
+        }
+        CUDA_TRY(cudaMemcpyAsync(converged + done * P.nseg, d_conv, n * P.nseg,
+                                 cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(iterations + done * P.nseg, d_it, n * P.nseg * 4,
+                                 cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaEventRecord(ev[slot], st));
+        used[slot] = true;
+        slot ^= 1;
+        done += n;
+      }
+      CUDA_TRY(cudaStreamSynchronize(st));
+    } catch (...) {
+      cudaEventDestroy(ev[0]);
+      cudaEventDestroy(ev[1]);
+      throw;
+    }
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,283 @@
+"""GPU parity tests proper: the CUDA path (through the C-ABI) against the CPU
+oracle and — where the prebuilt library travelled — the compiled reference, on
+identical graphs, priors and syndromes.  Bit-exact for every mode the reference
+has (float, int8, int16); structure follows proj/tests/test_decoder.cpp and
+proj/tests/test_quantized.cpp.
+"""
+import numpy as np
+import pytest
+
+from paper_2508_07879_b200 import (Decoder, DecoderConfig, codes, decode, decode_batch,
+                                   decode_css, gf2)
+from tests.helpers import (error_syndromes, random_ldpc_matrix, random_syndrome,
+                           random_syndromes)
+
+pytestmark = pytest.mark.gpu
+
+REF_MODES = ("float", "int8", "int16")
+
+
+def assert_matches_oracle(oracle, graph, cfg, syndromes, segments=None, dec=None, messages=False):
+    """CUDA (single-shot path) == oracle on every syndrome: estimate, residual,
+    per-segment converged and iterations; optionally the edge messages."""
+    own = dec is None
+    dec = dec or Decoder(graph, cfg, segments=segments)
+    try:
+        for s in syndromes:
+            oe, ores, oc, oi, oq, orr = oracle.decode(graph, cfg, s, segments)
+            if messages:
+                e, r, c, i, q, rr = dec.decode_debug(s)
+            else:
+                e, r, c, i = dec.decode_segments(s)
+            assert np.array_equal(e, oe), "estimate differs"
+            assert np.array_equal(r, ores), "residual differs"
+            assert np.array_equal(c, oc), "converged differs"
+            assert np.array_equal(i, oi), "iterations differ"
+            if messages:
+                # q is defined by the last VN stage in both; r likewise by the last CN stage
+                assert np.array_equal(q.view(np.uint32) if q.dtype == np.float32 else q,
+                                      oq.view(np.uint32) if oq.dtype == np.float32 else oq), "q differs"
+                assert np.array_equal(rr.view(np.uint32) if rr.dtype == np.float32 else rr,
+                                      orr.view(np.uint32) if orr.dtype == np.float32 else orr), "r differs"
+    finally:
+        if own:
+            dec.close()
+
+
+def test_device_is_blackwell(gpu_lib):
+    assert gpu_lib["cc"][0] >= 10, gpu_lib
+    assert gpu_lib["sms"] > 0
+
+
+@pytest.mark.parametrize("mode", REF_MODES + ("half",))
+def test_zero_syndrome_is_a_one_iteration_fixed_point(mode):
+    """proj/tests/test_decoder.cpp:247-267, test_quantized.cpp:206-220."""
+    for name in ("bb72", "bb108", "bb144", "bb288", "bb756", "bb784"):
+        code = codes.make_code(name)
+        g = code.combined_graph
+        zero = np.zeros(gf2.num_words(g.num_checks), dtype=np.uint64)
+        cfg = DecoderConfig(arithmetic=mode)
+        out = decode(g, zero, cfg)
+        assert out.converged and out.iterations_used == 1
+        assert not out.error_estimate.any() and not out.syndrome_residual.any()
+        cfg.early_termination = False
+        out = decode(g, zero, cfg)
+        assert out.converged and out.iterations_used == cfg.max_iterations
+        assert not out.error_estimate.any()
+
+
+@pytest.mark.parametrize("mode", REF_MODES)
+def test_toy_code_every_syndrome(oracle, mode):
+    """proj/tests/test_decoder.cpp:269-294 and :417-424: converged iff s == 0,
+    iterations 1 or 10 (period-2 oscillation), and bit-exact with the oracle
+    including every edge message."""
+    h = codes.toy_code_3x6()
+    g = codes.build_tanner_graph(h)
+    cfg = DecoderConfig(alpha=0.8, max_iterations=10, arithmetic=mode)
+    syndromes = [gf2.pack_bits(np.array([(mask >> m) & 1 for m in range(3)], dtype=np.uint8))
+                 for mask in range(8)]
+    with Decoder(g, cfg) as dec:
+        for mask, s in enumerate(syndromes):
+            out = dec.decode(s)
+            est_bits = gf2.unpack_bits(out.error_estimate, 6)
+            hs = h.mat_vec(est_bits)
+            assert np.array_equal(gf2.unpack_bits(out.syndrome_residual, 3),
+                                  hs ^ gf2.unpack_bits(s, 3))
+            if mode == "float":
+                assert out.converged == (mask == 0)
+                assert out.iterations_used == (1 if mask == 0 else 10)
+        assert_matches_oracle(oracle, g, cfg, syndromes, dec=dec, messages=True)
+
+
+@pytest.mark.parametrize("mode", REF_MODES)
+def test_bb72_x_graph_matches_oracle_bit_for_bit(oracle, mode):
+    """proj/tests/test_decoder.cpp:426-434 / test_quantized.cpp:250-258."""
+    code = codes.make_code("bb72")
+    rng = np.random.default_rng(71)
+    for trial in range(25):
+        cfg = DecoderConfig(alpha=0.8, max_iterations=10, early_termination=trial % 2 == 0,
+                            arithmetic=mode)
+        s = random_syndrome(rng, code.hz.rows, 0.1)
+        assert_matches_oracle(oracle, code.graph_x, cfg, [s], messages=True)
+
+
+@pytest.mark.parametrize("mode", REF_MODES)
+def test_irregular_graphs_with_unit_degrees(oracle, mode):
+    """proj/tests/test_decoder.cpp:436-447: degree-1 checks and variables."""
+    rng = np.random.default_rng(5)
+    for _ in range(10):
+        h = random_ldpc_matrix(rng, 6 + int(rng.integers(0, 6)), 10 + int(rng.integers(0, 8)))
+        g = codes.build_tanner_graph(h)
+        for trial in range(10):
+            cfg = DecoderConfig(alpha=0.8, max_iterations=10, early_termination=trial % 2 == 0,
+                                arithmetic=mode)
+            s = random_syndrome(rng, g.num_checks, 0.3)
+            assert_matches_oracle(oracle, g, cfg, [s], messages=True)
+
+
+def test_non_uniform_priors(oracle):
+    """proj/tests/test_decoder.cpp:449-458."""
+    g = codes.build_tanner_graph(codes.toy_code_3x6())
+    cfg = DecoderConfig(alpha=0.8, max_iterations=10, priors=[0.5, 1.25, 2.0, 0.75, 3.0, 1.5])
+    syndromes = [gf2.pack_bits(np.array([(mask >> m) & 1 for m in range(3)], dtype=np.uint8))
+                 for mask in range(8)]
+    assert_matches_oracle(oracle, g, cfg, syndromes, messages=True)
+    # negative and zero priors take the same code path in the reference
+    cfg.priors = [-0.5, 0.0, 2.0, -0.75, 3.0, 1e-3]
+    assert_matches_oracle(oracle, g, cfg, syndromes, messages=True)
+
+
+@pytest.mark.parametrize("mode", ("int8", "int16"))
+def test_saturating_priors(oracle, mode):
+    """proj/tests/test_quantized.cpp:272-283."""
+    g = codes.build_tanner_graph(codes.toy_code_3x6())
+    cfg = DecoderConfig(alpha=0.8, max_iterations=10, arithmetic=mode, quant_scale=16.0,
+                        priors=[20.0, 1.0, -2.0, 500.0, 0.25, 1.0])
+    syndromes = [gf2.pack_bits(np.array([(mask >> m) & 1 for m in range(3)], dtype=np.uint8))
+                 for mask in range(8)]
+    assert_matches_oracle(oracle, g, cfg, syndromes, messages=True)
+
+
+def test_validation_errors():
+    """proj/tests/test_decoder.cpp:296-326, test_quantized.cpp:185-204."""
+    g = codes.build_tanner_graph(codes.toy_code_3x6())
+    for bad in (dict(alpha=0.0), dict(alpha=1.25), dict(max_iterations=0),
+                dict(priors=[1.0, 2.0]),
+                dict(priors=[1.0, 1.0, 1.0, float("inf"), 1.0, 1.0]),
+                dict(arithmetic="int8", quant_scale=0.3),
+                dict(arithmetic="int16", alpha=1e-6),
+                dict(arithmetic="int8", quant_scale=-4.0)):
+        with pytest.raises(ValueError):
+            Decoder(g, DecoderConfig(**bad))
+    with pytest.raises(ValueError, match="quantizes to 0"):
+        Decoder(g, DecoderConfig(arithmetic="int8", quant_scale=0.3))
+    code = codes.make_code("bb72")
+    with Decoder(code.graph_x, DecoderConfig()) as dec:
+        with pytest.raises(ValueError):
+            dec.decode(np.zeros(1, dtype=np.uint64), bits=35)
+        with pytest.raises(ValueError):
+            dec.decode_css_into(np.zeros(1, dtype=np.uint64), np.zeros(1, dtype=np.uint64))
+    with pytest.raises(ValueError):
+        decode(code.graph_x, np.zeros(2, dtype=np.uint64), DecoderConfig(), bits=72)
+
+
+def test_decoder_instances_are_reusable():
+    """proj/tests/test_decoder.cpp:328-339."""
+    code = codes.make_code("bb72")
+    rng = np.random.default_rng(3)
+    with Decoder(code.graph_x, DecoderConfig()) as dec:
+        s = random_syndrome(rng, code.hz.rows, 0.1)
+        first = dec.decode(s)
+        dec.decode(random_syndrome(rng, code.hz.rows, 0.4))
+        again = dec.decode(s)
+        assert first.same_as(again)
+
+
+@pytest.mark.parametrize("mode", REF_MODES)
+def test_batch_equals_sequential_map(oracle, mode):
+    """proj/tests/test_decoder.cpp:341-377, test_quantized.cpp:285-301."""
+    code = codes.make_code("bb72")
+    cfg = DecoderConfig(alpha=0.8, arithmetic=mode)
+    rng = np.random.default_rng(29)
+    syndromes = [random_syndrome(rng, code.hz.rows, 0.08) for _ in range(64)]
+    batch = decode_batch(code.graph_x, syndromes, cfg, 1)
+    assert len(batch) == 64
+    with Decoder(code.graph_x, cfg) as dec:
+        for s, b in zip(syndromes, batch):
+            assert b.same_as(dec.decode(s))
+    for workers in (2, 8):
+        again = decode_batch(code.graph_x, syndromes, cfg, workers)
+        assert all(a.same_as(b) for a, b in zip(again, batch))
+    assert decode_batch(code.graph_x, [], cfg, 4) == []
+    bad = list(syndromes)
+    bad[7] = np.zeros(1, dtype=np.uint64)
+    with pytest.raises(ValueError):
+        decode_batch(code.graph_x, bad, cfg, 2, bits=[36] * 7 + [5] + [36] * 56)
+    oe, ores, oc, oi = oracle.decode_many(code.graph_x, cfg, np.stack(syndromes))
+    for k, b in enumerate(batch):
+        assert np.array_equal(b.error_estimate, oe[k]) and b.iterations_used == oi[k, 0]
+        assert b.converged == bool(oc[k, 0]) and np.array_equal(b.syndrome_residual, ores[k])
+
+
+@pytest.mark.parametrize("mode", REF_MODES)
+def test_combined_decode_equals_two_separate_decodes(mode):
+    """proj/tests/test_decoder.cpp:379-405, test_quantized.cpp:303-320."""
+    for name in ("bb72", "bb144"):
+        code = codes.make_code(name)
+        rng = np.random.default_rng(59)
+        for trial in range(24):
+            cfg = DecoderConfig(alpha=0.8, early_termination=trial % 2 == 0, arithmetic=mode)
+            s_x = random_syndrome(rng, code.hz.rows, 0.06)
+            s_z = random_syndrome(rng, code.hx.rows, 0.06)
+            cx, cz = decode_css(code, s_x, s_z, cfg)
+            assert cx.same_as(decode(code.graph_x, s_x, cfg))
+            assert cz.same_as(decode(code.graph_z, s_z, cfg))
+
+
+@pytest.mark.parametrize("name,mode", [("bb144", "float"), ("bb144", "int8"), ("bb784", "float"),
+                                       ("bb784", "int8"), ("bb784", "int16"), ("bb756", "float")])
+def test_css_batch_matches_oracle(oracle, name, mode):
+    """Combined-graph decode of error-derived syndromes (the bench / campaign
+    workload, proj/src/bench.cpp:203-211) at several error rates, batch path,
+    bit-exact with the oracle per segment."""
+    code = codes.make_code(name)
+    rng = np.random.default_rng(2024)
+    for p, iters, early in ((0.01, 50, True), (0.03, 30, True), (0.02, 10, False)):
+        cfg = DecoderConfig(max_iterations=iters, early_termination=early, arithmetic=mode)
+        _, _, syn = error_syndromes(code, rng, 96, p)
+        with Decoder(code, cfg) as dec:
+            est, res, conv, its = dec.decode_batch_segments(syn)
+            # and the single-shot path agrees with the batch path
+            e1, r1, c1, i1 = dec.decode_segments(syn[5])
+        oe, ores, oc, oi = oracle.decode_many(code.combined_graph, cfg, syn, code.segments)
+        assert np.array_equal(est, oe)
+        assert np.array_equal(res, ores)
+        assert np.array_equal(conv, oc)
+        assert np.array_equal(its, oi)
+        assert np.array_equal(e1, oe[5]) and np.array_equal(r1, ores[5])
+        assert np.array_equal(c1, oc[5]) and np.array_equal(i1, oi[5])
+
+
+def test_against_compiled_reference(ref):
+    """The unmodified reference Decoder (prebuilt oracle/_ref) on its own bench
+    pool recipe: decode_into and decode_css_into outcomes equal ours exactly."""
+    for name in ("bb144", "bb784"):
+        rc = ref.code(name)
+        code = codes.make_code(name)
+        pool = ref.syndrome_pool(rc, 0.02, 1, 128)
+        for mode in REF_MODES:
+            cfg = DecoderConfig(max_iterations=50, arithmetic=mode)
+            rest, rres, rconv, rits = ref.decoder(rc, cfg).decode_many(pool)
+            with Decoder(code, cfg) as dec:
+                est, res, conv, its = dec.decode_batch_segments(pool)
+            assert np.array_equal(est, rest)
+            assert np.array_equal(res, rres)
+            assert np.array_equal(conv.all(axis=1), rconv.astype(bool))
+            assert np.array_equal(its.max(axis=1), rits)
+
+
+def test_large_batch_soundness_properties():
+    """Size-independent properties at scale (proj/tests/acceptance.cpp:56-100):
+    residual == H*e_hat ^ s for every shot, converged <=> residual == 0,
+    iterations within [1, cap], and the batch is reproducible."""
+    code = codes.make_code("bb784")
+    rng = np.random.default_rng(7)
+    shots = 20000
+    _, _, syn = error_syndromes(code, rng, shots, 0.02)
+    cfg = DecoderConfig(max_iterations=30)
+    with Decoder(code, cfg) as dec:
+        est, res, conv, its = dec.decode_batch_segments(syn)
+        est2, res2, conv2, its2 = dec.decode_batch_segments(syn)
+    assert np.array_equal(est, est2) and np.array_equal(res, res2)
+    assert np.array_equal(conv, conv2) and np.array_equal(its, its2)
+    g = code.combined_graph
+    e_bits = gf2.unpack_bits(est, g.num_vars)
+    s_bits = gf2.unpack_bits(syn, g.num_checks)
+    hs = code.combined.mat_vec(e_bits)
+    assert np.array_equal(gf2.unpack_bits(res, g.num_checks), hs ^ s_bits)
+    mz = code.hz.rows
+    rb = gf2.unpack_bits(res, g.num_checks)
+    assert np.array_equal(conv[:, 0].astype(bool), ~rb[:, :mz].any(axis=1))
+    assert np.array_equal(conv[:, 1].astype(bool), ~rb[:, mz:].any(axis=1))
+    assert its.min() >= 1 and its.max() <= 30
+    assert conv.mean() > 0.9
