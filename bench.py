@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: batched min-sum decodes/s and single-shot latency
+at [[784,24,24]] (BASELINE.json), one process per GPU.
+
+    python bench.py --gpus 1 --steps 5 --warmup 3            # our CUDA path
+    python bench.py --impl reference --gpus 1 --steps 3 ...  # reference CPU path
+
+A STEP is one pass of the decoder over one batch of `--shots` synthetic
+syndromes per GPU (bb784 combined X+Z graph, independent-XZ bit-flip noise at
+`--p`, fp32 min-sum, 50-iteration cap with syndrome-match early stop — config 4
+of BASELINE.json at its centre point).  The batch is generated ON the device by
+the library's SplitMix64-exact generator before the timed region, so inputs are
+resident in HBM; input + output of one step (~310 MB at 1 Mi shots) exceed the
+126 MB L2, so no step re-reads a cached batch.
+
+One JSON line is printed by rank 0 (see DESIGN.md §Measurement for every key).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "batched decodes/s at [[784,24,24]] (p50/p99 single-shot latency in `latency_us`)"
+BYTES_PER_EDGE_UPDATE = {"float": 16, "half": 8, "int16": 8, "int8": 4}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--code", default="bb784")
+    ap.add_argument("--shots", type=int, default=1 << 20, help="shots per GPU per step")
+    ap.add_argument("--p", type=float, default=0.01)
+    ap.add_argument("--max-iterations", type=int, default=50)
+    ap.add_argument("--no-early-stop", action="store_true")
+    ap.add_argument("--arithmetic", default="float")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--latency-shots", type=int, default=4000)
+    ap.add_argument("--skip-latency", action="store_true")
+    ap.add_argument("--skip-cpu-baseline", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--ref-shots", type=int, default=1 << 14,
+                    help="--impl reference: shots per step (bounded sample)")
+    return ap.parse_args()
+
+
+def workload_name(args) -> str:
+    stop = "fixed" if args.no_early_stop else "early-stop"
+    return (f"{args.code} combined X+Z graph, {args.arithmetic} min-sum, alpha 0.8, "
+            f"{args.max_iterations}-iteration cap {stop}, independent-XZ p={args.p}")
+
+
+# --------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons with nvidia-smi DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._pump, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(smax)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def nearest_rank(sorted_vals, pct):
+    """reference: percentile_nearest_rank (proj/src/bench.cpp:169-180)."""
+    n = len(sorted_vals)
+    rank = min(max(int(np.ceil(pct / 100.0 * n)), 1), n)
+    return float(sorted_vals[rank - 1])
+
+
+# --------------------------------------------------------------------------- reference arm
+
+def reference_throughput(args, shots_per_step, steps, warmup):
+    """Times the reference's own CPU implementation of the path (oracle/_ref, the
+    unmodified sources compiled in place) with every host thread, on a bounded
+    sample of the same workload; falls back to the C oracle port if the prebuilt
+    library is absent.  Returns (decodes/s, seconds/step, cpu_baseline dict)."""
+    from oracle.pyoracle import Oracle, Ref
+    cores = os.cpu_count() or 1
+    if Ref.available() and args.arithmetic in ("float", "int8", "int16"):
+        ref = Ref()
+        rc = ref.code(args.code)
+        # run_bench's protocol (bench.cpp:182-337): persistent worker pool, one Decoder per
+        # worker, timed region = copy-in + decode + copy-out of one batch.
+        r = ref.run_bench(rc, arithmetic=args.arithmetic, alpha=0.8,
+                          max_iterations=args.max_iterations,
+                          early_termination=not args.no_early_stop, batch=shots_per_step,
+                          threads=0, warmup=warmup, measure=steps, p=args.p, seed=args.seed)
+        per_decode_us = r["mean_us"]
+        return (1e6 / per_decode_us, per_decode_us * shots_per_step * 1e-6,
+                {"value": 1e6 / per_decode_us, "unit": "decodes/s", "cores": int(r["threads"]),
+                 "kind": "reference",
+                 "sample": f"run_bench: {steps} batches of {shots_per_step} shots, "
+                           f"{int(r['threads'])} threads, conv_rate {r['conv_rate']:.4f}",
+                 "host": ref.host_descriptor()})
+    from paper_2508_07879_b200 import DecoderConfig, codes, gf2
+    code = codes.make_code(args.code)
+    rng = np.random.default_rng(args.seed)
+    n = min(shots_per_step, 2048)
+    ex = (rng.random((n, code.n)) < args.p).astype(np.uint8)
+    ez = (rng.random((n, code.n)) < args.p).astype(np.uint8)
+    syn = gf2.pack_bits(np.concatenate([code.hz.mat_vec(ex), code.hx.mat_vec(ez)], axis=-1))
+    cfg = DecoderConfig(max_iterations=args.max_iterations,
+                        early_termination=not args.no_early_stop, arithmetic=args.arithmetic)
+    orc = Oracle()
+    t0 = time.perf_counter()
+    for _ in range(max(steps, 1)):
+        orc.decode_many(code.combined_graph, cfg, syn, code.segments)
+    dt = (time.perf_counter() - t0) / max(steps, 1)
+    return (n / dt, dt, {"value": n / dt, "unit": "decodes/s", "cores": 1, "kind": "port",
+                         "sample": f"C oracle, {n} shots per step, 1 thread"})
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    value, sec_per_step, base = reference_throughput(args, args.ref_shots, args.steps, args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "decodes/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec_per_step * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if args.arithmetic == "float" else args.arithmetic,
+        "data": "synthetic", "config": {"workload": workload_name(args),
+                                        "shots_per_step": args.ref_shots},
+        "cpu_baseline": base,
+        "e2e": {"value": value, "unit": "decodes/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+
+def run_ours(args):
+    import torch
+    from paper_2508_07879_b200 import Decoder, DecoderConfig, _lib, codes, gf2
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise RuntimeError("bench.py needs a CUDA device: there is no CPU fallback")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    code = codes.make_code(args.code)
+    g = code.combined_graph
+    cfg = DecoderConfig(max_iterations=args.max_iterations,
+                        early_termination=not args.no_early_stop, arithmetic=args.arithmetic)
+    dec = Decoder(code, cfg, device=local)
+    lib = _lib.load()
+    shots = args.shots
+    sw, ew, nseg = gf2.num_words(g.num_checks), gf2.num_words(g.num_vars), dec.num_segments
+
+    # ---- resident inputs: generated on the device, trial ids unique across ranks
+    d_syn = torch.zeros((shots, sw), dtype=torch.int64, device=dev)
+    d_err = torch.zeros((shots, ew), dtype=torch.int64, device=dev)
+    d_est = torch.zeros((shots, ew), dtype=torch.int64, device=dev)
+    d_conv = torch.zeros((shots, nseg), dtype=torch.uint8, device=dev)
+    d_its = torch.zeros((shots, nseg), dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream().cuda_stream
+    dec.generate_syndromes(args.seed, args.p, shots, d_syn.data_ptr(), d_err.data_ptr(),
+                           first_trial=rank * shots, stream=stream)
+    torch.cuda.synchronize()
+
+    def step():
+        dec.decode_batch_device(shots, d_syn.data_ptr(), d_est.data_ptr(), None,
+                                d_conv.data_ptr(), d_its.data_ptr(), stream)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
+    launches0 = dec.launch_count()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ev[0].record()
+    for k in range(args.steps):
+        step()
+        ev[k + 1].record()
+    barrier()
+    clocks = sampler.stop() if rank == 0 else None
+    launches = dec.launch_count() - launches0
+    total_ms = ev[0].elapsed_time(ev[-1])
+    kernel_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = world * shots * args.steps / (total_ms * 1e-3)
+
+    # ---- outcome counters: the only data-path collective
+    seg_edges = [int(g.check_offsets[c1] - g.check_offsets[c0]) for c0, c1, _, _ in code.segments]
+    its64 = d_its.to(torch.int64)
+    edge_updates = sum(int(its64[:, s].sum().item()) * seg_edges[s] for s in range(nseg))
+    conv_all = d_conv.min(dim=1).values
+    counters = torch.tensor([shots, int((conv_all == 0).sum().item()),
+                             int(its64.max(dim=1).values.sum().item()), edge_updates],
+                            dtype=torch.int64, device=dev)
+    if dist is not None:
+        dist.all_reduce(counters, op=dist.ReduceOp.SUM)
+    tot_shots, non_conv, iter_sum, edge_updates_all = [int(x) for x in counters.tolist()]
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant (only) kernel in the timed region
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_src = "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback 6650 GB/s"
+    g32, g128 = C.c_double(), C.c_double()
+    st = lib.qb_measure_smem_bandwidth(local, C.byref(g32), C.byref(g128))
+    assert st == 0, lib.qb_last_error(None).decode()
+    bpe = BYTES_PER_EDGE_UPDATE[args.arithmetic]
+    k_ms = float(np.mean(kernel_ms))
+    eu_per_launch = edge_updates / 1.0  # per step on this rank (every step decodes the same batch)
+    smem_achieved = eu_per_launch * bpe / (k_ms * 1e-3) / 1e9
+    hbm_bytes_per_shot = sw * 8 + ew * 8 + nseg + 4 * nseg
+    hbm_achieved = shots * hbm_bytes_per_shot / (k_ms * 1e-3) / 1e9
+    sm_clock = (clocks or {}).get("sm_mhz") or float(peaks.get("sm_max_mhz", 1965.0))
+    roofline = {
+        "bound": "smem", "kernel": "decode_generic_kernel", "achieved": smem_achieved,
+        "peak": g32.value, "unit": "GB/s", "frac": smem_achieved / g32.value,
+        "peak_source": "qb_measure_smem_bandwidth (32-bit conflict-free ld/st stream, this run)",
+        "peak_128bit": g128.value,
+        "peak_theoretical": 148 * 128 * sm_clock * 1e6 / 1e9,
+        "edge_updates_per_s": eu_per_launch / (k_ms * 1e-3),
+        "bytes_per_edge_update": bpe, "kernel_ms": k_ms, "traffic": None,
+        "hbm": {"bound": "hbm", "achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": hbm_achieved / hbm_peak, "peak_source": hbm_src,
+                "bytes_per_shot": hbm_bytes_per_shot, "traffic": None},
+    }
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "decodes/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if args.arithmetic == "float" else args.arithmetic, "data": "synthetic",
+        "config": {"workload": workload_name(args), "shots_per_gpu_per_step": shots,
+                   "l2": "inputs+outputs per step exceed L2 (no flush needed)",
+                   "generator": "on-device SplitMix64 (reference-exact), seed %d" % args.seed},
+        "roofline": roofline, "gpu_launches": int(launches), "clocks": clocks,
+        "outcomes": {"shots": tot_shots, "non_converged": non_conv,
+                     "mean_iterations": iter_sum / max(tot_shots, 1),
+                     "logical_error_rate_nonconv": non_conv / max(tot_shots, 1)},
+    }
+
+    # ---- e2e: the public batch call on HOST (pinned) buffers, copies inside the timed region
+    if not args.skip_e2e:
+        line["e2e"] = measure_e2e(args, dec, lib, d_syn, shots, sw, ew, nseg, world)
+    # ---- single-shot latency (N=1 only)
+    if world == 1 and not args.skip_latency:
+        line["latency_us"] = measure_latency(args, code, lib, d_syn)
+    if world == 1 and not args.skip_cpu_baseline:
+        try:
+            _, _, base = reference_throughput(args, 4096, 40, 2)
+            line["cpu_baseline"] = base
+        except Exception as exc:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "unit": "decodes/s", "cores": 0,
+                                    "kind": "reference", "sample": f"failed: {exc}"}
+    print(json.dumps(line), flush=True)
+    dec.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def measure_e2e(args, dec, lib, d_syn, shots, sw, ew, nseg, world):
+    """qb_decode_batch through pinned host buffers: H2D + kernel + D2H per step."""
+    import torch
+
+    def pinned(nbytes):
+        p = C.c_void_p()
+        assert lib.qb_host_alloc(C.byref(p), nbytes) == 0
+        return p
+
+    n = shots
+    h_syn, h_est = pinned(n * sw * 8), pinned(n * ew * 8)
+    h_conv, h_its = pinned(n * nseg), pinned(n * nseg * 4)
+    # stage the same synthetic batch on the host (outside the timed region)
+    torch.cuda.synchronize()
+    host_syn = d_syn.cpu().numpy()
+    C.memmove(h_syn, host_syn.ctypes.data, n * sw * 8)
+    l0 = dec.launch_count()
+    for _ in range(2):
+        dec.decode_batch_raw(n, h_syn.value, h_est.value, None, h_conv.value, h_its.value)
+    times = []
+    for _ in range(max(args.steps, 3)):
+        t0 = time.perf_counter()
+        dec.decode_batch_raw(n, h_syn.value, h_est.value, None, h_conv.value, h_its.value)
+        times.append(time.perf_counter() - t0)
+    dt = float(np.median(times))
+    out = {"value": world * n / dt, "unit": "decodes/s", "h2d_bytes_per_step": n * sw * 8,
+           "d2h_bytes_per_step": n * (ew * 8 + nseg + 4 * nseg), "ms_per_step": dt * 1e3,
+           "api": "qb_decode_batch (pinned host buffers; H2D, kernel, D2H inside the call)",
+           "timer": "host perf_counter around the blocking call, median of %d" % len(times),
+           "gpu_launches_per_step": (dec.launch_count() - l0) // (2 + len(times))}
+    for p in (h_syn, h_est, h_conv, h_its):
+        lib.qb_host_free(p)
+    return out
+
+
+def measure_latency(args, code, lib, d_syn):
+    """Single-shot decode latency through qb_decode (host buffers in, host buffers
+    out), per the reference protocol: pool of 256 syndromes, 10 iterations fixed
+    (bench.hpp:20-28) and the 50-iteration early-stop variant; nearest-rank
+    percentiles (bench.cpp:169-180)."""
+    from paper_2508_07879_b200 import Decoder, DecoderConfig
+    pool = d_syn[:256].cpu().numpy().astype(np.uint64)
+    out = {}
+    for label, iters, early in (("fixed10", 10, False), ("cap50_early", 50, True)):
+        cfg = DecoderConfig(max_iterations=iters, early_termination=early,
+                            arithmetic=args.arithmetic)
+        with Decoder(code, cfg) as dec:
+            for io_mode, io_name in ((0, "mapped"), (1, "memcpy")):
+                dec.set_option(1, io_mode)
+                wall, kern, digest = dec.latency_run(pool, 300, args.latency_shots)
+                wall = np.sort(wall.astype(np.float64) * 1e-3)
+                kern = np.sort(kern.astype(np.float64) * 1e-3)
+                out[f"{label}_{io_name}"] = {
+                    "p50": nearest_rank(wall, 50), "p99": nearest_rank(wall, 99),
+                    "mean": float(np.mean(wall)), "min": float(wall[0]), "max": float(wall[-1]),
+                    "kernel_p50": nearest_rank(kern, 50), "kernel_p99": nearest_rank(kern, 99),
+                    "shots": args.latency_shots, "digest": "%016x" % digest}
+    out["note"] = ("wall = host steady_clock around the whole qb_decode (copy-in, launch, "
+                   "completion, copy-out) inside qb_latency_run; kernel = in-kernel %globaltimer "
+                   "span; mapped = zero-copy pinned I/O + completion flag, memcpy = "
+                   "cudaMemcpyAsync H2D / kernel / D2H + stream sync (paper protocol)")
+    return out
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

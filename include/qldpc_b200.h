@@ -157,6 +157,20 @@ qb_status qb_decode_debug(qb_decoder* h, const uint64_t* syndrome,
                           float* q_f32, float* r_f32, int32_t* q_i32,
                           int32_t* r_i32);
 
+/* Latency harness with the reference's run_bench protocol at batch 1
+ * (proj/src/bench.cpp:182-337): decode pool[(b) % pool_size] for b in
+ * [0, warmup + measure); for each measured decode record the host wall-clock
+ * nanoseconds of the whole qb_decode (copy-in, launch, completion, copy-out)
+ * in wall_ns[measure] and the device %globaltimer span in kernel_ns[measure]
+ * (either may be NULL).  *digest receives the reference's FNV-1a output digest
+ * (bench.cpp:27-36, :287-291) over (converged AND, iterations MAX as uint64,
+ * estimate words) of the measured decodes, so a GPU run can be compared with
+ * BenchResult::output_digest of the CPU reference. */
+qb_status qb_latency_run(qb_decoder* h, const uint64_t* pool,
+                         uint64_t pool_size, uint64_t warmup, uint64_t measure,
+                         uint64_t* wall_ns, uint64_t* kernel_ns,
+                         uint64_t* digest);
+
 /* Decoder::last_kernel_ns (decoder.cpp:593-596): device-side %globaltimer
  * span of the most recent qb_decode (first instruction to last store). */
 uint64_t qb_last_kernel_ns(const qb_decoder* h);
@@ -164,9 +178,33 @@ uint64_t qb_last_kernel_ns(const qb_decoder* h);
 /* Number of kernels this handle has launched since creation. */
 uint64_t qb_launch_count(const qb_decoder* h);
 
+/* On-device code-capacity noise + syndrome generator (reference:
+ * sample_error + extract_syndromes, proj/src/noise.cpp:67-105), bit-exact
+ * with the reference's SplitMix64 streams: shot i of the call is trial
+ * `first_trial + i` of NoiseModel{independent-xz, p, seed}.  Each variable of
+ * the decoder's graph flips with probability `p` (or `probs[v]`, a HOST array
+ * of num_vars doubles, when non-NULL); the syndrome H*e is written packed to
+ * DEVICE memory `d_syndromes` ([shots][ceil(M/64)] words) and, if non-NULL, the
+ * sampled error to `d_errors` ([shots][ceil(N/64)] words).
+ * `css_interleave` = 1 maps the variables of a two-segment CSS decoder onto
+ * the reference's draw order (X_0, Z_0, X_1, Z_1, ...); 0 uses draw v for
+ * variable v. */
+qb_status qb_generate_syndromes(qb_decoder* h, uint64_t seed, double p,
+                                const double* probs, int css_interleave,
+                                uint64_t first_trial, uint64_t shots,
+                                uint64_t* d_syndromes, uint64_t* d_errors,
+                                void* stream);
+
 /* Pinned (page-locked, device-mapped) host memory for batch I/O. */
 qb_status qb_host_alloc(void** out, size_t bytes);
 void qb_host_free(void* p);
+
+/* Measures the device's aggregate shared-memory bandwidth (GB/s) with a
+ * conflict-free streaming 50/50 load/store kernel on every SM: `gbs_32bit` with
+ * 32-bit accesses (the message arrays' access width), `gbs_128bit` with 128-bit
+ * accesses (the crossbar ceiling).  Used as the roofline denominator. */
+qb_status qb_measure_smem_bandwidth(int device, double* gbs_32bit,
+                                    double* gbs_128bit);
 
 /* Library / device description, e.g. for bench logs. */
 const char* qb_version(void);

@@ -17,7 +17,6 @@ ARITH = {"float": 0, "int8": 1, "int16": 2, "half": 3}
 ARITH_NAMES = {v: k for k, v in ARITH.items()}
 
 OPT_KERNEL, OPT_LATENCY_IO, OPT_LATENCY_SHAPE, OPT_GROUP_THREADS, OPT_BATCH_CTAS_PER_SM = range(5)
-OPT_PIPELINE_STREAMS = 5
 
 u32p = C.POINTER(C.c_uint32)
 u64p = C.POINTER(C.c_uint64)
@@ -50,6 +49,7 @@ SYMBOLS = {
     "qb_last_error": (C.c_char_p, [C.c_void_p]),
     "qb_device_info": (C.c_int, [C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_int),
                                  C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "qb_measure_smem_bandwidth": (C.c_int, [C.c_int, f64p, f64p]),
     "qb_host_alloc": (C.c_int, [C.POINTER(C.c_void_p), C.c_size_t]),
     "qb_host_free": (None, [C.c_void_p]),
     "qb_decoder_create": (C.c_int, [C.POINTER(QbGraph), C.POINTER(QbSegment), C.c_uint32,
@@ -67,6 +67,11 @@ SYMBOLS = {
                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "qb_decode_debug": (C.c_int, [C.c_void_p, u64p, u64p, u64p, u8p, u32p, f32p, f32p, i32p,
                                   i32p]),
+    "qb_generate_syndromes": (C.c_int, [C.c_void_p, C.c_uint64, C.c_double, f64p, C.c_int,
+                                        C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
+                                        C.c_void_p]),
+    "qb_latency_run": (C.c_int, [C.c_void_p, u64p, C.c_uint64, C.c_uint64, C.c_uint64, u64p,
+                                 u64p, u64p]),
     "qb_last_kernel_ns": (C.c_uint64, [C.c_void_p]),
     "qb_launch_count": (C.c_uint64, [C.c_void_p]),
 }

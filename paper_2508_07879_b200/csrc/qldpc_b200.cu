@@ -19,6 +19,8 @@
 
 #include "common.cuh"
 #include "kernel_generic.cuh"
+#include "kernel_noise.cuh"
+#include "kernel_bw.cuh"
 
 using namespace qb;
 
@@ -101,6 +103,7 @@ struct qb_decoder {
   uint8_t* b_conv = nullptr;
   // debug dumps
   void *d_qdump = nullptr, *d_rdump = nullptr;
+  double* d_probs = nullptr;  // per-variable flip probabilities of the noise generator
 
   // options
   int64_t opt_kernel = 0, opt_latency_io = 0, opt_latency_shape = 0, opt_group_threads = 0,
@@ -134,6 +137,7 @@ void destroy(qb_decoder* h) {
   cudaFree(h->d_out_dev);
   cudaFree(h->d_qdump);
   cudaFree(h->d_rdump);
+  cudaFree(h->d_probs);
   if (h->h_in) cudaFreeHost(h->h_in);
   if (h->h_out) cudaFreeHost(h->h_out);
   free_batch(h);
@@ -409,6 +413,45 @@ qb_status qb_device_info(int device, char* name, size_t name_len, int* sm_count,
   });
 }
 
+qb_status qb_measure_smem_bandwidth(int device, double* gbs_32bit, double* gbs_128bit) {
+  return guarded(nullptr, [&] {
+    CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    float* sink = nullptr;
+    CUDA_TRY(cudaMalloc(&sink, sizeof(float)));
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    const size_t smem = kBwWords * sizeof(float);
+    const unsigned grid = static_cast<unsigned>(prop.multiProcessorCount);
+    const uint32_t iters = 4000;
+    auto run = [&](auto kern) {
+      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+      double best = 0.0;
+      for (int rep = 0; rep < 5; ++rep) {
+        CUDA_TRY(cudaEventRecord(e0));
+        kern<<<grid, kBwThreads, smem>>>(iters, sink);
+        CUDA_TRY(cudaEventRecord(e1));
+        CUDA_TRY(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+        const double bytes = 2.0 * smem * static_cast<double>(iters) * grid;  // load + store
+        best = std::max(best, bytes / (ms * 1e-3) / 1e9);
+      }
+      return best;
+    };
+    const double g32 = run(smem_bandwidth_kernel<1>);
+    const double g128 = run(smem_bandwidth_kernel<4>);
+    if (gbs_32bit) *gbs_32bit = g32;
+    if (gbs_128bit) *gbs_128bit = g128;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+  });
+}
+
 qb_status qb_host_alloc(void** out, size_t bytes) {
   return guarded(nullptr, [&] {
     if (!out) fail(QB_INVALID_ARGUMENT, "qb_host_alloc: NULL out");
@@ -665,6 +708,51 @@ qb_status qb_decode(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate,
   return guarded(h, [&] { single_shot(h, syndrome, estimate, residual, converged, iterations, false); });
 }
 
+qb_status qb_latency_run(qb_decoder* h, const uint64_t* pool, uint64_t pool_size,
+                         uint64_t warmup, uint64_t measure, uint64_t* wall_ns,
+                         uint64_t* kernel_ns, uint64_t* digest) {
+  if (!h) return QB_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    if (!pool || pool_size == 0) fail(QB_INVALID_ARGUMENT, "latency_run: empty pool");
+    const DecodeParams& P = h->P;
+    const size_t sw = P.syn_w32 / 2, ew = P.est_w32 / 2;
+    std::vector<uint64_t> est(ew), res(sw);
+    std::vector<uint8_t> conv(P.nseg);
+    std::vector<uint32_t> its(P.nseg);
+    uint64_t hsh = 14695981039346656037ull;  // FNV-1a (bench.cpp:27-36)
+    auto mix = [&](const void* data, size_t len) {
+      const unsigned char* b = static_cast<const unsigned char*>(data);
+      for (size_t i = 0; i < len; ++i) {
+        hsh ^= b[i];
+        hsh *= 1099511628211ull;
+      }
+    };
+    for (uint64_t b = 0; b < warmup + measure; ++b) {
+      const uint64_t* syn = pool + (b % pool_size) * sw;
+      const auto t0 = std::chrono::steady_clock::now();
+      single_shot(h, syn, est.data(), res.data(), conv.data(), its.data(), false);
+      const auto t1 = std::chrono::steady_clock::now();
+      if (b < warmup) continue;
+      const uint64_t k = b - warmup;
+      if (wall_ns) {
+        wall_ns[k] = static_cast<uint64_t>(
+            std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count());
+      }
+      if (kernel_ns) kernel_ns[k] = h->last_kernel_ns;
+      unsigned char c = 1;
+      uint64_t it = 0;
+      for (uint32_t s = 0; s < P.nseg; ++s) {
+        c = c && conv[s];
+        it = std::max<uint64_t>(it, its[s]);
+      }
+      mix(&c, 1);
+      mix(&it, sizeof(it));
+      mix(est.data(), ew * sizeof(uint64_t));
+    }
+    if (digest) *digest = hsh;
+  });
+}
+
 qb_status qb_decode_debug(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate,
                           uint64_t* residual, uint8_t* converged, uint32_t* iterations,
                           float* q_f32, float* r_f32, int32_t* q_i32, int32_t* r_i32) {
@@ -695,6 +783,51 @@ qb_status qb_decode_batch_device(qb_decoder* h, uint64_t shots, const uint64_t* 
                      reinterpret_cast<uint32_t*>(d_estimates),
                      reinterpret_cast<uint32_t*>(d_residuals), d_converged, d_iterations,
                      static_cast<cudaStream_t>(stream));
+  });
+}
+
+qb_status qb_generate_syndromes(qb_decoder* h, uint64_t seed, double p, const double* probs,
+                                int css_interleave, uint64_t first_trial, uint64_t shots,
+                                uint64_t* d_syndromes, uint64_t* d_errors, void* stream) {
+  if (!h) return QB_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    if (shots == 0) return;
+    if (!d_syndromes) fail(QB_INVALID_ARGUMENT, "generate_syndromes: NULL output");
+    const DecodeParams& P = h->P;
+    auto check_p = [](double v) {
+      if (!(v >= 0.0 && v <= 1.0)) fail(QB_INVALID_ARGUMENT, "NoiseModel: p must lie in [0, 1]");
+    };
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    NoiseParams np{};
+    np.seed = seed;
+    np.first_trial = first_trial;
+    np.nshots = shots;
+    np.p = p;
+    if (probs) {
+      for (uint32_t v = 0; v < P.N; ++v) check_p(probs[v]);
+      if (!h->d_probs) CUDA_TRY(cudaMalloc(&h->d_probs, sizeof(double) * P.N));
+      CUDA_TRY(cudaMemcpyAsync(h->d_probs, probs, sizeof(double) * P.N, cudaMemcpyHostToDevice, st));
+      np.probs = h->d_probs;
+    } else {
+      check_p(p);
+    }
+    np.mode = css_interleave ? 1u : 0u;
+    if (css_interleave) {
+      if (P.nseg != 2 || P.segs[0].v1 * 2 != P.N) {
+        fail(QB_INVALID_ARGUMENT,
+             "generate_syndromes: css_interleave needs a two-segment decoder over 2n variables");
+      }
+      np.n_qubits = P.segs[0].v1;
+    }
+    np.syn = reinterpret_cast<uint32_t*>(d_syndromes);
+    np.err = reinterpret_cast<uint32_t*>(d_errors);
+    const uint64_t blocks_needed = (shots + kNoiseWarps - 1) / kNoiseWarps;
+    const unsigned grid = static_cast<unsigned>(
+        std::min<uint64_t>(blocks_needed, static_cast<uint64_t>(h->sm_count) * 8));
+    const size_t smem = static_cast<size_t>(kNoiseWarps) * P.est_w32 * 4;
+    noise_syndrome_kernel<<<grid, kNoiseWarps * 32, smem, st>>>(P, np);
+    CUDA_TRY(cudaGetLastError());
+    ++h->launches;
   });
 }
 

@@ -272,6 +272,37 @@ class Decoder:
             _raise(st, self._h)
 
 
+    def latency_run(self, pool: np.ndarray, warmup: int, measure: int):
+        """qb_latency_run: the reference's run_bench protocol at batch 1
+        (proj/src/bench.cpp:182-337) -> (wall_ns[measure], kernel_ns[measure], digest)."""
+        pool = np.ascontiguousarray(pool, dtype=np.uint64)
+        if pool.ndim != 2 or pool.shape[1] != self._sw:
+            raise ValueError(f"latency_run: pool must be (n, {self._sw}) uint64 words")
+        wall = np.zeros(measure, dtype=np.uint64)
+        kern = np.zeros(measure, dtype=np.uint64)
+        digest = C.c_uint64()
+        st = self._lib.qb_latency_run(self._h, _ptr(pool, _lib.u64p), pool.shape[0], warmup,
+                                      measure, _ptr(wall, _lib.u64p), _ptr(kern, _lib.u64p),
+                                      C.byref(digest))
+        if st != _lib.QB_OK:
+            _raise(st, self._h)
+        return wall, kern, int(digest.value)
+
+    def generate_syndromes(self, seed: int, p: float, shots: int, d_syn: int,
+                           d_err: Optional[int] = None, first_trial: int = 0,
+                           probs: Optional[Sequence[float]] = None, css_interleave: bool = True,
+                           stream: int = 0) -> None:
+        """qb_generate_syndromes: on-device sample_error + extract_syndromes
+        (proj/src/noise.cpp:67-105) into DEVICE buffers, bit-exact with the
+        reference's SplitMix64 streams."""
+        pr = None if probs is None else np.ascontiguousarray(probs, dtype=np.float64)
+        st = self._lib.qb_generate_syndromes(self._h, seed, float(p), _ptr(pr, _lib.f64p),
+                                             1 if css_interleave else 0, first_trial, shots,
+                                             d_syn, d_err, stream)
+        if st != _lib.QB_OK:
+            _raise(st, self._h)
+
+
 # ---- free functions (decoder.hpp:110-129) -----------------------------------
 
 def decode(graph: TannerGraph, syndrome: np.ndarray, cfg: DecoderConfig,
