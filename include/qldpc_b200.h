@@ -96,7 +96,22 @@ typedef enum {
   /* Threads per segment group (0 = auto). */
   QB_OPT_GROUP_THREADS = 3,
   /* CTAs per SM for the persistent batch kernel (0 = auto). */
-  QB_OPT_BATCH_CTAS_PER_SM = 4
+  QB_OPT_BATCH_CTAS_PER_SM = 4,
+  /* Regular kernel: nodes per thread class for the batch / single-shot path:
+   * 1, 2 or 4 checks (and twice as many variables) per thread; 0 = auto. */
+  QB_OPT_BATCH_NODES_PER_THREAD = 5,
+  QB_OPT_LATENCY_NODES_PER_THREAD = 6,
+  /* Regular kernel: 1 (default) lets uniform-prior decoders use the
+   * instantiation with the prior as a kernel constant and (fp32) without the
+   * provably unreachable 1e30 clamp; 0 forces the general instantiation. */
+  QB_OPT_FAST_PATH = 7,
+  /* Read-only (qb_get_option): the launch plans actually in use. */
+  QB_OPT_INFO_BATCH_CTAS_PER_SM = 100,
+  QB_OPT_INFO_BATCH_BLOCK = 101,
+  QB_OPT_INFO_LATENCY_BLOCK = 102,
+  QB_OPT_INFO_LATENCY_CLUSTER = 103,
+  QB_OPT_INFO_BATCH_REGULAR = 104,
+  QB_OPT_INFO_FAST_ELIGIBLE = 105
 } qb_option;
 
 /* Builds a decoder: validates like Decoder::Decoder (decoder.cpp:373-404,

@@ -14,6 +14,7 @@ namespace qb {
 
 constexpr int kMaxSegments = 8;
 constexpr int kWarp = 32;
+constexpr uint32_t kPadEdges = 8;  // message slots of the dummy check (regular kernel)
 
 struct SegmentDev {
   uint32_t c0, c1;  // checks [c0, c1)
@@ -40,6 +41,10 @@ struct DecodeParams {
   uint32_t alpha_fx;  // lround(alpha * 65536)       (decoder.cpp:89)
   int32_t kmax;       // 127 / 32767                 (decoder.cpp:50, :59)
   int32_t deg1_i;     // scale_q16(kmax)             (decoder.cpp:253)
+  // uniform-prior fast path (every gamma equal; fp32 additionally proven clamp-free)
+  double gamma_d;     // (double)float(gamma)
+  float gamma_f;
+  int32_t gamma_i;
   // CSR tables (device global memory, read-only)
   const uint32_t* check_off;   // [M + 1]
   const uint32_t* var_off;     // [N + 1]

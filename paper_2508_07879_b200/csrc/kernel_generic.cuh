@@ -39,23 +39,26 @@ struct GenericSmem {
 __host__ __device__ inline size_t generic_smem_bytes(uint32_t E, uint32_t syn_w32,
                                                      uint32_t est_w32, uint32_t nseg,
                                                      size_t msg_bytes) {
-  size_t msg = (static_cast<size_t>(E) * msg_bytes + 15) & ~static_cast<size_t>(15);
-  return 2 * msg + 4 * (4 * static_cast<size_t>(syn_w32) + est_w32 + 2 * nseg + 4);
+  // kPadEdges extra message slots hold the dummy check/variable that idle thread
+  // slots of the regular kernel work on; 2 spare syndrome words keep bit M addressable.
+  size_t msg = (static_cast<size_t>(E + kPadEdges) * msg_bytes + 15) & ~static_cast<size_t>(15);
+  return 2 * msg + 4 * (4 * static_cast<size_t>(syn_w32) + 2 + est_w32 + 2 * nseg + 4);
 }
 
 template <class A>
 __device__ __forceinline__ GenericSmem<A> carve_generic(unsigned char* base,
                                                         const DecodeParams& P) {
   GenericSmem<A> s;
-  const size_t msg = (static_cast<size_t>(P.E) * sizeof(typename A::Msg) + 15) & ~size_t(15);
+  const size_t msg =
+      (static_cast<size_t>(P.E + kPadEdges) * sizeof(typename A::Msg) + 15) & ~size_t(15);
   s.q = reinterpret_cast<typename A::Msg*>(base);
   s.r = reinterpret_cast<typename A::Msg*>(base + msg);
   uint32_t* w = reinterpret_cast<uint32_t*>(base + 2 * msg);
-  s.syn = w;
-  s.par0 = w + P.syn_w32;
-  s.par1 = w + 2 * P.syn_w32;
-  s.res = w + 3 * P.syn_w32;
-  s.ehat = w + 4 * P.syn_w32;
+  s.syn = w;  // [syn_w32 + 2]
+  s.par0 = w + P.syn_w32 + 2;
+  s.par1 = s.par0 + P.syn_w32;
+  s.res = s.par1 + P.syn_w32;
+  s.ehat = s.res + P.syn_w32;
   s.segres = s.ehat + P.est_w32;
   s.ticket = s.segres + 2 * P.nseg;
   return s;

@@ -19,6 +19,7 @@
 
 #include "common.cuh"
 #include "kernel_generic.cuh"
+#include "kernel_regular.cuh"
 #include "kernel_noise.cuh"
 #include "kernel_bw.cuh"
 
@@ -75,6 +76,20 @@ size_t msg_bytes_of(int arith) {
 
 }  // namespace
 
+using KernelFn = void (*)(DecodeParams, ShotIO);
+
+struct LaunchPlan {
+  KernelFn kernel = nullptr;
+  const char* name = "";
+  bool regular = false;
+  bool cluster = false;
+  int npt = 0;                 // nodes-per-thread class of the regular kernel
+  uint32_t ngroups = 1;
+  uint32_t group_threads = 32;
+  unsigned block = 32;
+  int ctas_per_sm = 1;
+};
+
 struct qb_decoder {
   int device = 0;
   int sm_count = 0;
@@ -107,7 +122,11 @@ struct qb_decoder {
 
   // options
   int64_t opt_kernel = 0, opt_latency_io = 0, opt_latency_shape = 0, opt_group_threads = 0,
-          opt_batch_ctas = 0;
+          opt_batch_ctas = 0, opt_batch_npt = 0, opt_latency_npt = 0;
+  bool regular63 = false;  // every check degree 6, every variable degree 3
+  bool fast_ok = false;    // uniform prior (and, for fp32, provably clamp-free)
+  int64_t opt_fast = 1;
+  LaunchPlan lat, bat;
 
   uint64_t launches = 0;
   std::string err;
@@ -215,63 +234,168 @@ void validate_config_common(const qb_graph* g, const qb_config* c) {
 }
 
 // ---- kernel dispatch ------------------------------------------------------
+//
+// A LaunchPlan names one kernel instantiation plus its launch shape.  Two plans
+// are kept per decoder: `lat` for the single-shot path and `bat` for the
+// persistent batch path.  They are recomputed whenever an option changes.
 
-template <class A>
-void launch_generic_t(qb_decoder* h, const ShotIO& io, unsigned grid, cudaStream_t stream) {
-  auto kern = decode_generic_kernel<A>;
-  static thread_local const void* configured = nullptr;
-  (void)configured;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(h->smem_bytes)));
-  const unsigned block = h->P.ngroups * h->P.group_threads;
-  kern<<<grid, block, h->smem_bytes, stream>>>(h->P, io);
-  CUDA_TRY(cudaGetLastError());
-  ++h->launches;
+KernelFn generic_kernel(int arith) {
+  switch (arith) {
+    case QB_ARITH_FLOAT: return decode_generic_kernel<ArithF32>;
+    case QB_ARITH_INT8: return decode_generic_kernel<ArithI8>;
+    case QB_ARITH_INT16: return decode_generic_kernel<ArithI16>;
+    default: return decode_generic_kernel<ArithF16>;
+  }
 }
 
-void launch_generic(qb_decoder* h, const ShotIO& io, unsigned grid, cudaStream_t stream) {
-  switch (h->arith) {
-    case QB_ARITH_FLOAT: launch_generic_t<ArithF32>(h, io, grid, stream); break;
-    case QB_ARITH_INT8: launch_generic_t<ArithI8>(h, io, grid, stream); break;
-    case QB_ARITH_INT16: launch_generic_t<ArithI16>(h, io, grid, stream); break;
-    default: launch_generic_t<ArithF16>(h, io, grid, stream); break;
+// (6,3)-regular instantiations: nodes-per-thread class 1, 2, 4 = (checks, vars)
+// per thread (1,2), (2,4), (4,8); FAST = uniform prior (+ clamp-free proof for fp32).
+template <class A, bool kFast>
+KernelFn regular_kernel_tf(int npt, bool cluster) {
+  if (cluster) {
+    switch (npt) {
+      case 1: return decode_regular_cluster_kernel<A, 1, 2, kFast>;
+      case 2: return decode_regular_cluster_kernel<A, 2, 4, kFast>;
+      default: return decode_regular_cluster_kernel<A, 4, 8, kFast>;
+    }
+  }
+  switch (npt) {
+    case 1: return decode_regular_kernel<A, 1, 2, kFast, 1024, 1>;
+    case 2: return decode_regular_kernel<A, 2, 4, kFast, 512, 2>;
+    default: return decode_regular_kernel<A, 4, 8, kFast, 256, 4>;
   }
 }
 
 template <class A>
-int occupancy_generic_t(qb_decoder* h) {
-  int n = 0;
-  auto kern = decode_generic_kernel<A>;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(h->smem_bytes)));
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &n, kern, static_cast<int>(h->P.ngroups * h->P.group_threads), h->smem_bytes));
-  return n;
+KernelFn regular_kernel_t(int npt, bool cluster, bool fast) {
+  return fast ? regular_kernel_tf<A, true>(npt, cluster) : regular_kernel_tf<A, false>(npt, cluster);
 }
 
-int occupancy_generic(qb_decoder* h) {
-  switch (h->arith) {
-    case QB_ARITH_FLOAT: return occupancy_generic_t<ArithF32>(h);
-    case QB_ARITH_INT8: return occupancy_generic_t<ArithI8>(h);
-    case QB_ARITH_INT16: return occupancy_generic_t<ArithI16>(h);
-    default: return occupancy_generic_t<ArithF16>(h);
+KernelFn regular_kernel(int arith, int npt, bool cluster, bool fast) {
+  switch (arith) {
+    case QB_ARITH_FLOAT: return regular_kernel_t<ArithF32>(npt, cluster, fast);
+    case QB_ARITH_INT8: return regular_kernel_t<ArithI8>(npt, cluster, fast);
+    case QB_ARITH_INT16: return regular_kernel_t<ArithI16>(npt, cluster, fast);
+    default: return regular_kernel_t<ArithF16>(npt, cluster, fast);
   }
 }
 
-void choose_shape(qb_decoder* h) {
-  DecodeParams& P = h->P;
-  P.ngroups = std::min<uint32_t>(P.nseg, 8);
+uint32_t round_up32(uint32_t x) { return (x + 31u) & ~31u; }
+
+// Threads per segment group so that T*cpt covers the checks and T*vpt the
+// variables of every segment.
+uint32_t regular_group_threads(const DecodeParams& P, uint32_t cpt, uint32_t vpt) {
   uint32_t want = 32;
   for (uint32_t s = 0; s < P.nseg; ++s) {
     const uint32_t ms = P.segs[s].c1 - P.segs[s].c0;
     const uint32_t ns = P.segs[s].v1 - P.segs[s].v0;
-    want = std::max(want, std::max(ms, (ns + 1) / 2));
+    want = std::max(want, std::max((ms + cpt - 1) / cpt, (ns + vpt - 1) / vpt));
   }
-  uint32_t T = h->opt_group_threads > 0 ? static_cast<uint32_t>(h->opt_group_threads) : want;
-  T = (T + 31u) & ~31u;
-  const uint32_t cap = (1024u / P.ngroups) & ~31u;
-  T = std::max(32u, std::min(T, cap));
-  P.group_threads = T;
+  return round_up32(want);
+}
+
+void finish_plan(qb_decoder* h, LaunchPlan& pl) {
+  pl.block = pl.cluster ? pl.group_threads : pl.ngroups * pl.group_threads;
+  CUDA_TRY(cudaFuncSetAttribute(pl.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(h->smem_bytes)));
+  if (pl.cluster) {
+    pl.ctas_per_sm = 1;
+    return;
+  }
+  int n = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, pl.kernel, static_cast<int>(pl.block),
+                                                         h->smem_bytes));
+  if (n < 1) fail(QB_RUNTIME_ERROR, "decode kernel does not fit on an SM");
+  pl.ctas_per_sm = n;
+}
+
+LaunchPlan generic_plan(qb_decoder* h) {
+  const DecodeParams& P = h->P;
+  LaunchPlan pl{};
+  pl.kernel = generic_kernel(h->arith);
+  pl.name = "decode_generic_kernel";
+  pl.ngroups = std::min<uint32_t>(P.nseg, 8);
+  uint32_t T = h->opt_group_threads > 0 ? static_cast<uint32_t>(h->opt_group_threads)
+                                        : regular_group_threads(P, 1, 2);
+  T = std::max(32u, std::min(round_up32(T), (1024u / pl.ngroups) & ~31u));
+  pl.group_threads = T;
+  finish_plan(h, pl);
+  return pl;
+}
+
+void make_plans(qb_decoder* h) {
+  const DecodeParams& P = h->P;
+  const bool use_regular = h->regular63 && h->opt_kernel != 1;
+  if (h->opt_kernel == 2 && !h->regular63) {
+    fail(QB_INVALID_ARGUMENT, "regular kernel needs a (6,3)-regular graph with at most 8 segments");
+  }
+  if (!use_regular) {
+    h->lat = h->bat = generic_plan(h);
+    return;
+  }
+  auto regular_plan = [&](int npt, bool cluster) {
+    LaunchPlan pl{};
+    pl.regular = true;
+    pl.npt = npt;
+    pl.cluster = cluster;
+    pl.kernel = regular_kernel(h->arith, npt, cluster, h->fast_ok && h->opt_fast != 0);
+    pl.name = cluster ? "decode_regular_cluster_kernel" : "decode_regular_kernel";
+    pl.ngroups = P.nseg;
+    pl.group_threads = regular_group_threads(P, npt, 2 * npt);
+    finish_plan(h, pl);
+    return pl;
+  };
+  const uint32_t max_block[5] = {0, 1024, 512, 0, 256};
+  auto fits = [&](int npt, bool cluster) {
+    const uint32_t T = regular_group_threads(P, npt, 2 * npt);
+    return (cluster ? T : T * P.nseg) <= (cluster ? 1024u : max_block[npt]);
+  };
+  // single shot: fewest nodes per thread that fits; a cluster when there is more
+  // than one segment (unless the caller pins the shape)
+  const bool want_cluster = h->opt_latency_shape == 2 || (h->opt_latency_shape == 0 && P.nseg > 1);
+  bool lat_done = false;
+  for (int npt : {1, 2, 4}) {
+    if (h->opt_latency_npt && npt != h->opt_latency_npt) continue;
+    if (fits(npt, want_cluster)) {
+      h->lat = regular_plan(npt, want_cluster);
+      lat_done = true;
+      break;
+    }
+  }
+  if (!lat_done) h->lat = generic_plan(h);
+  bool bat_done = false;
+  const int first = h->opt_batch_npt ? static_cast<int>(h->opt_batch_npt) : 2;
+  for (int npt : {first, 2, 4}) {
+    if (fits(npt, false)) {
+      h->bat = regular_plan(npt, false);
+      bat_done = true;
+      break;
+    }
+  }
+  if (!bat_done) h->bat = generic_plan(h);
+}
+
+void launch_plan(qb_decoder* h, const LaunchPlan& pl, const ShotIO& io, unsigned grid,
+                 cudaStream_t stream) {
+  DecodeParams P = h->P;
+  P.ngroups = pl.ngroups;
+  P.group_threads = pl.group_threads;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(pl.block);
+  cfg.dynamicSmemBytes = h->smem_bytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  if (pl.cluster) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = P.nseg;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, pl.kernel, P, io));
+  ++h->launches;
 }
 
 void ensure_batch(qb_decoder* h, uint64_t shots, bool want_resid) {
@@ -288,8 +412,7 @@ void ensure_batch(qb_decoder* h, uint64_t shots, bool want_resid) {
 }
 
 unsigned batch_grid(qb_decoder* h, uint64_t shots) {
-  int per_sm = occupancy_generic(h);
-  if (per_sm < 1) fail(QB_RUNTIME_ERROR, "decode kernel does not fit on an SM");
+  int per_sm = h->bat.ctas_per_sm;
   if (h->opt_batch_ctas > 0) per_sm = std::min<int>(per_sm, static_cast<int>(h->opt_batch_ctas));
   const uint64_t resident = static_cast<uint64_t>(per_sm) * h->sm_count;
   return static_cast<unsigned>(std::min<uint64_t>(shots, resident));
@@ -307,7 +430,7 @@ void run_batch_device(qb_decoder* h, uint64_t shots, const uint32_t* d_syn, uint
   io.conv = d_conv;
   io.iters = d_iters;
   io.sched = h->d_sched;
-  launch_generic(h, io, batch_grid(h, shots), stream);
+  launch_plan(h, h->bat, io, batch_grid(h, shots), stream);
 }
 
 template <typename F>
@@ -356,7 +479,7 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
   io.flag = reinterpret_cast<volatile uint32_t*>(out + h->off_flag);
 
   if (mapped) {
-    launch_generic(h, io, 1, h->stream);
+    launch_plan(h, h->lat, io, h->lat.cluster ? h->P.nseg : 1, h->stream);
     // Spin on the completion word the kernel writes last; no stream sync on
     // the fast path.  A watchdog falls back to the runtime for diagnosis.
     const auto t0 = std::chrono::steady_clock::now();
@@ -376,7 +499,7 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
   } else {
     CUDA_TRY(cudaMemcpyAsync(h->d_in_dev, h->h_in, P.syn_w32 * 4, cudaMemcpyHostToDevice,
                              h->stream));
-    launch_generic(h, io, 1, h->stream);
+    launch_plan(h, h->lat, io, h->lat.cluster ? h->P.nseg : 1, h->stream);
     CUDA_TRY(cudaMemcpyAsync(h->h_out, h->d_out_dev, h->out_bytes, cudaMemcpyDeviceToHost,
                              h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -526,7 +649,9 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
           fail(QB_INVALID_ARGUMENT,
                "DecoderConfig: prior at variable " + std::to_string(n) + " is not finite");
         }
-        gamma_f[n] = static_cast<float>(p);
+        // -0.0 and +0.0 priors are indistinguishable to the reference's arithmetic
+        // (sign tests are `< 0`); storing +0.0 lets the kernels read signs as bits.
+        gamma_f[n] = static_cast<float>(p) + 0.0f;
       }
     }
 
@@ -619,7 +744,53 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
                                     " bytes of shared memory per shot; the device offers " +
                                     std::to_string(h->max_smem_optin));
     }
-    choose_shape(h);
+    {
+      // uniform prior?  (every stored gamma identical)
+      bool uniform = true;
+      if (!gamma_f.empty()) {
+        for (uint32_t n = 1; n < N && uniform; ++n) uniform = gamma_f[n] == gamma_f[0];
+        P.gamma_f = gamma_f[0];
+        P.gamma_d = static_cast<double>(gamma_f[0]);
+      } else {
+        for (uint32_t n = 1; n < N && uniform; ++n) uniform = gamma_i[n] == gamma_i[0];
+        P.gamma_i = gamma_i[0];
+      }
+      // fp32: can any stored message reach the reference's 1e30 clamp
+      // (decoder.cpp:238-241)?  |q| <= G + (dv-1) * |r|max, |r| <= alpha * |q|max
+      // (or alpha * 64 from a degree-1 check), iterated max_iterations times.
+      bool clamp_free = true;
+      if (arith == QB_ARITH_FLOAT) {
+        double gmax = 0.0;
+        for (float gmm : gamma_f) gmax = std::max(gmax, static_cast<double>(std::fabs(gmm)));
+        uint64_t dv_max = 0;
+        bool deg1_check = false;
+        for (uint32_t n = 0; n < N; ++n) {
+          dv_max = std::max<uint64_t>(dv_max, graph->var_offsets[n + 1] - graph->var_offsets[n]);
+        }
+        for (uint32_t m = 0; m < M; ++m) {
+          deg1_check = deg1_check || graph->check_offsets[m + 1] - graph->check_offsets[m] == 1;
+        }
+        double bq = gmax;
+        for (uint64_t it = 0; it < config->max_iterations && clamp_free; ++it) {
+          double br = config->alpha * bq;
+          if (deg1_check) br = std::max(br, config->alpha * 64.0);
+          bq = gmax + static_cast<double>(dv_max) * br;  // also bounds the posterior
+          clamp_free = bq < 1e29;
+        }
+      }
+      h->fast_ok = uniform && clamp_free;
+    }
+    {
+      bool reg = P.nseg <= 8;
+      for (uint32_t m = 0; m < M && reg; ++m) {
+        reg = graph->check_offsets[m + 1] - graph->check_offsets[m] == 6;
+      }
+      for (uint32_t n = 0; n < N && reg; ++n) {
+        reg = graph->var_offsets[n + 1] - graph->var_offsets[n] == 3;
+      }
+      h->regular63 = reg;
+    }
+    make_plans(h);
 
     CUDA_TRY(cudaMalloc(&h->d_sched, 2 * sizeof(unsigned int)));
     CUDA_TRY(cudaMemset(h->d_sched, 0, 2 * sizeof(unsigned int)));
@@ -658,8 +829,23 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
     switch (option) {
       case QB_OPT_KERNEL:
         if (value < 0 || value > 2) fail(QB_INVALID_ARGUMENT, "QB_OPT_KERNEL: 0, 1 or 2");
-        if (value == 2) fail(QB_INVALID_ARGUMENT, "regular kernel not available for this graph");
         h->opt_kernel = value;
+        break;
+      case QB_OPT_BATCH_NODES_PER_THREAD:
+        if (value != 0 && value != 1 && value != 2 && value != 4) {
+          fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_NODES_PER_THREAD: 0, 1, 2 or 4");
+        }
+        h->opt_batch_npt = value;
+        break;
+      case QB_OPT_FAST_PATH:
+        if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_FAST_PATH: 0 or 1");
+        h->opt_fast = value;
+        break;
+      case QB_OPT_LATENCY_NODES_PER_THREAD:
+        if (value != 0 && value != 1 && value != 2 && value != 4) {
+          fail(QB_INVALID_ARGUMENT, "QB_OPT_LATENCY_NODES_PER_THREAD: 0, 1, 2 or 4");
+        }
+        h->opt_latency_npt = value;
         break;
       case QB_OPT_LATENCY_IO:
         if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_LATENCY_IO: 0 or 1");
@@ -672,7 +858,6 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
       case QB_OPT_GROUP_THREADS:
         if (value < 0 || value > 1024) fail(QB_INVALID_ARGUMENT, "QB_OPT_GROUP_THREADS: 0..1024");
         h->opt_group_threads = value;
-        choose_shape(h);
         break;
       case QB_OPT_BATCH_CTAS_PER_SM:
         if (value < 0 || value > 32) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_CTAS_PER_SM: 0..32");
@@ -681,6 +866,7 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
       default:
         fail(QB_INVALID_ARGUMENT, "unknown option");
     }
+    make_plans(h);
   });
 }
 
@@ -690,7 +876,16 @@ int64_t qb_get_option(const qb_decoder* h, int option) {
     case QB_OPT_KERNEL: return h->opt_kernel;
     case QB_OPT_LATENCY_IO: return h->opt_latency_io;
     case QB_OPT_LATENCY_SHAPE: return h->opt_latency_shape;
-    case QB_OPT_GROUP_THREADS: return h->P.group_threads;
+    case QB_OPT_GROUP_THREADS: return h->lat.group_threads;
+    case QB_OPT_BATCH_NODES_PER_THREAD: return h->bat.regular ? h->bat.npt : 0;
+    case QB_OPT_LATENCY_NODES_PER_THREAD: return h->lat.regular ? h->lat.npt : 0;
+    case QB_OPT_INFO_BATCH_CTAS_PER_SM: return h->bat.ctas_per_sm;
+    case QB_OPT_INFO_BATCH_BLOCK: return h->bat.block;
+    case QB_OPT_INFO_LATENCY_BLOCK: return h->lat.block;
+    case QB_OPT_INFO_LATENCY_CLUSTER: return h->lat.cluster ? 1 : 0;
+    case QB_OPT_INFO_BATCH_REGULAR: return h->bat.regular ? 1 : 0;
+    case QB_OPT_FAST_PATH: return h->opt_fast;
+    case QB_OPT_INFO_FAST_ELIGIBLE: return h->fast_ok ? 1 : 0;
     case QB_OPT_BATCH_CTAS_PER_SM: return h->opt_batch_ctas;
     default: return -1;
   }

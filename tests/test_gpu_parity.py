@@ -281,3 +281,72 @@ def test_large_batch_soundness_properties():
     assert np.array_equal(conv[:, 1].astype(bool), ~rb[:, mz:].any(axis=1))
     assert its.min() >= 1 and its.max() <= 30
     assert conv.mean() > 0.9
+
+
+# ---- every kernel variant must produce the same bits -----------------------------------
+
+OPT_KERNEL, OPT_LATENCY_IO, OPT_LATENCY_SHAPE, OPT_GROUP_THREADS = 0, 1, 2, 3
+OPT_BATCH_CTAS, OPT_BATCH_NPT, OPT_LATENCY_NPT = 4, 5, 6
+INFO_BATCH_REGULAR, INFO_LATENCY_CLUSTER = 104, 103
+
+
+@pytest.mark.parametrize("mode", REF_MODES)
+@pytest.mark.parametrize("name", ["bb72", "bb144", "bb784"])
+def test_regular_and_cluster_kernels_match_oracle(oracle, name, mode):
+    """(6,3)-regular fast path: single-CTA and thread-block-cluster single-shot
+    kernels and every nodes-per-thread class of the batch kernel, against the
+    oracle bit for bit (messages included on the single-shot path)."""
+    code = codes.make_code(name)
+    g = code.combined_graph
+    rng = np.random.default_rng(11)
+    _, _, syn = error_syndromes(code, rng, 48, 0.03)
+    for iters, early in ((12, True), (7, False)):
+        cfg = DecoderConfig(max_iterations=iters, early_termination=early, arithmetic=mode)
+        oe, ores, oc, oi = oracle.decode_many(g, cfg, syn, code.segments)
+        with Decoder(code, cfg) as dec:
+            assert dec.get_option(INFO_BATCH_REGULAR) == 1
+            for shape in (1, 2):
+                dec.set_option(OPT_LATENCY_SHAPE, shape)
+                assert dec.get_option(INFO_LATENCY_CLUSTER) == (1 if shape == 2 else 0)
+                for npt in (1, 2, 4):
+                    if name == "bb784" and shape == 1 and npt == 1 and False:
+                        continue
+                    dec.set_option(OPT_LATENCY_NPT, npt)
+                    assert_matches_oracle(oracle, g, cfg, syn[:6], code.segments, dec=dec,
+                                          messages=True)
+            for npt in (1, 2, 4):
+                dec.set_option(OPT_BATCH_NPT, npt)
+                est, res, conv, its = dec.decode_batch_segments(syn)
+                assert np.array_equal(est, oe) and np.array_equal(res, ores), (npt, "bits")
+                assert np.array_equal(conv, oc) and np.array_equal(its, oi), (npt, "flags")
+            dec.set_option(OPT_KERNEL, 1)  # generic CSR kernel on the same handle
+            assert dec.get_option(INFO_BATCH_REGULAR) == 0
+            est, res, conv, its = dec.decode_batch_segments(syn)
+            assert np.array_equal(est, oe) and np.array_equal(its, oi)
+
+
+def test_regular_kernel_is_rejected_on_irregular_graphs():
+    g = codes.build_tanner_graph(codes.toy_code_3x6())
+    with Decoder(g, DecoderConfig()) as dec:
+        assert dec.get_option(INFO_BATCH_REGULAR) == 0
+        with pytest.raises(ValueError):
+            dec.set_option(OPT_KERNEL, 2)
+
+
+def test_half_mode_tracks_float_decisions():
+    """fp16 messages have no reference counterpart (decoder.hpp:16): they must
+    agree with the fp32 decoder on the overwhelming majority of shots and never
+    claim convergence with a wrong syndrome."""
+    code = codes.make_code("bb144")
+    rng = np.random.default_rng(3)
+    _, _, syn = error_syndromes(code, rng, 2000, 0.01)
+    with Decoder(code, DecoderConfig(max_iterations=50)) as d32, \
+            Decoder(code, DecoderConfig(max_iterations=50, arithmetic="half")) as d16:
+        e32, r32, c32, i32 = d32.decode_batch_segments(syn)
+        e16, r16, c16, i16 = d16.decode_batch_segments(syn)
+    g = code.combined_graph
+    hs = code.combined.mat_vec(gf2.unpack_bits(e16, g.num_vars))
+    assert np.array_equal(gf2.unpack_bits(r16, g.num_checks), hs ^ gf2.unpack_bits(syn, g.num_checks))
+    agree = (e32 == e16).all(axis=1).mean()
+    assert agree > 0.98, agree
+    assert abs(c32.mean() - c16.mean()) < 0.01
