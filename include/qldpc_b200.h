@@ -105,6 +105,10 @@ typedef enum {
    * instantiation with the prior as a kernel constant and (fp32) without the
    * provably unreachable 1e30 clamp; 0 forces the general instantiation. */
   QB_OPT_FAST_PATH = 7,
+  /* Batch work decomposition on regular codes: 0 = auto, 1 = one CTA per shot
+   * (one warp group per segment), 2 = one CTA per (shot, segment) work item
+   * drawn from per-segment queues. */
+  QB_OPT_BATCH_SHAPE = 8,
   /* Read-only (qb_get_option): the launch plans actually in use. */
   QB_OPT_INFO_BATCH_CTAS_PER_SM = 100,
   QB_OPT_INFO_BATCH_BLOCK = 101,

@@ -27,6 +27,7 @@ struct SegmentDev {
 // constant bank 0 and costs no loads from global memory.
 struct DecodeParams {
   uint32_t M, N, E, nseg;
+  uint32_t seg_emax;  // edges of the largest segment
   uint32_t syn_w32;  // 2 * ceil(M / 64): 32-bit words per packed syndrome
   uint32_t est_w32;  // 2 * ceil(N / 64): 32-bit words per packed estimate
   uint32_t max_iter;
@@ -64,7 +65,7 @@ struct ShotIO {
   uint32_t* resid;      // [nshots][syn_w32] or nullptr
   uint8_t* conv;        // [nshots][nseg]
   uint32_t* iters;      // [nshots][nseg]
-  unsigned int* sched;  // [0] next-shot ticket, [1] finished-CTA count
+  unsigned int* sched;  // [0] next-shot ticket, [1] finished-CTA count, [2+s] per-segment tickets
   // single-shot completion (nullptr on the batch path)
   uint64_t* kernel_ns;       // %globaltimer span, written before the flag
   volatile uint32_t* flag;   // receives `seq` after every result is visible

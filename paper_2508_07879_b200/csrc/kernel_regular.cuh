@@ -233,15 +233,21 @@ struct RegTables {
   uint32_t cbit[CPT];      // global check index (syndrome bit position)
   typename A::Gam gamma[kFast ? 1 : VPT];
   uint32_t valid;          // bit k: variable slot k is a real variable
+  uint32_t mbase;          // global check index of message element 0
 };
 
 template <class A, int CPT, int VPT, bool kFast>
 __device__ __forceinline__ void load_tables(const DecodeParams& P, const SegmentDev& seg,
                                             uint32_t t, uint32_t T,
-                                            RegTables<A, CPT, VPT, kFast>& tab) {
+                                            RegTables<A, CPT, VPT, kFast>& tab,
+                                            uint32_t ebase = 0, uint32_t pad0 = 0xffffffffu) {
+  // Message element i of the shared arrays holds global edge ebase + i; the dummy
+  // check / variable live at elements pad0 .. pad0+5 (default: right after edge E-1).
   using Gam = typename A::Gam;
   const Gam* __restrict__ gamma = static_cast<const Gam*>(P.gamma);
+  if (pad0 == 0xffffffffu) pad0 = P.E;
   tab.valid = 0;
+  tab.mbase = ebase / kDC;
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
     const uint32_t n = seg.v0 + t + k * T;
@@ -249,7 +255,7 @@ __device__ __forceinline__ void load_tables(const DecodeParams& P, const Segment
     tab.valid |= (ok ? 1u : 0u) << k;
 #pragma unroll
     for (int i = 0; i < kDV; ++i) {
-      tab.ea[k][i] = ok ? P.var_edges[n * kDV + i] : P.E + i;  // dummy variable: pad slots 0..2
+      tab.ea[k][i] = ok ? P.var_edges[n * kDV + i] - ebase : pad0 + i;  // dummy: pad slots 0..2
     }
     if constexpr (!kFast) tab.gamma[k] = ok ? gamma[n] : static_cast<Gam>(1);
   }
@@ -257,8 +263,8 @@ __device__ __forceinline__ void load_tables(const DecodeParams& P, const Segment
   for (int k = 0; k < CPT; ++k) {
     const uint32_t m = seg.c0 + t + k * T;
     const bool ok = m < seg.c1;
-    tab.cbit[k] = ok ? m : P.M;          // dummy check: syndrome bit M is always 0
-    tab.ce[k] = (ok ? m : P.M) * kDC;    // its edges are the pad slots E .. E+5
+    tab.cbit[k] = ok ? m : P.M;                 // dummy check: syndrome bit M is always 0
+    tab.ce[k] = ok ? m * kDC - ebase : pad0;    // its edges are the pad slots
   }
 }
 
@@ -321,7 +327,7 @@ __device__ __forceinline__ void decode_segment_regular(
         if ((ebits >> k) & 1u) {
 #pragma unroll
           for (int i = 0; i < kDV; ++i) {
-            const uint32_t m = tab.ea[k][i] / kDC;
+            const uint32_t m = tab.ea[k][i] / kDC + tab.mbase;
             atomicXor(&par[m >> 5], 1u << (m & 31u));
           }
         }
@@ -375,13 +381,15 @@ __device__ __forceinline__ void decode_segment_regular(
 
 template <class A>
 __device__ __forceinline__ void init_pads(const DecodeParams& P, const GenericSmem<A>& S,
-                                          uint32_t tid) {
+                                          uint32_t tid, uint32_t pad0) {
   // the dummy check's message slots and the spare syndrome words, once per kernel
   if (tid < kPadEdges) {
-    S.q[P.E + tid] = static_cast<typename A::Msg>(0);
-    S.r[P.E + tid] = static_cast<typename A::Msg>(0);
+    S.q[pad0 + tid] = static_cast<typename A::Msg>(0);
+    S.r[pad0 + tid] = static_cast<typename A::Msg>(0);
   }
-  if (tid < 2) S.syn[P.syn_w32 + tid] = 0;
+  // every syndrome word starts at 0 (the item kernel only ever writes its own
+  // segment's words; the dummy check reads bit M)
+  for (uint32_t w = tid; w < P.syn_w32 + 2; w += blockDim.x) S.syn[w] = 0;
 }
 
 template <class A>
@@ -470,7 +478,7 @@ decode_regular_kernel(const __grid_constant__ DecodeParams P, const __grid_const
   const SegmentDev seg = P.segs[group];
   RegTables<A, CPT, VPT, kFast> tab;
   load_tables<A, CPT, VPT, kFast>(P, seg, t, P.group_threads, tab);
-  init_pads<A>(P, S, tid);
+  init_pads<A>(P, S, tid, P.E);
 
   for (uint64_t shot = blockIdx.x; shot < io.nshots;) {
     shot_prologue<A>(P, S, io.syn + shot * P.syn_w32, tid, nthr);
@@ -492,6 +500,109 @@ decode_regular_kernel(const __grid_constant__ DecodeParams P, const __grid_const
   rewind_scheduler(io, tid);
 }
 
+// Batch kernel, work item = (shot, segment).  Segments are independent graphs, so
+// nothing forces the X and Z halves of a shot onto the same CTA: here each
+// persistent CTA serves ONE segment (its register tables are loaded once) and
+// draws shots from that segment's ticket counter, switching to another segment
+// only when its own queue is empty.  Compared with one-CTA-per-shot this (a) keeps
+// shared memory per CTA at one segment's messages, (b) removes the idle warps of
+// the half that converged first, and (c) lets a CTA be exactly as wide as one
+// segment needs.  Estimate / residual words that straddle a segment boundary are
+// merged into global memory with an atomicAnd + atomicOr pair that touches only
+// this segment's bits, so the two halves may finish in any order.
+template <class A, int CPT, int VPT, bool kFast, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB)
+decode_items_kernel(const __grid_constant__ DecodeParams P, const __grid_constant__ ShotIO io) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const GenericSmem<A> S = carve_items<A>(smem_raw, P);
+  const uint32_t tid = threadIdx.x, nthr = blockDim.x;
+  const uint32_t nseg = P.nseg;
+  init_pads<A>(P, S, tid, P.seg_emax);
+
+  uint32_t s = blockIdx.x % nseg;
+  // CTAs b with b % nseg == s start on shots b / nseg; later tickets continue from there
+  uint64_t shot = blockIdx.x / nseg;
+  uint32_t tried = 0;
+  while (tried < nseg) {
+    const SegmentDev seg = P.segs[s];
+    const uint32_t peers = (gridDim.x - s + nseg - 1) / nseg;  // CTAs that started on s
+    RegTables<A, CPT, VPT, kFast> tab;
+    load_tables<A, CPT, VPT, kFast>(P, seg, tid, nthr, tab, seg.e0, P.seg_emax);
+    const uint32_t cw0 = seg.c0 >> 5, cw1 = (seg.c1 - 1) >> 5;
+    const uint32_t vw0 = seg.v0 >> 5, vw1 = (seg.v1 - 1) >> 5;
+    while (shot < io.nshots) {
+      // ---- prologue: this segment's syndrome words
+      const uint32_t* syn_g = io.syn + shot * P.syn_w32;
+      for (uint32_t w = cw0 + tid; w <= cw1; w += nthr) {
+        const uint32_t v = syn_g[w] & range_mask(w, 0, P.M);
+        S.syn[w] = v;
+        S.par0[w] = v;
+        S.par1[w] = v;
+        S.res[w] = 0;
+      }
+      for (uint32_t w = vw0 + tid; w <= vw1; w += nthr) S.ehat[w] = 0;
+      __syncthreads();
+      decode_segment_regular<A, CPT, VPT, kFast>(P, S, seg, s, tid, nthr, 1u, tab);
+      __syncthreads();
+      // ---- epilogue: own bits only
+      uint32_t* est_g = io.est + shot * P.est_w32;
+      for (uint32_t w = vw0 + tid; w <= vw1; w += nthr) {
+        const uint32_t mask = range_mask(w, seg.v0, seg.v1);
+        if (mask == 0xffffffffu) {
+          est_g[w] = S.ehat[w];
+        } else {
+          atomicAnd(&est_g[w], ~mask);
+          atomicOr(&est_g[w], S.ehat[w] & mask);
+        }
+      }
+      if (io.resid) {
+        uint32_t* res_g = io.resid + shot * P.syn_w32;
+        for (uint32_t w = cw0 + tid; w <= cw1; w += nthr) {
+          const uint32_t mask = range_mask(w, seg.c0, seg.c1);
+          if (mask == 0xffffffffu) {
+            res_g[w] = S.res[w];
+          } else {
+            atomicAnd(&res_g[w], ~mask);
+            atomicOr(&res_g[w], S.res[w] & mask);
+          }
+        }
+      }
+      if (tid == 0) {
+        io.conv[shot * nseg + s] = static_cast<uint8_t>(S.segres[2 * s]);
+        io.iters[shot * nseg + s] = S.segres[2 * s + 1];
+        const uint64_t nxt = static_cast<uint64_t>(atomicAdd(&io.sched[2 + s], 1u)) + peers;
+        S.ticket[0] = static_cast<uint32_t>(nxt);
+        S.ticket[1] = static_cast<uint32_t>(nxt >> 32);
+      }
+      __syncthreads();
+      shot = static_cast<uint64_t>(S.ticket[0]) | (static_cast<uint64_t>(S.ticket[1]) << 32);
+      tried = 0;
+    }
+    // own queue empty: help another segment
+    ++tried;
+    if (tried >= nseg) break;
+    s = (s + 1) % nseg;
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t peers2 = (gridDim.x - s + nseg - 1) / nseg;
+      const uint64_t nxt = static_cast<uint64_t>(atomicAdd(&io.sched[2 + s], 1u)) + peers2;
+      S.ticket[0] = static_cast<uint32_t>(nxt);
+      S.ticket[1] = static_cast<uint32_t>(nxt >> 32);
+    }
+    __syncthreads();
+    shot = static_cast<uint64_t>(S.ticket[0]) | (static_cast<uint64_t>(S.ticket[1]) << 32);
+  }
+  // the last CTA out rewinds every ticket counter for the next launch
+  if (tid == 0) {
+    __threadfence();
+    const unsigned int done = atomicAdd(&io.sched[1], 1u);
+    if (done == gridDim.x - 1) {
+      for (uint32_t k = 0; k < 2 + kMaxSegments; ++k) io.sched[k] = 0;
+      __threadfence();
+    }
+  }
+}
+
 // Latency kernel for ONE shot on a thread-block cluster: CTA rank s of the
 // cluster decodes segment s on its own SM (segments are independent graphs, so
 // the iteration loop needs no cross-CTA traffic at all); when a segment is done
@@ -511,7 +622,7 @@ decode_regular_cluster_kernel(const __grid_constant__ DecodeParams P,
   const SegmentDev seg = P.segs[s];
   RegTables<A, CPT, VPT, kFast> tab;
   load_tables<A, CPT, VPT, kFast>(P, seg, tid, nthr, tab);
-  init_pads<A>(P, S, tid);
+  init_pads<A>(P, S, tid, P.E);
 
   shot_prologue<A>(P, S, io.syn, tid, nthr);
   __syncthreads();

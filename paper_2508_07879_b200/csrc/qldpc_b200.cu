@@ -88,6 +88,8 @@ struct LaunchPlan {
   uint32_t group_threads = 32;
   unsigned block = 32;
   int ctas_per_sm = 1;
+  size_t smem = 0;
+  bool items = false;          // work item = (shot, segment): grid-stride over per-segment queues
 };
 
 struct qb_decoder {
@@ -122,7 +124,7 @@ struct qb_decoder {
 
   // options
   int64_t opt_kernel = 0, opt_latency_io = 0, opt_latency_shape = 0, opt_group_threads = 0,
-          opt_batch_ctas = 0, opt_batch_npt = 0, opt_latency_npt = 0;
+          opt_batch_ctas = 0, opt_batch_npt = 0, opt_latency_npt = 0, opt_batch_shape = 0;
   bool regular63 = false;  // every check degree 6, every variable degree 3
   bool fast_ok = false;    // uniform prior (and, for fp32, provably clamp-free)
   int64_t opt_fast = 1;
@@ -131,6 +133,7 @@ struct qb_decoder {
   uint64_t launches = 0;
   std::string err;
   size_t smem_bytes = 0;
+  size_t smem_items = 0;
 };
 
 namespace {
@@ -271,6 +274,28 @@ KernelFn regular_kernel_t(int npt, bool cluster, bool fast) {
   return fast ? regular_kernel_tf<A, true>(npt, cluster) : regular_kernel_tf<A, false>(npt, cluster);
 }
 
+template <class A, bool kFast>
+KernelFn items_kernel_tf(int npt) {
+  switch (npt) {
+    case 1: return decode_items_kernel<A, 1, 2, kFast, 1024, 1>;
+    case 2: return decode_items_kernel<A, 2, 4, kFast, 512, 2>;
+    default: return decode_items_kernel<A, 4, 8, kFast, 256, 4>;
+  }
+}
+
+KernelFn items_kernel(int arith, int npt, bool fast) {
+  switch (arith) {
+    case QB_ARITH_FLOAT:
+      return fast ? items_kernel_tf<ArithF32, true>(npt) : items_kernel_tf<ArithF32, false>(npt);
+    case QB_ARITH_INT8:
+      return fast ? items_kernel_tf<ArithI8, true>(npt) : items_kernel_tf<ArithI8, false>(npt);
+    case QB_ARITH_INT16:
+      return fast ? items_kernel_tf<ArithI16, true>(npt) : items_kernel_tf<ArithI16, false>(npt);
+    default:
+      return fast ? items_kernel_tf<ArithF16, true>(npt) : items_kernel_tf<ArithF16, false>(npt);
+  }
+}
+
 KernelFn regular_kernel(int arith, int npt, bool cluster, bool fast) {
   switch (arith) {
     case QB_ARITH_FLOAT: return regular_kernel_t<ArithF32>(npt, cluster, fast);
@@ -296,15 +321,17 @@ uint32_t regular_group_threads(const DecodeParams& P, uint32_t cpt, uint32_t vpt
 
 void finish_plan(qb_decoder* h, LaunchPlan& pl) {
   pl.block = pl.cluster ? pl.group_threads : pl.ngroups * pl.group_threads;
+  if (pl.items) pl.block = pl.group_threads;
+  pl.smem = pl.items ? h->smem_items : h->smem_bytes;
   CUDA_TRY(cudaFuncSetAttribute(pl.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(h->smem_bytes)));
+                                static_cast<int>(pl.smem)));
   if (pl.cluster) {
     pl.ctas_per_sm = 1;
     return;
   }
   int n = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, pl.kernel, static_cast<int>(pl.block),
-                                                         h->smem_bytes));
+                                                         pl.smem));
   if (n < 1) fail(QB_RUNTIME_ERROR, "decode kernel does not fit on an SM");
   pl.ctas_per_sm = n;
 }
@@ -364,8 +391,25 @@ void make_plans(qb_decoder* h) {
   }
   if (!lat_done) h->lat = generic_plan(h);
   bool bat_done = false;
-  const int first = h->opt_batch_npt ? static_cast<int>(h->opt_batch_npt) : 2;
-  for (int npt : {first, 2, 4}) {
+  const int first = h->opt_batch_npt ? static_cast<int>(h->opt_batch_npt) : 1;
+  const bool fast = h->fast_ok && h->opt_fast != 0;
+  for (int npt : {first, 1, 2, 4}) {
+    if (h->opt_batch_shape != 1) {  // work item = (shot, segment)
+      const uint32_t T = regular_group_threads(P, npt, 2 * npt);
+      if (T > max_block[npt]) continue;
+      LaunchPlan pl{};
+      pl.regular = true;
+      pl.items = true;
+      pl.npt = npt;
+      pl.kernel = items_kernel(h->arith, npt, fast);
+      pl.name = "decode_items_kernel";
+      pl.ngroups = 1;
+      pl.group_threads = T;
+      finish_plan(h, pl);
+      h->bat = pl;
+      bat_done = true;
+      break;
+    }
     if (fits(npt, false)) {
       h->bat = regular_plan(npt, false);
       bat_done = true;
@@ -383,7 +427,7 @@ void launch_plan(qb_decoder* h, const LaunchPlan& pl, const ShotIO& io, unsigned
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(pl.block);
-  cfg.dynamicSmemBytes = h->smem_bytes;
+  cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   if (pl.cluster) {
@@ -415,7 +459,8 @@ unsigned batch_grid(qb_decoder* h, uint64_t shots) {
   int per_sm = h->bat.ctas_per_sm;
   if (h->opt_batch_ctas > 0) per_sm = std::min<int>(per_sm, static_cast<int>(h->opt_batch_ctas));
   const uint64_t resident = static_cast<uint64_t>(per_sm) * h->sm_count;
-  return static_cast<unsigned>(std::min<uint64_t>(shots, resident));
+  const uint64_t items = h->bat.items ? shots * h->P.nseg : shots;
+  return static_cast<unsigned>(std::min<uint64_t>(items, resident));
 }
 
 void run_batch_device(qb_decoder* h, uint64_t shots, const uint32_t* d_syn, uint32_t* d_est,
@@ -738,7 +783,13 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
     P.gamma = gamma_f.empty() ? static_cast<const void*>(keep(dev_upload(gamma_i)))
                               : static_cast<const void*>(keep(dev_upload(gamma_f)));
 
+    P.seg_emax = 0;
+    for (uint32_t k = 0; k < P.nseg; ++k) {
+      P.seg_emax = std::max(P.seg_emax, P.segs[k].e1 - P.segs[k].e0);
+    }
     h->smem_bytes = generic_smem_bytes(E, P.syn_w32, P.est_w32, P.nseg, msg_bytes_of(arith));
+    h->smem_items =
+        items_smem_bytes(P.seg_emax, P.syn_w32, P.est_w32, P.nseg, msg_bytes_of(arith));
     if (h->smem_bytes > static_cast<size_t>(h->max_smem_optin)) {
       fail(QB_INVALID_ARGUMENT, "graph needs " + std::to_string(h->smem_bytes) +
                                     " bytes of shared memory per shot; the device offers " +
@@ -792,8 +843,8 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
     }
     make_plans(h);
 
-    CUDA_TRY(cudaMalloc(&h->d_sched, 2 * sizeof(unsigned int)));
-    CUDA_TRY(cudaMemset(h->d_sched, 0, 2 * sizeof(unsigned int)));
+    CUDA_TRY(cudaMalloc(&h->d_sched, (2 + kMaxSegments) * sizeof(unsigned int)));
+    CUDA_TRY(cudaMemset(h->d_sched, 0, (2 + kMaxSegments) * sizeof(unsigned int)));
 
     // ---- single-shot staging
     auto align8 = [](size_t x) { return (x + 7) & ~static_cast<size_t>(7); };
@@ -836,6 +887,10 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
           fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_NODES_PER_THREAD: 0, 1, 2 or 4");
         }
         h->opt_batch_npt = value;
+        break;
+      case QB_OPT_BATCH_SHAPE:
+        if (value < 0 || value > 2) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_SHAPE: 0, 1 or 2");
+        h->opt_batch_shape = value;
         break;
       case QB_OPT_FAST_PATH:
         if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_FAST_PATH: 0 or 1");
@@ -885,6 +940,7 @@ int64_t qb_get_option(const qb_decoder* h, int option) {
     case QB_OPT_INFO_LATENCY_CLUSTER: return h->lat.cluster ? 1 : 0;
     case QB_OPT_INFO_BATCH_REGULAR: return h->bat.regular ? 1 : 0;
     case QB_OPT_FAST_PATH: return h->opt_fast;
+    case QB_OPT_BATCH_SHAPE: return h->bat.items ? 2 : 1;
     case QB_OPT_INFO_FAST_ELIGIBLE: return h->fast_ok ? 1 : 0;
     case QB_OPT_BATCH_CTAS_PER_SM: return h->opt_batch_ctas;
     default: return -1;

@@ -286,7 +286,7 @@ def test_large_batch_soundness_properties():
 # ---- every kernel variant must produce the same bits -----------------------------------
 
 OPT_KERNEL, OPT_LATENCY_IO, OPT_LATENCY_SHAPE, OPT_GROUP_THREADS = 0, 1, 2, 3
-OPT_BATCH_CTAS, OPT_BATCH_NPT, OPT_LATENCY_NPT = 4, 5, 6
+OPT_BATCH_CTAS, OPT_BATCH_NPT, OPT_LATENCY_NPT, OPT_FAST_PATH, OPT_BATCH_SHAPE = 4, 5, 6, 7, 8
 INFO_BATCH_REGULAR, INFO_LATENCY_CLUSTER = 104, 103
 
 
@@ -314,11 +314,18 @@ def test_regular_and_cluster_kernels_match_oracle(oracle, name, mode):
                     dec.set_option(OPT_LATENCY_NPT, npt)
                     assert_matches_oracle(oracle, g, cfg, syn[:6], code.segments, dec=dec,
                                           messages=True)
-            for npt in (1, 2, 4):
-                dec.set_option(OPT_BATCH_NPT, npt)
-                est, res, conv, its = dec.decode_batch_segments(syn)
-                assert np.array_equal(est, oe) and np.array_equal(res, ores), (npt, "bits")
-                assert np.array_equal(conv, oc) and np.array_equal(its, oi), (npt, "flags")
+            for bshape in (1, 2):  # CTA per shot / CTA per (shot, segment) work item
+                dec.set_option(OPT_BATCH_SHAPE, bshape)
+                assert dec.get_option(OPT_BATCH_SHAPE) == bshape
+                for npt in (1, 2, 4):
+                    dec.set_option(OPT_BATCH_NPT, npt)
+                    for fast in (1, 0):
+                        dec.set_option(OPT_FAST_PATH, fast)
+                        est, res, conv, its = dec.decode_batch_segments(syn)
+                        assert np.array_equal(est, oe) and np.array_equal(res, ores), (npt, "bits")
+                        assert np.array_equal(conv, oc) and np.array_equal(its, oi), (npt, "flags")
+                        est2, _, conv2, its2 = dec.decode_batch_segments(syn, want_residual=False)
+                        assert np.array_equal(est2, oe) and np.array_equal(its2, oi)
             dec.set_option(OPT_KERNEL, 1)  # generic CSR kernel on the same handle
             assert dec.get_option(INFO_BATCH_REGULAR) == 0
             est, res, conv, its = dec.decode_batch_segments(syn)
