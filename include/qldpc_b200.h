@@ -107,7 +107,8 @@ typedef enum {
   QB_OPT_FAST_PATH = 7,
   /* Batch work decomposition on regular codes: 0 = auto, 1 = one CTA per shot
    * (one warp group per segment), 2 = one CTA per (shot, segment) work item
-   * drawn from per-segment queues. */
+   * drawn from per-segment queues, 3 = the same with several shots in flight
+   * per CTA (continuous batching; the auto choice). */
   QB_OPT_BATCH_SHAPE = 8,
   /* Read-only (qb_get_option): the launch plans actually in use. */
   QB_OPT_INFO_BATCH_CTAS_PER_SM = 100,

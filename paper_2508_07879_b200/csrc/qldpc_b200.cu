@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "kernel_generic.cuh"
 #include "kernel_regular.cuh"
+#include "kernel_stream.cuh"
 #include "kernel_noise.cuh"
 #include "kernel_bw.cuh"
 
@@ -90,6 +91,7 @@ struct LaunchPlan {
   int ctas_per_sm = 1;
   size_t smem = 0;
   bool items = false;          // work item = (shot, segment): grid-stride over per-segment queues
+  bool stream = false;         // ... with K slots per CTA and continuous batching
 };
 
 struct qb_decoder {
@@ -134,6 +136,7 @@ struct qb_decoder {
   std::string err;
   size_t smem_bytes = 0;
   size_t smem_items = 0;
+  size_t smem_stream = 0;
 };
 
 namespace {
@@ -283,6 +286,30 @@ KernelFn items_kernel_tf(int npt) {
   }
 }
 
+constexpr int kStreamSlots = 2;
+
+template <class A, bool kFast>
+KernelFn stream_kernel_tf(int npt) {
+  switch (npt) {
+    case 1: return decode_stream_kernel<A, 1, 2, kFast, kStreamSlots, 1024, 1>;
+    case 2: return decode_stream_kernel<A, 2, 4, kFast, kStreamSlots, 512, 2>;
+    default: return decode_stream_kernel<A, 4, 8, kFast, kStreamSlots, 256, 4>;
+  }
+}
+
+KernelFn stream_kernel(int arith, int npt, bool fast) {
+  switch (arith) {
+    case QB_ARITH_FLOAT:
+      return fast ? stream_kernel_tf<ArithF32, true>(npt) : stream_kernel_tf<ArithF32, false>(npt);
+    case QB_ARITH_INT8:
+      return fast ? stream_kernel_tf<ArithI8, true>(npt) : stream_kernel_tf<ArithI8, false>(npt);
+    case QB_ARITH_INT16:
+      return fast ? stream_kernel_tf<ArithI16, true>(npt) : stream_kernel_tf<ArithI16, false>(npt);
+    default:
+      return fast ? stream_kernel_tf<ArithF16, true>(npt) : stream_kernel_tf<ArithF16, false>(npt);
+  }
+}
+
 KernelFn items_kernel(int arith, int npt, bool fast) {
   switch (arith) {
     case QB_ARITH_FLOAT:
@@ -322,7 +349,7 @@ uint32_t regular_group_threads(const DecodeParams& P, uint32_t cpt, uint32_t vpt
 void finish_plan(qb_decoder* h, LaunchPlan& pl) {
   pl.block = pl.cluster ? pl.group_threads : pl.ngroups * pl.group_threads;
   if (pl.items) pl.block = pl.group_threads;
-  pl.smem = pl.items ? h->smem_items : h->smem_bytes;
+  pl.smem = pl.stream ? h->smem_stream : pl.items ? h->smem_items : h->smem_bytes;
   CUDA_TRY(cudaFuncSetAttribute(pl.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(pl.smem)));
   if (pl.cluster) {
@@ -401,8 +428,9 @@ void make_plans(qb_decoder* h) {
       pl.regular = true;
       pl.items = true;
       pl.npt = npt;
-      pl.kernel = items_kernel(h->arith, npt, fast);
-      pl.name = "decode_items_kernel";
+      pl.stream = h->opt_batch_shape != 2;
+      pl.kernel = pl.stream ? stream_kernel(h->arith, npt, fast) : items_kernel(h->arith, npt, fast);
+      pl.name = pl.stream ? "decode_stream_kernel" : "decode_items_kernel";
       pl.ngroups = 1;
       pl.group_threads = T;
       finish_plan(h, pl);
@@ -459,6 +487,13 @@ unsigned batch_grid(qb_decoder* h, uint64_t shots) {
   int per_sm = h->bat.ctas_per_sm;
   if (h->opt_batch_ctas > 0) per_sm = std::min<int>(per_sm, static_cast<int>(h->opt_batch_ctas));
   const uint64_t resident = static_cast<uint64_t>(per_sm) * h->sm_count;
+  if (h->bat.stream) {
+    // equal numbers of CTAs per segment; no more CTAs than there are slot-fuls of shots
+    const uint64_t nseg = h->P.nseg;
+    const uint64_t per_seg = std::max<uint64_t>(
+        1, std::min<uint64_t>(resident / nseg, (shots + kStreamSlots - 1) / kStreamSlots));
+    return static_cast<unsigned>(per_seg * nseg);
+  }
   const uint64_t items = h->bat.items ? shots * h->P.nseg : shots;
   return static_cast<unsigned>(std::min<uint64_t>(items, resident));
 }
@@ -790,6 +825,11 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
     h->smem_bytes = generic_smem_bytes(E, P.syn_w32, P.est_w32, P.nseg, msg_bytes_of(arith));
     h->smem_items =
         items_smem_bytes(P.seg_emax, P.syn_w32, P.est_w32, P.nseg, msg_bytes_of(arith));
+    P.seg_mmax = 0;
+    for (uint32_t k = 0; k < P.nseg; ++k) {
+      P.seg_mmax = std::max(P.seg_mmax, P.segs[k].c1 - P.segs[k].c0);
+    }
+    h->smem_stream = stream_smem_bytes(P.seg_emax, P.seg_mmax, msg_bytes_of(arith), kStreamSlots);
     if (h->smem_bytes > static_cast<size_t>(h->max_smem_optin)) {
       fail(QB_INVALID_ARGUMENT, "graph needs " + std::to_string(h->smem_bytes) +
                                     " bytes of shared memory per shot; the device offers " +
@@ -889,7 +929,7 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
         h->opt_batch_npt = value;
         break;
       case QB_OPT_BATCH_SHAPE:
-        if (value < 0 || value > 2) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_SHAPE: 0, 1 or 2");
+        if (value < 0 || value > 3) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_SHAPE: 0 .. 3");
         h->opt_batch_shape = value;
         break;
       case QB_OPT_FAST_PATH:
@@ -940,7 +980,7 @@ int64_t qb_get_option(const qb_decoder* h, int option) {
     case QB_OPT_INFO_LATENCY_CLUSTER: return h->lat.cluster ? 1 : 0;
     case QB_OPT_INFO_BATCH_REGULAR: return h->bat.regular ? 1 : 0;
     case QB_OPT_FAST_PATH: return h->opt_fast;
-    case QB_OPT_BATCH_SHAPE: return h->bat.items ? 2 : 1;
+    case QB_OPT_BATCH_SHAPE: return h->bat.stream ? 3 : h->bat.items ? 2 : 1;
     case QB_OPT_INFO_FAST_ELIGIBLE: return h->fast_ok ? 1 : 0;
     case QB_OPT_BATCH_CTAS_PER_SM: return h->opt_batch_ctas;
     default: return -1;
