@@ -108,7 +108,8 @@ typedef enum {
   /* Batch work decomposition on regular codes: 0 = auto, 1 = one CTA per shot
    * (one warp group per segment), 2 = one CTA per (shot, segment) work item
    * drawn from per-segment queues, 3 = the same with several shots in flight
-   * per CTA (continuous batching; the auto choice). */
+   * per CTA (continuous batching), 4 = the instruction-lean item kernel
+   * (interleaved message blocks, counter-based stop test; the auto choice). */
   QB_OPT_BATCH_SHAPE = 8,
   /* Read-only (qb_get_option): the launch plans actually in use. */
   QB_OPT_INFO_BATCH_CTAS_PER_SM = 100,

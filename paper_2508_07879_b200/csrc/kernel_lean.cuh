@@ -1,0 +1,446 @@
+// Throughput kernel for (6,3)-regular codes, work item = (shot, segment).
+//
+// The arithmetic is the regular kernel's (bit-exact with the reference); this
+// kernel is about spending as few instructions per iteration as possible
+// OUTSIDE the two node updates, because on B200 this decoder is bound by
+// instruction issue and the conversion pipe, not by shared-memory bandwidth
+// (DESIGN.md "what bounds the path"):
+//
+//  * one message block per check in shared memory, [6 x q | 6 x r | pad], with a
+//    per-arithmetic stride chosen so that a warp of consecutive checks reads and
+//    writes its blocks without bank conflicts; r sits at a compile-time offset
+//    from q, so each variable edge costs ONE register (a byte offset) and every
+//    access is [reg + immediate];
+//  * the syndrome-match test is a single counter: the parity bitmap starts as the
+//    syndrome, a variable toggles its three checks only when its hard decision
+//    CHANGES (atomicXor, rare after the first iterations), and the toggling
+//    thread adjusts `unsat` by the bits it set or cleared - the per-iteration test
+//    is one broadcast load and a compare, with no preset, no scan, no masks;
+//  * bit vectors are segment-local (bit i = check c0 + i); the packed syndrome is
+//    prefetched into registers one shot ahead and shifted into place with warp
+//    shuffles, results are shifted back on the way out; words shared by two
+//    segments are only touched with bit-masked atomics, so the X and Z halves of a
+//    shot may be decoded by different CTAs in any order;
+//  * per-shot bit state is double-buffered on the item parity, which removes the
+//    barrier between one shot's exit test and the next shot's prologue:
+//    1 + 2 * iterations barriers per item.
+#pragma once
+
+#include "common.cuh"
+#include "kernel_regular.cuh"
+
+namespace qb {
+
+// Message-block layout per arithmetic: byte stride between checks, byte offset
+// of the r half.  Strides are conflict-free for the check-side vector access of
+// 32 consecutive checks: fp32 3 x 64-bit at stride 14 words; fp16 / int16
+// 3 x 32-bit at stride 7 words; int8 1 x 64-bit at stride 6 words.
+template <class A> struct Lay;
+template <> struct Lay<ArithF32> { static constexpr uint32_t kStride = 56, kROff = 24; };
+template <> struct Lay<ArithF16> { static constexpr uint32_t kStride = 28, kROff = 12; };
+template <> struct Lay<ArithI16> { static constexpr uint32_t kStride = 28, kROff = 12; };
+template <> struct Lay<ArithI8> { static constexpr uint32_t kStride = 24, kROff = 8; };
+
+__host__ __device__ inline uint32_t lean_stride(int arith) {
+  return arith == 0 ? 56u : arith == 1 ? 24u : 28u;
+}
+__host__ __device__ inline uint32_t lean_pw(uint32_t seg_mmax) { return (seg_mmax >> 5) + 1; }
+__host__ __device__ inline size_t lean_smem_bytes(uint32_t seg_mmax, int arith) {
+  const size_t msg = (static_cast<size_t>(seg_mmax + 1) * lean_stride(arith) + 15) & ~size_t(15);
+  return msg + 4 * (2 * static_cast<size_t>(lean_pw(seg_mmax)) + 8);
+}
+
+// ---- check update on one message block ---------------------------------------
+
+__device__ __forceinline__ void cn6_block(const DecodeParams& P, ArithF32, unsigned char* blk,
+                                          uint32_t syn_bit) {
+  const float2* qp = reinterpret_cast<const float2*>(blk);
+  float v[6];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const float2 p = qp[j];
+    v[2 * j] = p.x;
+    v[2 * j + 1] = p.y;
+  }
+  // |.| folds into the min/max/compare instructions as a source modifier
+  const float l0 = fminf(fabsf(v[0]), fabsf(v[1])), h0 = fmaxf(fabsf(v[0]), fabsf(v[1]));
+  const float l1 = fminf(fabsf(v[2]), fabsf(v[3])), h1 = fmaxf(fabsf(v[2]), fabsf(v[3]));
+  const float l2 = fminf(fabsf(v[4]), fabsf(v[5])), h2 = fmaxf(fabsf(v[4]), fabsf(v[5]));
+  const float m1 = fminf(fminf(l0, l1), l2);
+  const float med = fmaxf(fminf(l0, l1), fminf(fmaxf(l0, l1), l2));
+  const float m2 = fminf(med, fminf(fminf(h0, h1), h2));
+  // float(alpha * |min|): fp64 product, one rounding (decoder.cpp:302-307)
+  const uint32_t s1 = __float_as_uint(static_cast<float>(P.alpha * static_cast<double>(m1)));
+  const uint32_t s2 = __float_as_uint(static_cast<float>(P.alpha * static_cast<double>(m2)));
+  uint32_t sx = syn_bit << 31;
+#pragma unroll
+  for (int j = 0; j < 6; ++j) sx ^= __float_as_uint(v[j]);
+  float2* rp = reinterpret_cast<float2*>(blk + Lay<ArithF32>::kROff);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const uint32_t ox = (fabsf(v[2 * j]) == m1 ? s2 : s1) |
+                        ((sx ^ __float_as_uint(v[2 * j])) & 0x80000000u);
+    const uint32_t oy = (fabsf(v[2 * j + 1]) == m1 ? s2 : s1) |
+                        ((sx ^ __float_as_uint(v[2 * j + 1])) & 0x80000000u);
+    rp[j] = make_float2(__uint_as_float(ox), __uint_as_float(oy));
+  }
+}
+
+__device__ __forceinline__ void cn6_block(const DecodeParams& P, ArithF16, unsigned char* blk,
+                                          uint32_t syn_bit) {
+  const uint32_t* qp = reinterpret_cast<const uint32_t*>(blk);
+  uint32_t u[6];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const uint32_t w = qp[j];
+    u[2 * j] = w & 0xffffu;
+    u[2 * j + 1] = w >> 16;
+  }
+  int32_t a[6];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) a[j] = static_cast<int32_t>(u[j] & 0x7fffu);
+  int32_t m1, m2;
+  two_smallest6(a, m1, m2);
+  const uint32_t s1 = __half_as_ushort(__float2half_rn(
+      P.alpha_f * __half2float(__ushort_as_half(static_cast<unsigned short>(m1)))));
+  const uint32_t s2 = __half_as_ushort(__float2half_rn(
+      P.alpha_f * __half2float(__ushort_as_half(static_cast<unsigned short>(m2)))));
+  const uint32_t sx = u[0] ^ u[1] ^ u[2] ^ u[3] ^ u[4] ^ u[5] ^ (syn_bit << 15);
+  uint32_t* rp = reinterpret_cast<uint32_t*>(blk + Lay<ArithF16>::kROff);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const uint32_t lo = (a[2 * j] == m1 ? s2 : s1) | ((sx ^ u[2 * j]) & 0x8000u);
+    const uint32_t hi = (a[2 * j + 1] == m1 ? s2 : s1) | ((sx ^ u[2 * j + 1]) & 0x8000u);
+    rp[j] = lo | (hi << 16);
+  }
+}
+
+__device__ __forceinline__ void cn6_finish_int(const DecodeParams& P, const int32_t (&v)[6],
+                                               int32_t (&out)[6], uint32_t syn_bit) {
+  int32_t a[6];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) a[j] = abs(v[j]);
+  int32_t m1, m2;
+  two_smallest6(a, m1, m2);
+  const int32_t s1 = scale_q16(static_cast<uint32_t>(m1), P.alpha_fx);
+  const int32_t s2 = scale_q16(static_cast<uint32_t>(m2), P.alpha_fx);
+  const int32_t sx = v[0] ^ v[1] ^ v[2] ^ v[3] ^ v[4] ^ v[5] ^ static_cast<int32_t>(syn_bit << 31);
+#pragma unroll
+  for (int j = 0; j < 6; ++j) {
+    const int32_t mag = a[j] == m1 ? s2 : s1;
+    const int32_t neg = (sx ^ v[j]) >> 31;  // 0 or -1
+    out[j] = (mag ^ neg) - neg;
+  }
+}
+
+__device__ __forceinline__ void cn6_block(const DecodeParams& P, ArithI16, unsigned char* blk,
+                                          uint32_t syn_bit) {
+  const short2* qp = reinterpret_cast<const short2*>(blk);
+  int32_t v[6], o[6];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const short2 p = qp[j];
+    v[2 * j] = p.x;
+    v[2 * j + 1] = p.y;
+  }
+  cn6_finish_int(P, v, o, syn_bit);
+  short2* rp = reinterpret_cast<short2*>(blk + Lay<ArithI16>::kROff);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    rp[j] = make_short2(static_cast<short>(o[2 * j]), static_cast<short>(o[2 * j + 1]));
+  }
+}
+
+__device__ __forceinline__ void cn6_block(const DecodeParams& P, ArithI8, unsigned char* blk,
+                                          uint32_t syn_bit) {
+  const uint2 w = *reinterpret_cast<const uint2*>(blk);  // 6 message bytes + 2 unused
+  int32_t v[6], o[6];
+  v[0] = static_cast<int8_t>(w.x);
+  v[1] = static_cast<int8_t>(w.x >> 8);
+  v[2] = static_cast<int8_t>(w.x >> 16);
+  v[3] = static_cast<int8_t>(w.x >> 24);
+  v[4] = static_cast<int8_t>(w.y);
+  v[5] = static_cast<int8_t>(w.y >> 8);
+  cn6_finish_int(P, v, o, syn_bit);
+  uint2 r;
+  r.x = (o[0] & 0xff) | ((o[1] & 0xff) << 8) | ((o[2] & 0xff) << 16) |
+        (static_cast<uint32_t>(o[3]) << 24);
+  r.y = (o[4] & 0xff) | ((o[5] & 0xff) << 8);
+  *reinterpret_cast<uint2*>(blk + Lay<ArithI8>::kROff) = r;
+}
+
+// ---- variable update through byte offsets; returns 1 iff the variable decides 1 ----
+
+template <bool kFast>
+__device__ __forceinline__ uint32_t vn3_off(const DecodeParams& P, ArithF32, unsigned char* base,
+                                            const uint32_t (&eo)[3], float gamma) {
+  constexpr uint32_t R = Lay<ArithF32>::kROff;
+  const double r0 = static_cast<double>(*reinterpret_cast<const float*>(base + eo[0] + R));
+  const double r1 = static_cast<double>(*reinterpret_cast<const float*>(base + eo[1] + R));
+  const double r2 = static_cast<double>(*reinterpret_cast<const float*>(base + eo[2] + R));
+  double total = kFast ? P.gamma_d : static_cast<double>(gamma);  // ascending edge order
+  total += r0;
+  total += r1;
+  total += r2;
+  float x0 = static_cast<float>(total - r0);
+  float x1 = static_cast<float>(total - r1);
+  float x2 = static_cast<float>(total - r2);
+  if constexpr (!kFast) {
+    x0 = fminf(fmaxf(x0, -P.clamp_f), P.clamp_f);
+    x1 = fminf(fmaxf(x1, -P.clamp_f), P.clamp_f);
+    x2 = fminf(fmaxf(x2, -P.clamp_f), P.clamp_f);
+  }
+  *reinterpret_cast<float*>(base + eo[0]) = x0;
+  *reinterpret_cast<float*>(base + eo[1]) = x1;
+  *reinterpret_cast<float*>(base + eo[2]) = x2;
+  return static_cast<uint32_t>(__double2hiint(total)) >> 31;
+}
+
+template <bool kFast>
+__device__ __forceinline__ uint32_t vn3_off(const DecodeParams& P, ArithF16, unsigned char* base,
+                                            const uint32_t (&eo)[3], float gamma) {
+  constexpr uint32_t R = Lay<ArithF16>::kROff;
+  const float r0 = __half2float(*reinterpret_cast<const __half*>(base + eo[0] + R));
+  const float r1 = __half2float(*reinterpret_cast<const __half*>(base + eo[1] + R));
+  const float r2 = __half2float(*reinterpret_cast<const __half*>(base + eo[2] + R));
+  const float total = (kFast ? P.gamma_f : gamma) + r0 + r1 + r2;
+  *reinterpret_cast<__half*>(base + eo[0]) =
+      __float2half_rn(fminf(fmaxf(total - r0, -kHalfClamp), kHalfClamp));
+  *reinterpret_cast<__half*>(base + eo[1]) =
+      __float2half_rn(fminf(fmaxf(total - r1, -kHalfClamp), kHalfClamp));
+  *reinterpret_cast<__half*>(base + eo[2]) =
+      __float2half_rn(fminf(fmaxf(total - r2, -kHalfClamp), kHalfClamp));
+  return total < 0.0f ? 1u : 0u;
+}
+
+template <bool kFast, class A>
+__device__ __forceinline__ uint32_t vn3_off_int(const DecodeParams& P, unsigned char* base,
+                                                const uint32_t (&eo)[3], int32_t gamma) {
+  using MsgI = typename A::Msg;
+  constexpr uint32_t R = Lay<A>::kROff;
+  const int32_t r0 = *reinterpret_cast<const MsgI*>(base + eo[0] + R);
+  const int32_t r1 = *reinterpret_cast<const MsgI*>(base + eo[1] + R);
+  const int32_t r2 = *reinterpret_cast<const MsgI*>(base + eo[2] + R);
+  const int32_t total = (kFast ? P.gamma_i : gamma) + r0 + r1 + r2;
+  *reinterpret_cast<MsgI*>(base + eo[0]) = static_cast<MsgI>(max(-P.kmax, min(P.kmax, total - r0)));
+  *reinterpret_cast<MsgI*>(base + eo[1]) = static_cast<MsgI>(max(-P.kmax, min(P.kmax, total - r1)));
+  *reinterpret_cast<MsgI*>(base + eo[2]) = static_cast<MsgI>(max(-P.kmax, min(P.kmax, total - r2)));
+  return static_cast<uint32_t>(total) >> 31;
+}
+template <bool kFast>
+__device__ __forceinline__ uint32_t vn3_off(const DecodeParams& P, ArithI8, unsigned char* base,
+                                            const uint32_t (&eo)[3], int32_t gamma) {
+  return vn3_off_int<kFast, ArithI8>(P, base, eo, gamma);
+}
+template <bool kFast>
+__device__ __forceinline__ uint32_t vn3_off(const DecodeParams& P, ArithI16, unsigned char* base,
+                                            const uint32_t (&eo)[3], int32_t gamma) {
+  return vn3_off_int<kFast, ArithI16>(P, base, eo, gamma);
+}
+
+// ---- the kernel ---------------------------------------------------------------
+
+template <class A, int CPT, int VPT, bool kFast, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB)
+decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant__ ShotIO io) {
+  using Msg = typename A::Msg;
+  using Gam = typename A::Gam;
+  constexpr uint32_t kStride = Lay<A>::kStride;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t tid = threadIdx.x, T = blockDim.x, lane = tid & 31u, warp = tid >> 5;
+  const uint32_t nwarps = T >> 5;
+  const uint32_t nseg = P.nseg;
+  const uint32_t s = blockIdx.x % nseg;      // the segment this CTA serves for its whole life
+  const uint32_t peer = blockIdx.x / nseg;
+  const uint32_t peers = (gridDim.x - s + nseg - 1) / nseg;
+  const SegmentDev seg = P.segs[s];
+  const uint32_t Ms = seg.c1 - seg.c0;
+  const uint32_t pw = lean_pw(P.seg_mmax);
+  const uint32_t pws = (Ms + 31u) >> 5;
+  const uint32_t gw0 = seg.c0 >> 5, gspan = ((seg.c1 - 1) >> 5) - gw0 + 1, cshift = seg.c0 & 31u;
+  const uint32_t vw0 = seg.v0 >> 5, vspan = ((seg.v1 - 1) >> 5) - vw0 + 1;
+
+  unsigned char* const msgs = smem_raw;
+  const size_t msg_bytes = (static_cast<size_t>(P.seg_mmax + 1) * kStride + 15) & ~size_t(15);
+  uint32_t* const bits = reinterpret_cast<uint32_t*>(smem_raw + msg_bytes);
+  uint32_t* const unsat_ctr = bits + 2 * pw;  // [2]
+  uint32_t* const ticket = bits + 2 * pw + 2;  // [2]
+
+  // ---- per-thread tables: byte offsets of the q side of every edge / check block
+  uint32_t eo[VPT][kDV], co[CPT], cl[CPT], valid = 0;
+  Gam gam[kFast ? 1 : VPT];
+  {
+    const Gam* __restrict__ gamma = static_cast<const Gam*>(P.gamma);
+    const uint32_t dummy = P.seg_mmax * kStride;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const uint32_t n = seg.v0 + tid + k * T;
+      const bool ok = n < seg.v1;
+      valid |= (ok ? 1u : 0u) << k;
+#pragma unroll
+      for (int i = 0; i < kDV; ++i) {
+        const uint32_t e = ok ? P.var_edges[n * kDV + i] - seg.e0 : 0u;
+        eo[k][i] = ok ? (e / kDC) * kStride + (e % kDC) * static_cast<uint32_t>(sizeof(Msg))
+                      : dummy + i * static_cast<uint32_t>(sizeof(Msg));
+      }
+      if constexpr (!kFast) gam[k] = ok ? gamma[n] : static_cast<Gam>(1);
+    }
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+      const uint32_t m = tid + k * T;
+      cl[k] = m < Ms ? m : Ms;                    // dummy check: bit Ms of the bitmap, always 0
+      co[k] = (m < Ms ? m : P.seg_mmax) * kStride;
+    }
+  }
+  for (uint32_t b = tid; b < kStride; b += T) msgs[P.seg_mmax * kStride + b] = 0;  // dummy block
+
+  uint64_t shot = peer;
+  uint32_t raw_next = 0;
+  if (warp == 0 && lane < gspan && shot < io.nshots) {
+    raw_next = io.syn[shot * P.syn_w32 + gw0 + lane];
+  }
+  uint32_t ipar = 0;
+  __syncthreads();
+
+  while (shot < io.nshots) {
+    uint32_t* const par = bits + ipar * pw;
+    volatile uint32_t* const unsat = unsat_ctr + ipar;
+    // ---------------- prologue ----------------
+    if (warp == 0) {
+      // packed syndrome words -> segment-local bitmap, and its population count
+      uint32_t nb = __shfl_down_sync(0xffffffffu, raw_next, 1);
+      if (lane + 1 >= gspan) nb = 0;
+      uint32_t loc = cshift ? __funnelshift_r(raw_next, nb, cshift) : raw_next;
+      if (lane >= pws) {
+        loc = 0;
+      } else if (Ms - lane * 32u < 32u) {
+        loc &= (1u << (Ms - lane * 32u)) - 1u;
+      }
+      if (lane < pw) par[lane] = loc;
+      const uint32_t cnt = __reduce_add_sync(0xffffffffu, __popc(loc));
+      if (lane == 0) {
+        *unsat = cnt;
+        const uint64_t t = static_cast<uint64_t>(atomicAdd(&io.sched[2 + s], 1u)) + peers;
+        ticket[ipar] = t < io.nshots ? static_cast<uint32_t>(t) : kNoShot;
+      }
+    }
+    if (warp == nwarps - 1) {  // zero this segment's bits of the shot's estimate
+      uint32_t* est_g = io.est + shot * P.est_w32 + vw0;
+      for (uint32_t w = lane; w < vspan; w += 32u) {
+        const uint32_t mask = range_mask(vw0 + w, seg.v0, seg.v1);
+        if (mask == 0xffffffffu) {
+          est_g[w] = 0u;
+        } else {
+          atomicAnd(&est_g[w], ~mask);
+        }
+      }
+    }
+    // q[e] = gamma[var(e)] (decoder.cpp:156-158)
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      Gam g;
+      if constexpr (kFast) {
+        if constexpr (A::kInt) g = P.gamma_i; else g = P.gamma_f;
+      } else {
+        g = gam[k];
+      }
+      const Msg init = prior_as_msg<A>(g);
+#pragma unroll
+      for (int i = 0; i < kDV; ++i) *reinterpret_cast<Msg*>(msgs + eo[k][i]) = init;
+    }
+    uint32_t eprev = 0;
+    __syncthreads();
+
+    uint32_t synbits = 0;
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) synbits |= ((par[cl[k] >> 5] >> (cl[k] & 31u)) & 1u) << k;
+    const uint32_t next = ticket[ipar];
+    if (warp == 0 && lane < gspan && next != kNoShot) {  // prefetch the next shot's syndrome
+      raw_next = io.syn[static_cast<uint64_t>(next) * P.syn_w32 + gw0 + lane];
+    }
+
+    // ---------------- iterations ----------------
+    uint32_t iter = 0;
+    bool still_unsat;
+    for (;;) {
+      ++iter;
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) cn6_block(P, A{}, msgs + co[k], (synbits >> k) & 1u);
+      __syncthreads();
+      uint32_t eb = 0;
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) {
+        Gam g{};
+        if constexpr (!kFast) g = gam[k];
+        eb |= vn3_off<kFast>(P, A{}, msgs, eo[k], g) << k;
+      }
+      eb &= valid;
+      const uint32_t changed = eb ^ eprev;
+      eprev = eb;
+      if (changed) {  // a hard decision flipped: toggle its checks, keep the counter exact
+        int32_t delta = 0;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+          if ((changed >> k) & 1u) {
+#pragma unroll
+            for (int i = 0; i < kDV; ++i) {
+              const uint32_t lm = eo[k][i] / kStride;
+              const uint32_t bit = 1u << (lm & 31u);
+              const uint32_t old = atomicXor(&par[lm >> 5], bit);
+              delta += (old & bit) ? -1 : 1;
+            }
+          }
+        }
+        atomicAdd(const_cast<uint32_t*>(unsat), static_cast<uint32_t>(delta));
+      }
+      __syncthreads();
+      still_unsat = *unsat != 0u;
+      if ((P.early && !still_unsat) || iter >= P.max_iter) break;
+    }
+
+    // ---------------- epilogue ----------------
+    if (warp == 0 && io.resid) {
+      const uint32_t hi = lane < pw ? par[lane] : 0u;
+      uint32_t lo = __shfl_up_sync(0xffffffffu, hi, 1);
+      if (lane == 0) lo = 0;
+      const uint32_t out = cshift ? __funnelshift_l(lo, hi, cshift) : hi;
+      if (lane < gspan) {
+        uint32_t* dst = io.resid + shot * P.syn_w32 + gw0 + lane;
+        const uint32_t mask = range_mask(gw0 + lane, seg.c0, seg.c1);
+        if (mask == 0xffffffffu) {
+          *dst = out;
+        } else {
+          atomicAnd(dst, ~mask);
+          atomicOr(dst, out & mask);
+        }
+      }
+    }
+    if (eprev) {
+      uint32_t* est_g = io.est + shot * P.est_w32;
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) {
+        if ((eprev >> k) & 1u) {
+          const uint32_t n = seg.v0 + tid + k * T;
+          atomicOr(&est_g[n >> 5], 1u << (n & 31u));
+        }
+      }
+    }
+    if (tid == 0) {
+      io.conv[shot * nseg + s] = still_unsat ? 0 : 1;
+      io.iters[shot * nseg + s] = iter;
+    }
+    shot = next == kNoShot ? ~0ull : static_cast<uint64_t>(next);
+    ipar ^= 1u;
+  }
+
+  if (tid == 0) {
+    __threadfence();
+    const unsigned int done = atomicAdd(&io.sched[1], 1u);
+    if (done == gridDim.x - 1) {
+      for (uint32_t k = 0; k < 2 + kMaxSegments; ++k) io.sched[k] = 0;
+      __threadfence();
+    }
+  }
+}
+
+}  // namespace qb

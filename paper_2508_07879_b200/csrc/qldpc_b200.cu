@@ -21,6 +21,7 @@
 #include "kernel_generic.cuh"
 #include "kernel_regular.cuh"
 #include "kernel_stream.cuh"
+#include "kernel_lean.cuh"
 #include "kernel_noise.cuh"
 #include "kernel_bw.cuh"
 
@@ -92,6 +93,7 @@ struct LaunchPlan {
   size_t smem = 0;
   bool items = false;          // work item = (shot, segment): grid-stride over per-segment queues
   bool stream = false;         // ... with K slots per CTA and continuous batching
+  bool lean = false;           // ... the instruction-lean single-slot variant
 };
 
 struct qb_decoder {
@@ -137,6 +139,7 @@ struct qb_decoder {
   size_t smem_bytes = 0;
   size_t smem_items = 0;
   size_t smem_stream = 0;
+  size_t smem_lean = 0;
 };
 
 namespace {
@@ -310,6 +313,28 @@ KernelFn stream_kernel(int arith, int npt, bool fast) {
   }
 }
 
+template <class A, bool kFast>
+KernelFn lean_kernel_tf(int npt) {
+  switch (npt) {
+    case 1: return decode_lean_kernel<A, 1, 2, kFast, 1024, 1>;
+    case 2: return decode_lean_kernel<A, 2, 4, kFast, 512, 2>;
+    default: return decode_lean_kernel<A, 4, 8, kFast, 256, 4>;
+  }
+}
+
+KernelFn lean_kernel(int arith, int npt, bool fast) {
+  switch (arith) {
+    case QB_ARITH_FLOAT:
+      return fast ? lean_kernel_tf<ArithF32, true>(npt) : lean_kernel_tf<ArithF32, false>(npt);
+    case QB_ARITH_INT8:
+      return fast ? lean_kernel_tf<ArithI8, true>(npt) : lean_kernel_tf<ArithI8, false>(npt);
+    case QB_ARITH_INT16:
+      return fast ? lean_kernel_tf<ArithI16, true>(npt) : lean_kernel_tf<ArithI16, false>(npt);
+    default:
+      return fast ? lean_kernel_tf<ArithF16, true>(npt) : lean_kernel_tf<ArithF16, false>(npt);
+  }
+}
+
 KernelFn items_kernel(int arith, int npt, bool fast) {
   switch (arith) {
     case QB_ARITH_FLOAT:
@@ -349,7 +374,10 @@ uint32_t regular_group_threads(const DecodeParams& P, uint32_t cpt, uint32_t vpt
 void finish_plan(qb_decoder* h, LaunchPlan& pl) {
   pl.block = pl.cluster ? pl.group_threads : pl.ngroups * pl.group_threads;
   if (pl.items) pl.block = pl.group_threads;
-  pl.smem = pl.stream ? h->smem_stream : pl.items ? h->smem_items : h->smem_bytes;
+  pl.smem = pl.lean     ? h->smem_lean
+            : pl.stream ? h->smem_stream
+            : pl.items  ? h->smem_items
+                        : h->smem_bytes;
   CUDA_TRY(cudaFuncSetAttribute(pl.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(pl.smem)));
   if (pl.cluster) {
@@ -428,9 +456,15 @@ void make_plans(qb_decoder* h) {
       pl.regular = true;
       pl.items = true;
       pl.npt = npt;
-      pl.stream = h->opt_batch_shape != 2;
-      pl.kernel = pl.stream ? stream_kernel(h->arith, npt, fast) : items_kernel(h->arith, npt, fast);
-      pl.name = pl.stream ? "decode_stream_kernel" : "decode_items_kernel";
+      const bool lean_ok = P.seg_mmax <= 960;
+      pl.lean = lean_ok && (h->opt_batch_shape == 0 || h->opt_batch_shape == 4);
+      pl.stream = !pl.lean && h->opt_batch_shape != 2;
+      pl.kernel = pl.lean     ? lean_kernel(h->arith, npt, fast)
+                  : pl.stream ? stream_kernel(h->arith, npt, fast)
+                              : items_kernel(h->arith, npt, fast);
+      pl.name = pl.lean     ? "decode_lean_kernel"
+                : pl.stream ? "decode_stream_kernel"
+                            : "decode_items_kernel";
       pl.ngroups = 1;
       pl.group_threads = T;
       finish_plan(h, pl);
@@ -830,6 +864,7 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
       P.seg_mmax = std::max(P.seg_mmax, P.segs[k].c1 - P.segs[k].c0);
     }
     h->smem_stream = stream_smem_bytes(P.seg_emax, P.seg_mmax, msg_bytes_of(arith), kStreamSlots);
+    h->smem_lean = lean_smem_bytes(P.seg_mmax, arith == QB_ARITH_HALF ? 3 : arith);
     if (h->smem_bytes > static_cast<size_t>(h->max_smem_optin)) {
       fail(QB_INVALID_ARGUMENT, "graph needs " + std::to_string(h->smem_bytes) +
                                     " bytes of shared memory per shot; the device offers " +
@@ -929,7 +964,7 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
         h->opt_batch_npt = value;
         break;
       case QB_OPT_BATCH_SHAPE:
-        if (value < 0 || value > 3) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_SHAPE: 0 .. 3");
+        if (value < 0 || value > 4) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_SHAPE: 0 .. 4");
         h->opt_batch_shape = value;
         break;
       case QB_OPT_FAST_PATH:
@@ -980,7 +1015,7 @@ int64_t qb_get_option(const qb_decoder* h, int option) {
     case QB_OPT_INFO_LATENCY_CLUSTER: return h->lat.cluster ? 1 : 0;
     case QB_OPT_INFO_BATCH_REGULAR: return h->bat.regular ? 1 : 0;
     case QB_OPT_FAST_PATH: return h->opt_fast;
-    case QB_OPT_BATCH_SHAPE: return h->bat.stream ? 3 : h->bat.items ? 2 : 1;
+    case QB_OPT_BATCH_SHAPE: return h->bat.lean ? 4 : h->bat.stream ? 3 : h->bat.items ? 2 : 1;
     case QB_OPT_INFO_FAST_ELIGIBLE: return h->fast_ok ? 1 : 0;
     case QB_OPT_BATCH_CTAS_PER_SM: return h->opt_batch_ctas;
     default: return -1;

@@ -314,7 +314,7 @@ def test_regular_and_cluster_kernels_match_oracle(oracle, name, mode):
                     dec.set_option(OPT_LATENCY_NPT, npt)
                     assert_matches_oracle(oracle, g, cfg, syn[:6], code.segments, dec=dec,
                                           messages=True)
-            for bshape in (1, 2, 3):  # CTA per shot / per (shot, segment) item / streaming slots
+            for bshape in (1, 2, 3, 4):  # CTA per shot / (shot, segment) item / streaming / lean
                 dec.set_option(OPT_BATCH_SHAPE, bshape)
                 assert dec.get_option(OPT_BATCH_SHAPE) == bshape
                 for npt in (1, 2, 4):
