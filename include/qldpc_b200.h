@@ -97,9 +97,11 @@ typedef enum {
   QB_OPT_GROUP_THREADS = 3,
   /* CTAs per SM for the persistent batch kernel (0 = auto). */
   QB_OPT_BATCH_CTAS_PER_SM = 4,
-  /* Regular kernel: nodes per thread class for the batch / single-shot path:
-   * 1, 2 or 4 checks (and twice as many variables) per thread; 0 = auto. */
-  QB_OPT_BATCH_NODES_PER_THREAD = 5,
+  /* Batch item kernel variant (checks x variables per thread, CTAs per SM):
+   * 0 = auto, 1..6 = a specific instantiation (see kLeanVariants). */
+  QB_OPT_BATCH_VARIANT = 5,
+  /* Single-shot regular kernel: 1, 2 or 4 checks (and twice as many variables)
+   * per thread; 0 = auto. */
   QB_OPT_LATENCY_NODES_PER_THREAD = 6,
   /* Regular kernel: 1 (default) lets uniform-prior decoders use the
    * instantiation with the prior as a kernel constant and (fp32) without the
@@ -107,9 +109,7 @@ typedef enum {
   QB_OPT_FAST_PATH = 7,
   /* Batch work decomposition on regular codes: 0 = auto, 1 = one CTA per shot
    * (one warp group per segment), 2 = one CTA per (shot, segment) work item
-   * drawn from per-segment queues, 3 = the same with several shots in flight
-   * per CTA (continuous batching), 4 = the instruction-lean item kernel
-   * (interleaved message blocks, counter-based stop test; the auto choice). */
+   * drawn from per-segment queues (the lean item kernel; the auto choice). */
   QB_OPT_BATCH_SHAPE = 8,
   /* Read-only (qb_get_option): the launch plans actually in use. */
   QB_OPT_INFO_BATCH_CTAS_PER_SM = 100,

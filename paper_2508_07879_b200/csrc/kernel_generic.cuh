@@ -64,32 +64,6 @@ __device__ __forceinline__ GenericSmem<A> carve_generic(unsigned char* base,
   return s;
 }
 
-// Layout of the per-segment work-item kernel: message arrays sized for the
-// largest segment only; bit arrays keep their global indexing.
-__host__ __device__ inline size_t items_smem_bytes(uint32_t seg_emax, uint32_t syn_w32,
-                                                   uint32_t est_w32, uint32_t nseg,
-                                                   size_t msg_bytes) {
-  return generic_smem_bytes(seg_emax, syn_w32, est_w32, nseg, msg_bytes);
-}
-
-template <class A>
-__device__ __forceinline__ GenericSmem<A> carve_items(unsigned char* base, const DecodeParams& P) {
-  GenericSmem<A> s;
-  const size_t msg =
-      (static_cast<size_t>(P.seg_emax + kPadEdges) * sizeof(typename A::Msg) + 15) & ~size_t(15);
-  s.q = reinterpret_cast<typename A::Msg*>(base);
-  s.r = reinterpret_cast<typename A::Msg*>(base + msg);
-  uint32_t* w = reinterpret_cast<uint32_t*>(base + 2 * msg);
-  s.syn = w;
-  s.par0 = w + P.syn_w32 + 2;
-  s.par1 = s.par0 + P.syn_w32;
-  s.res = s.par1 + P.syn_w32;
-  s.ehat = s.res + P.syn_w32;
-  s.segres = s.ehat + P.est_w32;
-  s.ticket = s.segres + 2 * P.nseg;
-  return s;
-}
-
 // ---- check-node update of one check over CSR edges [b, e1) ---------------
 
 __device__ __forceinline__ void cn_update(const DecodeParams& P, const float* q, float* r,

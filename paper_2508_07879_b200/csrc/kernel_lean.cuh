@@ -31,6 +31,8 @@
 
 namespace qb {
 
+constexpr uint32_t kNoShot = 0xffffffffu;
+
 // Message-block layout per arithmetic: byte stride between checks, byte offset
 // of the r half.  Strides are conflict-free for the check-side vector access of
 // 32 consecutive checks: fp32 3 x 64-bit at stride 14 words; fp16 / int16

@@ -500,109 +500,6 @@ decode_regular_kernel(const __grid_constant__ DecodeParams P, const __grid_const
   rewind_scheduler(io, tid);
 }
 
-// Batch kernel, work item = (shot, segment).  Segments are independent graphs, so
-// nothing forces the X and Z halves of a shot onto the same CTA: here each
-// persistent CTA serves ONE segment (its register tables are loaded once) and
-// draws shots from that segment's ticket counter, switching to another segment
-// only when its own queue is empty.  Compared with one-CTA-per-shot this (a) keeps
-// shared memory per CTA at one segment's messages, (b) removes the idle warps of
-// the half that converged first, and (c) lets a CTA be exactly as wide as one
-// segment needs.  Estimate / residual words that straddle a segment boundary are
-// merged into global memory with an atomicAnd + atomicOr pair that touches only
-// this segment's bits, so the two halves may finish in any order.
-template <class A, int CPT, int VPT, bool kFast, int MAXT, int MINB>
-__global__ void __launch_bounds__(MAXT, MINB)
-decode_items_kernel(const __grid_constant__ DecodeParams P, const __grid_constant__ ShotIO io) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const GenericSmem<A> S = carve_items<A>(smem_raw, P);
-  const uint32_t tid = threadIdx.x, nthr = blockDim.x;
-  const uint32_t nseg = P.nseg;
-  init_pads<A>(P, S, tid, P.seg_emax);
-
-  uint32_t s = blockIdx.x % nseg;
-  // CTAs b with b % nseg == s start on shots b / nseg; later tickets continue from there
-  uint64_t shot = blockIdx.x / nseg;
-  uint32_t tried = 0;
-  while (tried < nseg) {
-    const SegmentDev seg = P.segs[s];
-    const uint32_t peers = (gridDim.x - s + nseg - 1) / nseg;  // CTAs that started on s
-    RegTables<A, CPT, VPT, kFast> tab;
-    load_tables<A, CPT, VPT, kFast>(P, seg, tid, nthr, tab, seg.e0, P.seg_emax);
-    const uint32_t cw0 = seg.c0 >> 5, cw1 = (seg.c1 - 1) >> 5;
-    const uint32_t vw0 = seg.v0 >> 5, vw1 = (seg.v1 - 1) >> 5;
-    while (shot < io.nshots) {
-      // ---- prologue: this segment's syndrome words
-      const uint32_t* syn_g = io.syn + shot * P.syn_w32;
-      for (uint32_t w = cw0 + tid; w <= cw1; w += nthr) {
-        const uint32_t v = syn_g[w] & range_mask(w, 0, P.M);
-        S.syn[w] = v;
-        S.par0[w] = v;
-        S.par1[w] = v;
-        S.res[w] = 0;
-      }
-      for (uint32_t w = vw0 + tid; w <= vw1; w += nthr) S.ehat[w] = 0;
-      __syncthreads();
-      decode_segment_regular<A, CPT, VPT, kFast>(P, S, seg, s, tid, nthr, 1u, tab);
-      __syncthreads();
-      // ---- epilogue: own bits only
-      uint32_t* est_g = io.est + shot * P.est_w32;
-      for (uint32_t w = vw0 + tid; w <= vw1; w += nthr) {
-        const uint32_t mask = range_mask(w, seg.v0, seg.v1);
-        if (mask == 0xffffffffu) {
-          est_g[w] = S.ehat[w];
-        } else {
-          atomicAnd(&est_g[w], ~mask);
-          atomicOr(&est_g[w], S.ehat[w] & mask);
-        }
-      }
-      if (io.resid) {
-        uint32_t* res_g = io.resid + shot * P.syn_w32;
-        for (uint32_t w = cw0 + tid; w <= cw1; w += nthr) {
-          const uint32_t mask = range_mask(w, seg.c0, seg.c1);
-          if (mask == 0xffffffffu) {
-            res_g[w] = S.res[w];
-          } else {
-            atomicAnd(&res_g[w], ~mask);
-            atomicOr(&res_g[w], S.res[w] & mask);
-          }
-        }
-      }
-      if (tid == 0) {
-        io.conv[shot * nseg + s] = static_cast<uint8_t>(S.segres[2 * s]);
-        io.iters[shot * nseg + s] = S.segres[2 * s + 1];
-        const uint64_t nxt = static_cast<uint64_t>(atomicAdd(&io.sched[2 + s], 1u)) + peers;
-        S.ticket[0] = static_cast<uint32_t>(nxt);
-        S.ticket[1] = static_cast<uint32_t>(nxt >> 32);
-      }
-      __syncthreads();
-      shot = static_cast<uint64_t>(S.ticket[0]) | (static_cast<uint64_t>(S.ticket[1]) << 32);
-      tried = 0;
-    }
-    // own queue empty: help another segment
-    ++tried;
-    if (tried >= nseg) break;
-    s = (s + 1) % nseg;
-    __syncthreads();
-    if (tid == 0) {
-      const uint32_t peers2 = (gridDim.x - s + nseg - 1) / nseg;
-      const uint64_t nxt = static_cast<uint64_t>(atomicAdd(&io.sched[2 + s], 1u)) + peers2;
-      S.ticket[0] = static_cast<uint32_t>(nxt);
-      S.ticket[1] = static_cast<uint32_t>(nxt >> 32);
-    }
-    __syncthreads();
-    shot = static_cast<uint64_t>(S.ticket[0]) | (static_cast<uint64_t>(S.ticket[1]) << 32);
-  }
-  // the last CTA out rewinds every ticket counter for the next launch
-  if (tid == 0) {
-    __threadfence();
-    const unsigned int done = atomicAdd(&io.sched[1], 1u);
-    if (done == gridDim.x - 1) {
-      for (uint32_t k = 0; k < 2 + kMaxSegments; ++k) io.sched[k] = 0;
-      __threadfence();
-    }
-  }
-}
-
 // Latency kernel for ONE shot on a thread-block cluster: CTA rank s of the
 // cluster decodes segment s on its own SM (segments are independent graphs, so
 // the iteration loop needs no cross-CTA traffic at all); when a segment is done

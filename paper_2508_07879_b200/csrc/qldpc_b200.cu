@@ -20,7 +20,6 @@
 #include "common.cuh"
 #include "kernel_generic.cuh"
 #include "kernel_regular.cuh"
-#include "kernel_stream.cuh"
 #include "kernel_lean.cuh"
 #include "kernel_noise.cuh"
 #include "kernel_bw.cuh"
@@ -92,7 +91,6 @@ struct LaunchPlan {
   int ctas_per_sm = 1;
   size_t smem = 0;
   bool items = false;          // work item = (shot, segment): grid-stride over per-segment queues
-  bool stream = false;         // ... with K slots per CTA and continuous batching
   bool lean = false;           // ... the instruction-lean single-slot variant
 };
 
@@ -137,8 +135,6 @@ struct qb_decoder {
   uint64_t launches = 0;
   std::string err;
   size_t smem_bytes = 0;
-  size_t smem_items = 0;
-  size_t smem_stream = 0;
   size_t smem_lean = 0;
 };
 
@@ -280,80 +276,51 @@ KernelFn regular_kernel_t(int npt, bool cluster, bool fast) {
   return fast ? regular_kernel_tf<A, true>(npt, cluster) : regular_kernel_tf<A, false>(npt, cluster);
 }
 
-template <class A, bool kFast>
-KernelFn items_kernel_tf(int npt) {
-  switch (npt) {
-    case 1: return decode_items_kernel<A, 1, 2, kFast, 1024, 1>;
-    case 2: return decode_items_kernel<A, 2, 4, kFast, 512, 2>;
-    default: return decode_items_kernel<A, 4, 8, kFast, 256, 4>;
-  }
-}
-
-constexpr int kStreamSlots = 2;
-
-template <class A, bool kFast>
-KernelFn stream_kernel_tf(int npt) {
-  switch (npt) {
-    case 1: return decode_stream_kernel<A, 1, 2, kFast, kStreamSlots, 1024, 1>;
-    case 2: return decode_stream_kernel<A, 2, 4, kFast, kStreamSlots, 512, 2>;
-    default: return decode_stream_kernel<A, 4, 8, kFast, kStreamSlots, 256, 4>;
-  }
-}
-
-KernelFn stream_kernel(int arith, int npt, bool fast) {
-  switch (arith) {
-    case QB_ARITH_FLOAT:
-      return fast ? stream_kernel_tf<ArithF32, true>(npt) : stream_kernel_tf<ArithF32, false>(npt);
-    case QB_ARITH_INT8:
-      return fast ? stream_kernel_tf<ArithI8, true>(npt) : stream_kernel_tf<ArithI8, false>(npt);
-    case QB_ARITH_INT16:
-      return fast ? stream_kernel_tf<ArithI16, true>(npt) : stream_kernel_tf<ArithI16, false>(npt);
-    default:
-      return fast ? stream_kernel_tf<ArithF16, true>(npt) : stream_kernel_tf<ArithF16, false>(npt);
-  }
-}
-
-template <class A, bool kFast>
-KernelFn lean_kernel_tf(int npt) {
-  switch (npt) {
-    case 1: return decode_lean_kernel<A, 1, 2, kFast, 1024, 1>;
-    case 2: return decode_lean_kernel<A, 2, 4, kFast, 512, 2>;
-    default: return decode_lean_kernel<A, 4, 8, kFast, 256, 4>;
-  }
-}
-
-KernelFn lean_kernel(int arith, int npt, bool fast) {
-  switch (arith) {
-    case QB_ARITH_FLOAT:
-      return fast ? lean_kernel_tf<ArithF32, true>(npt) : lean_kernel_tf<ArithF32, false>(npt);
-    case QB_ARITH_INT8:
-      return fast ? lean_kernel_tf<ArithI8, true>(npt) : lean_kernel_tf<ArithI8, false>(npt);
-    case QB_ARITH_INT16:
-      return fast ? lean_kernel_tf<ArithI16, true>(npt) : lean_kernel_tf<ArithI16, false>(npt);
-    default:
-      return fast ? lean_kernel_tf<ArithF16, true>(npt) : lean_kernel_tf<ArithF16, false>(npt);
-  }
-}
-
-KernelFn items_kernel(int arith, int npt, bool fast) {
-  switch (arith) {
-    case QB_ARITH_FLOAT:
-      return fast ? items_kernel_tf<ArithF32, true>(npt) : items_kernel_tf<ArithF32, false>(npt);
-    case QB_ARITH_INT8:
-      return fast ? items_kernel_tf<ArithI8, true>(npt) : items_kernel_tf<ArithI8, false>(npt);
-    case QB_ARITH_INT16:
-      return fast ? items_kernel_tf<ArithI16, true>(npt) : items_kernel_tf<ArithI16, false>(npt);
-    default:
-      return fast ? items_kernel_tf<ArithF16, true>(npt) : items_kernel_tf<ArithF16, false>(npt);
-  }
-}
-
 KernelFn regular_kernel(int arith, int npt, bool cluster, bool fast) {
   switch (arith) {
     case QB_ARITH_FLOAT: return regular_kernel_t<ArithF32>(npt, cluster, fast);
     case QB_ARITH_INT8: return regular_kernel_t<ArithI8>(npt, cluster, fast);
     case QB_ARITH_INT16: return regular_kernel_t<ArithI16>(npt, cluster, fast);
     default: return regular_kernel_t<ArithF16>(npt, cluster, fast);
+  }
+}
+
+// Lean item-kernel variants: (checks, variables) per thread, launch bounds.
+struct LeanVariant {
+  int cpt, vpt, maxt, minb;
+};
+constexpr LeanVariant kLeanVariants[] = {
+    {1, 2, 1024, 1},  // 1: widest CTA, any segment size up to 1024 checks
+    {1, 2, 448, 3},   // 2: 48 registers, three 13-warp CTAs per SM on [[784,24,24]]
+    {2, 4, 256, 3},   // 3
+    {3, 5, 192, 5},   // 4
+    {4, 8, 128, 6},   // 5
+    {2, 4, 512, 2},   // 6
+};
+constexpr int kNumLeanVariants = sizeof(kLeanVariants) / sizeof(kLeanVariants[0]);
+
+template <class A, bool kFast>
+KernelFn lean_kernel_tf(int variant) {
+  switch (variant) {
+    case 1: return decode_lean_kernel<A, 1, 2, kFast, 1024, 1>;
+    case 2: return decode_lean_kernel<A, 1, 2, kFast, 448, 3>;
+    case 3: return decode_lean_kernel<A, 2, 4, kFast, 256, 3>;
+    case 4: return decode_lean_kernel<A, 3, 5, kFast, 192, 5>;
+    case 5: return decode_lean_kernel<A, 4, 8, kFast, 128, 6>;
+    default: return decode_lean_kernel<A, 2, 4, kFast, 512, 2>;
+  }
+}
+
+KernelFn lean_kernel(int arith, int variant, bool fast) {
+  switch (arith) {
+    case QB_ARITH_FLOAT:
+      return fast ? lean_kernel_tf<ArithF32, true>(variant) : lean_kernel_tf<ArithF32, false>(variant);
+    case QB_ARITH_INT8:
+      return fast ? lean_kernel_tf<ArithI8, true>(variant) : lean_kernel_tf<ArithI8, false>(variant);
+    case QB_ARITH_INT16:
+      return fast ? lean_kernel_tf<ArithI16, true>(variant) : lean_kernel_tf<ArithI16, false>(variant);
+    default:
+      return fast ? lean_kernel_tf<ArithF16, true>(variant) : lean_kernel_tf<ArithF16, false>(variant);
   }
 }
 
@@ -374,10 +341,7 @@ uint32_t regular_group_threads(const DecodeParams& P, uint32_t cpt, uint32_t vpt
 void finish_plan(qb_decoder* h, LaunchPlan& pl) {
   pl.block = pl.cluster ? pl.group_threads : pl.ngroups * pl.group_threads;
   if (pl.items) pl.block = pl.group_threads;
-  pl.smem = pl.lean     ? h->smem_lean
-            : pl.stream ? h->smem_stream
-            : pl.items  ? h->smem_items
-                        : h->smem_bytes;
+  pl.smem = pl.lean ? h->smem_lean : h->smem_bytes;
   CUDA_TRY(cudaFuncSetAttribute(pl.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(pl.smem)));
   if (pl.cluster) {
@@ -446,36 +410,36 @@ void make_plans(qb_decoder* h) {
   }
   if (!lat_done) h->lat = generic_plan(h);
   bool bat_done = false;
-  const int first = h->opt_batch_npt ? static_cast<int>(h->opt_batch_npt) : 1;
   const bool fast = h->fast_ok && h->opt_fast != 0;
-  for (int npt : {first, 1, 2, 4}) {
-    if (h->opt_batch_shape != 1) {  // work item = (shot, segment)
-      const uint32_t T = regular_group_threads(P, npt, 2 * npt);
-      if (T > max_block[npt]) continue;
-      LaunchPlan pl{};
-      pl.regular = true;
-      pl.items = true;
-      pl.npt = npt;
-      const bool lean_ok = P.seg_mmax <= 960;
-      pl.lean = lean_ok && (h->opt_batch_shape == 0 || h->opt_batch_shape == 4);
-      pl.stream = !pl.lean && h->opt_batch_shape != 2;
-      pl.kernel = pl.lean     ? lean_kernel(h->arith, npt, fast)
-                  : pl.stream ? stream_kernel(h->arith, npt, fast)
-                              : items_kernel(h->arith, npt, fast);
-      pl.name = pl.lean     ? "decode_lean_kernel"
-                : pl.stream ? "decode_stream_kernel"
-                            : "decode_items_kernel";
-      pl.ngroups = 1;
-      pl.group_threads = T;
-      finish_plan(h, pl);
-      h->bat = pl;
-      bat_done = true;
-      break;
+  if (h->opt_batch_shape != 1 && P.seg_mmax <= 960) {
+    // work item = (shot, segment): lean item kernel; first variant whose CTA fits
+    const int order_auto[] = {4, 3, 5, 2, 6, 1};
+    for (int idx = 0; idx < kNumLeanVariants && !bat_done; ++idx) {
+      const int variant = h->opt_batch_npt ? static_cast<int>(h->opt_batch_npt) : order_auto[idx];
+      const LeanVariant& lv = kLeanVariants[variant - 1];
+      const uint32_t T = regular_group_threads(P, lv.cpt, lv.vpt);
+      if (T <= static_cast<uint32_t>(lv.maxt)) {
+        LaunchPlan pl{};
+        pl.regular = true;
+        pl.items = true;
+        pl.lean = true;
+        pl.npt = variant;
+        pl.kernel = lean_kernel(h->arith, variant, fast);
+        pl.name = "decode_lean_kernel";
+        pl.ngroups = 1;
+        pl.group_threads = T;
+        finish_plan(h, pl);
+        h->bat = pl;
+        bat_done = true;
+      } else if (h->opt_batch_npt) {
+        fail(QB_INVALID_ARGUMENT, "requested batch kernel variant does not fit this code");
+      }
     }
-    if (fits(npt, false)) {
+  }
+  for (int npt : {2, 4, 1}) {
+    if (!bat_done && fits(npt, false)) {
       h->bat = regular_plan(npt, false);
       bat_done = true;
-      break;
     }
   }
   if (!bat_done) h->bat = generic_plan(h);
@@ -521,15 +485,12 @@ unsigned batch_grid(qb_decoder* h, uint64_t shots) {
   int per_sm = h->bat.ctas_per_sm;
   if (h->opt_batch_ctas > 0) per_sm = std::min<int>(per_sm, static_cast<int>(h->opt_batch_ctas));
   const uint64_t resident = static_cast<uint64_t>(per_sm) * h->sm_count;
-  if (h->bat.stream) {
-    // equal numbers of CTAs per segment; no more CTAs than there are slot-fuls of shots
+  if (h->bat.items) {  // equal numbers of CTAs per segment
     const uint64_t nseg = h->P.nseg;
-    const uint64_t per_seg = std::max<uint64_t>(
-        1, std::min<uint64_t>(resident / nseg, (shots + kStreamSlots - 1) / kStreamSlots));
+    const uint64_t per_seg = std::max<uint64_t>(1, std::min<uint64_t>(resident / nseg, shots));
     return static_cast<unsigned>(per_seg * nseg);
   }
-  const uint64_t items = h->bat.items ? shots * h->P.nseg : shots;
-  return static_cast<unsigned>(std::min<uint64_t>(items, resident));
+  return static_cast<unsigned>(std::min<uint64_t>(shots, resident));
 }
 
 void run_batch_device(qb_decoder* h, uint64_t shots, const uint32_t* d_syn, uint32_t* d_est,
@@ -857,13 +818,10 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
       P.seg_emax = std::max(P.seg_emax, P.segs[k].e1 - P.segs[k].e0);
     }
     h->smem_bytes = generic_smem_bytes(E, P.syn_w32, P.est_w32, P.nseg, msg_bytes_of(arith));
-    h->smem_items =
-        items_smem_bytes(P.seg_emax, P.syn_w32, P.est_w32, P.nseg, msg_bytes_of(arith));
     P.seg_mmax = 0;
     for (uint32_t k = 0; k < P.nseg; ++k) {
       P.seg_mmax = std::max(P.seg_mmax, P.segs[k].c1 - P.segs[k].c0);
     }
-    h->smem_stream = stream_smem_bytes(P.seg_emax, P.seg_mmax, msg_bytes_of(arith), kStreamSlots);
     h->smem_lean = lean_smem_bytes(P.seg_mmax, arith == QB_ARITH_HALF ? 3 : arith);
     if (h->smem_bytes > static_cast<size_t>(h->max_smem_optin)) {
       fail(QB_INVALID_ARGUMENT, "graph needs " + std::to_string(h->smem_bytes) +
@@ -957,14 +915,14 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
         if (value < 0 || value > 2) fail(QB_INVALID_ARGUMENT, "QB_OPT_KERNEL: 0, 1 or 2");
         h->opt_kernel = value;
         break;
-      case QB_OPT_BATCH_NODES_PER_THREAD:
-        if (value != 0 && value != 1 && value != 2 && value != 4) {
-          fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_NODES_PER_THREAD: 0, 1, 2 or 4");
+      case QB_OPT_BATCH_VARIANT:
+        if (value < 0 || value > kNumLeanVariants) {
+          fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_VARIANT: 0 .. 6");
         }
         h->opt_batch_npt = value;
         break;
       case QB_OPT_BATCH_SHAPE:
-        if (value < 0 || value > 4) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_SHAPE: 0 .. 4");
+        if (value < 0 || value > 2) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_SHAPE: 0, 1 or 2");
         h->opt_batch_shape = value;
         break;
       case QB_OPT_FAST_PATH:
@@ -1007,7 +965,7 @@ int64_t qb_get_option(const qb_decoder* h, int option) {
     case QB_OPT_LATENCY_IO: return h->opt_latency_io;
     case QB_OPT_LATENCY_SHAPE: return h->opt_latency_shape;
     case QB_OPT_GROUP_THREADS: return h->lat.group_threads;
-    case QB_OPT_BATCH_NODES_PER_THREAD: return h->bat.regular ? h->bat.npt : 0;
+    case QB_OPT_BATCH_VARIANT: return h->bat.regular ? h->bat.npt : 0;
     case QB_OPT_LATENCY_NODES_PER_THREAD: return h->lat.regular ? h->lat.npt : 0;
     case QB_OPT_INFO_BATCH_CTAS_PER_SM: return h->bat.ctas_per_sm;
     case QB_OPT_INFO_BATCH_BLOCK: return h->bat.block;
@@ -1015,7 +973,7 @@ int64_t qb_get_option(const qb_decoder* h, int option) {
     case QB_OPT_INFO_LATENCY_CLUSTER: return h->lat.cluster ? 1 : 0;
     case QB_OPT_INFO_BATCH_REGULAR: return h->bat.regular ? 1 : 0;
     case QB_OPT_FAST_PATH: return h->opt_fast;
-    case QB_OPT_BATCH_SHAPE: return h->bat.lean ? 4 : h->bat.stream ? 3 : h->bat.items ? 2 : 1;
+    case QB_OPT_BATCH_SHAPE: return h->bat.lean ? 2 : 1;
     case QB_OPT_INFO_FAST_ELIGIBLE: return h->fast_ok ? 1 : 0;
     case QB_OPT_BATCH_CTAS_PER_SM: return h->opt_batch_ctas;
     default: return -1;

@@ -314,10 +314,10 @@ def test_regular_and_cluster_kernels_match_oracle(oracle, name, mode):
                     dec.set_option(OPT_LATENCY_NPT, npt)
                     assert_matches_oracle(oracle, g, cfg, syn[:6], code.segments, dec=dec,
                                           messages=True)
-            for bshape in (1, 2, 3, 4):  # CTA per shot / (shot, segment) item / streaming / lean
+            for bshape in (1, 2):  # CTA per shot / CTA per (shot, segment) work item
                 dec.set_option(OPT_BATCH_SHAPE, bshape)
                 assert dec.get_option(OPT_BATCH_SHAPE) == bshape
-                for npt in (1, 2, 4):
+                for npt in ((0,) if bshape == 1 else (1, 2, 3, 4, 5, 6)):
                     dec.set_option(OPT_BATCH_NPT, npt)
                     for fast in (1, 0):
                         dec.set_option(OPT_FAST_PATH, fast)

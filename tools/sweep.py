@@ -9,7 +9,7 @@ ap.add_argument("--code", default="bb784")
 ap.add_argument("--shots", type=int, default=1 << 19)
 ap.add_argument("--p", type=float, default=0.01)
 ap.add_argument("--ariths", default="float,int8,half,int16")
-ap.add_argument("--npts", default="1,2,4")
+ap.add_argument("--npts", default="1,2,3,4,5,6")
 ap.add_argument("--ctas", default="0")
 ap.add_argument("--iters", default="50:1,10:0")
 ap.add_argument("--kernel", type=int, default=0)
