@@ -83,12 +83,16 @@ typedef struct qb_decoder qb_decoder;
 
 /* Kernel selection and I/O policy knobs (qb_set_option). */
 typedef enum {
-  /* 0 = auto, 1 = generic CSR kernel, 2 = regular (ELL, register-resident
-   * tables) kernel.  Selecting 2 on a graph it cannot run is an error. */
+  /* 0 = auto, 1 = generic CSR kernel, 2 = regular (register-resident tables)
+   * kernels; selecting 2 on a graph they cannot run is an error.  3 = like 0
+   * but without the lean single-shot cluster kernel (regular v2 kernels). */
   QB_OPT_KERNEL = 0,
-  /* Single-shot I/O: 0 = mapped pinned host memory + completion flag (no
-   * memcpy, no stream sync), 1 = cudaMemcpyAsync H2D / kernel / D2H + stream
-   * synchronize (the reference paper's protocol). */
+  /* Single-shot I/O: 0 = syndrome in the kernel parameters, results to mapped
+   * pinned host memory + completion flag (no memcpy, no stream sync);
+   * 1 = cudaMemcpyAsync H2D / kernel / D2H + stream synchronize (the reference
+   * paper's protocol); 2 = persistent doorbell: a resident
+   * cluster polls a block of mapped host memory, so a decode costs no kernel
+   * launch at all (the kernel retires after QB_OPT_DOORBELL_IDLE_MS idle). */
   QB_OPT_LATENCY_IO = 1,
   /* Single-shot launch shape: 0 = auto, 1 = one CTA per shot, 2 = one thread
    * block cluster per shot (one CTA per segment, results merged over DSMEM). */
@@ -111,13 +115,15 @@ typedef enum {
    * (one warp group per segment), 2 = one CTA per (shot, segment) work item
    * drawn from per-segment queues (the lean item kernel; the auto choice). */
   QB_OPT_BATCH_SHAPE = 8,
+  QB_OPT_DOORBELL_IDLE_MS = 9,
   /* Read-only (qb_get_option): the launch plans actually in use. */
   QB_OPT_INFO_BATCH_CTAS_PER_SM = 100,
   QB_OPT_INFO_BATCH_BLOCK = 101,
   QB_OPT_INFO_LATENCY_BLOCK = 102,
   QB_OPT_INFO_LATENCY_CLUSTER = 103,
   QB_OPT_INFO_BATCH_REGULAR = 104,
-  QB_OPT_INFO_FAST_ELIGIBLE = 105
+  QB_OPT_INFO_FAST_ELIGIBLE = 105,
+  QB_OPT_INFO_LATENCY_LEAN = 106
 } qb_option;
 
 /* Builds a decoder: validates like Decoder::Decoder (decoder.cpp:373-404,

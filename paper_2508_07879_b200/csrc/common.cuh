@@ -29,6 +29,7 @@ struct DecodeParams {
   uint32_t M, N, E, nseg;
   uint32_t seg_emax;  // edges of the largest segment
   uint32_t seg_mmax;  // checks of the largest segment
+  uint32_t seg_nmax;  // variables of the largest segment
   uint32_t syn_w32;  // 2 * ceil(M / 64): 32-bit words per packed syndrome
   uint32_t est_w32;  // 2 * ceil(N / 64): 32-bit words per packed estimate
   uint32_t max_iter;

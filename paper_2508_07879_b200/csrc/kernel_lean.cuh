@@ -445,4 +445,356 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
   }
 }
 
+// =============================================================================
+// Single-shot latency kernel: one thread-block CLUSTER per shot, CTA rank s
+// decodes segment s on its own SM (segments are independent graphs, so the
+// iteration loop needs no cross-CTA traffic).  DSMEM carries the control plane
+// and the result merge: the leader (rank 0) obtains the syndrome, drops each
+// rank's packed words and a "go" word into that rank's mailbox, every rank
+// decodes its segment with the lean item loop above, then deposits its
+// segment-local estimate / residual words and (converged, iterations) in the
+// leader's shared memory; after ONE cluster barrier the leader shifts the
+// pieces into the reference's packed layout, writes them to (mapped host)
+// memory, fences and raises the completion word.
+//
+// Three ways to obtain the syndrome (LatencyCtl::mode):
+//   0  passed BY VALUE in the kernel parameters (no load at all on the device);
+//   1  read from io.syn (device memory after an explicit H2D copy - the paper's
+//      protocol - or mapped host memory);
+//   2  PERSISTENT: the cluster stays resident and polls a doorbell block in
+//      mapped host memory; each 32-byte sector of the block carries the
+//      sequence number in its first word, so one 128-byte read that shows the
+//      expected number in all four sectors already holds a consistent syndrome
+//      (host: data words first, sequence words last).  Removes the kernel launch
+//      from the critical path; the kernel retires by itself after idle_ns.
+// =============================================================================
+
+constexpr uint32_t kInlineSynWords = 64;
+constexpr uint32_t kDoorbellWords = 32;         // one 128-byte block
+constexpr uint32_t kDoorbellDataPerSector = 7;  // words 1..7 of each 8-word sector
+constexpr uint32_t kDoorbellExit = 0xffffffffu;
+
+struct SynInline {
+  uint32_t w[kInlineSynWords];
+};
+
+struct LatencyCtl {
+  uint32_t mode;                    // 0 inline, 1 pointer, 2 persistent doorbell
+  uint32_t first_seq;               // sequence number of the first shot served
+  const volatile uint32_t* doorbell;  // mode 2: mapped host memory, kDoorbellWords words
+  volatile uint32_t* alive;         // mode 2: set to 0 (after a system fence) when the kernel retires
+  uint64_t idle_ns;                 // mode 2: retire after this long without a doorbell
+};
+
+__device__ __forceinline__ uint32_t ld_volatile_global(const volatile uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// position of packed syndrome word `idx` inside the doorbell block
+__host__ __device__ inline uint32_t doorbell_pos(uint32_t idx) {
+  return 8u * (idx / kDoorbellDataPerSector) + 1u + idx % kDoorbellDataPerSector;
+}
+
+struct LatMailbox {
+  uint32_t go;       // sequence number of the shot to decode (kDoorbellExit = retire)
+  uint32_t raw[32];  // this rank's packed syndrome words (global word gw0 + i)
+};
+
+template <class A, int CPT, int VPT, bool kFast>
+__global__ void __launch_bounds__(1024, 1)
+decode_lean_latency_kernel(const __grid_constant__ DecodeParams P,
+                           const __grid_constant__ ShotIO io,
+                           const __grid_constant__ LatencyCtl ctl,
+                           const __grid_constant__ SynInline syn_in) {
+  using Msg = typename A::Msg;
+  using Gam = typename A::Gam;
+  constexpr uint32_t kStride = Lay<A>::kStride;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const uint32_t tid = threadIdx.x, T = blockDim.x, lane = tid & 31u, warp = tid >> 5;
+  const uint32_t nseg = P.nseg;
+  const uint32_t s = cluster.block_rank();  // == segment
+  const SegmentDev seg = P.segs[s];
+  const uint32_t Ms = seg.c1 - seg.c0, Ns = seg.v1 - seg.v0;
+  const uint32_t pw = lean_pw(P.seg_mmax);       // words of a local check bitmap
+  const uint32_t ew = lean_pw(P.seg_nmax);       // words of a local variable bitmap
+  const uint32_t pws = (Ms + 31u) >> 5;
+  const uint32_t gw0 = seg.c0 >> 5, gspan = ((seg.c1 - 1) >> 5) - gw0 + 1, cshift = seg.c0 & 31u;
+
+  // ---- shared memory: messages | par | ehat | unsat | mailbox | (leader) result area + out
+  unsigned char* const msgs = smem_raw;
+  const size_t msg_bytes = (static_cast<size_t>(P.seg_mmax + 1) * kStride + 15) & ~size_t(15);
+  uint32_t* const bits = reinterpret_cast<uint32_t*>(smem_raw + msg_bytes);
+  uint32_t* const par = bits;                       // [pw]
+  uint32_t* const ehat = bits + pw;                 // [ew]
+  volatile uint32_t* const unsat = bits + pw + ew;  // [1] (+1 pad)
+  LatMailbox* const mbox = reinterpret_cast<LatMailbox*>(bits + pw + ew + 2);
+  uint32_t* const area = bits + pw + ew + 2 + 34;   // leader: [nseg][pw + ew + 2]
+  const uint32_t area_stride = pw + ew + 2;
+  uint32_t* const out_est = area + kMaxSegments * area_stride;  // leader: [est_w32]
+  uint32_t* const out_res = out_est + P.est_w32;                // leader: [syn_w32]
+
+  // ---- per-thread tables
+  uint32_t eo[VPT][kDV], co[CPT], cl[CPT], valid = 0;
+  Gam gam[kFast ? 1 : VPT];
+  {
+    const Gam* __restrict__ gamma = static_cast<const Gam*>(P.gamma);
+    const uint32_t dummy = P.seg_mmax * kStride;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const uint32_t n = seg.v0 + tid + k * T;
+      const bool ok = n < seg.v1;
+      valid |= (ok ? 1u : 0u) << k;
+#pragma unroll
+      for (int i = 0; i < kDV; ++i) {
+        const uint32_t e = ok ? P.var_edges[n * kDV + i] - seg.e0 : 0u;
+        eo[k][i] = ok ? (e / kDC) * kStride + (e % kDC) * static_cast<uint32_t>(sizeof(Msg))
+                      : dummy + i * static_cast<uint32_t>(sizeof(Msg));
+      }
+      if constexpr (!kFast) gam[k] = ok ? gamma[n] : static_cast<Gam>(1);
+    }
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+      const uint32_t m = tid + k * T;
+      cl[k] = m < Ms ? m : Ms;
+      co[k] = (m < Ms ? m : P.seg_mmax) * kStride;
+    }
+  }
+  for (uint32_t b = tid; b < kStride; b += T) msgs[P.seg_mmax * kStride + b] = 0;
+  if (tid == 0) mbox->go = ctl.first_seq - 1u;
+  __syncthreads();
+  cluster.sync();  // every mailbox is initialised before the leader may write into it
+
+  uint32_t last = ctl.first_seq - 1u;
+  uint64_t t_idle0 = globaltimer_ns();
+  for (;;) {
+    // ---------------- obtain the shot (leader) and hand it out ----------------
+    uint64_t t_begin = 0;
+    if (s == 0 && warp == 0) {
+      uint32_t cmd = last + 1u;
+      uint32_t val = 0;  // mode 2: doorbell word `lane`
+      if (ctl.mode == 2u) {
+        uint32_t spins = 0;
+        for (;;) {
+          val = ld_volatile_global(ctl.doorbell + lane);
+          const uint32_t sq = __shfl_sync(0xffffffffu, val, lane & ~7u);  // my sector's number
+          if (__all_sync(0xffffffffu, sq == cmd)) break;
+          if (__any_sync(0xffffffffu, sq == kDoorbellExit)) {
+            cmd = kDoorbellExit;
+            break;
+          }
+          if ((++spins & 63u) == 0u && globaltimer_ns() - t_idle0 > ctl.idle_ns) {
+            cmd = kDoorbellExit;
+            break;
+          }
+        }
+      }
+      t_begin = globaltimer_ns();
+      for (uint32_t r = 0; r < nseg; ++r) {
+        const SegmentDev sr = P.segs[r];
+        const uint32_t g0 = sr.c0 >> 5, span = ((sr.c1 - 1) >> 5) - g0 + 1;
+        uint32_t word = 0;
+        if (ctl.mode == 2u) {
+          const uint32_t src = lane < span ? doorbell_pos(g0 + lane) : 0u;
+          word = __shfl_sync(0xffffffffu, val, src & 31u);
+        } else if (lane < span) {
+          word = ctl.mode == 0u ? syn_in.w[g0 + lane] : io.syn[g0 + lane];
+        }
+        if (lane >= span) word = 0;
+        LatMailbox* mb = cluster.map_shared_rank(mbox, r);
+        mb->raw[lane] = word;
+      }
+      __threadfence();  // order the words before the go flags (cluster scope included)
+      if (lane < nseg) {
+        LatMailbox* mb = cluster.map_shared_rank(mbox, lane);
+        *reinterpret_cast<volatile uint32_t*>(&mb->go) = cmd;
+      }
+    }
+    // ---------------- wait for the go word ----------------
+    if (warp == 0) {
+      while (*reinterpret_cast<volatile uint32_t*>(&mbox->go) == last) {
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    const uint32_t cmd = *reinterpret_cast<volatile uint32_t*>(&mbox->go);
+    if (cmd == kDoorbellExit) break;
+
+    // ---------------- prologue ----------------
+    if (warp == 0) {
+      const uint32_t raw = mbox->raw[lane];
+      uint32_t nb = __shfl_down_sync(0xffffffffu, raw, 1);
+      if (lane + 1 >= gspan) nb = 0;
+      uint32_t loc = cshift ? __funnelshift_r(raw, nb, cshift) : raw;
+      if (lane >= pws) {
+        loc = 0;
+      } else if (Ms - lane * 32u < 32u) {
+        loc &= (1u << (Ms - lane * 32u)) - 1u;
+      }
+      if (lane < pw) par[lane] = loc;
+      const uint32_t cnt = __reduce_add_sync(0xffffffffu, __popc(loc));
+      if (lane == 0) *unsat = cnt;
+    }
+    for (uint32_t w = tid; w < ew; w += T) ehat[w] = 0;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      Gam g;
+      if constexpr (kFast) {
+        if constexpr (A::kInt) g = P.gamma_i; else g = P.gamma_f;
+      } else {
+        g = gam[k];
+      }
+      const Msg init = prior_as_msg<A>(g);
+#pragma unroll
+      for (int i = 0; i < kDV; ++i) *reinterpret_cast<Msg*>(msgs + eo[k][i]) = init;
+    }
+    uint32_t eprev = 0;
+    __syncthreads();
+    uint32_t synbits = 0;
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) synbits |= ((par[cl[k] >> 5] >> (cl[k] & 31u)) & 1u) << k;
+
+    // ---------------- iterations ----------------
+    uint32_t iter = 0;
+    bool still_unsat;
+    for (;;) {
+      ++iter;
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) cn6_block(P, A{}, msgs + co[k], (synbits >> k) & 1u);
+      __syncthreads();
+      uint32_t eb = 0;
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) {
+        Gam g{};
+        if constexpr (!kFast) g = gam[k];
+        eb |= vn3_off<kFast>(P, A{}, msgs, eo[k], g) << k;
+      }
+      eb &= valid;
+      const uint32_t changed = eb ^ eprev;
+      eprev = eb;
+      if (changed) {
+        int32_t delta = 0;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+          if ((changed >> k) & 1u) {
+#pragma unroll
+            for (int i = 0; i < kDV; ++i) {
+              const uint32_t lm = eo[k][i] / kStride;
+              const uint32_t bit = 1u << (lm & 31u);
+              const uint32_t old = atomicXor(&par[lm >> 5], bit);
+              delta += (old & bit) ? -1 : 1;
+            }
+          }
+        }
+        atomicAdd(const_cast<uint32_t*>(unsat), static_cast<uint32_t>(delta));
+      }
+      __syncthreads();
+      still_unsat = *unsat != 0u;
+      if ((P.early && !still_unsat) || iter >= P.max_iter) break;
+    }
+
+    // ---------------- deposit this segment's result with the leader ----------------
+    if (eprev) {
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) {
+        if ((eprev >> k) & 1u) {
+          const uint32_t nl = tid + k * T;
+          atomicOr(&ehat[nl >> 5], 1u << (nl & 31u));
+        }
+      }
+    }
+    if (io.q_dump) {  // debug: messages back in reference edge order
+      for (uint32_t e = tid; e < seg.e1 - seg.e0; e += T) {
+        const unsigned char* src = msgs + (e / kDC) * kStride + (e % kDC) * sizeof(Msg);
+        if constexpr (A::kInt) {
+          static_cast<int32_t*>(io.q_dump)[seg.e0 + e] = *reinterpret_cast<const Msg*>(src);
+          static_cast<int32_t*>(io.r_dump)[seg.e0 + e] =
+              *reinterpret_cast<const Msg*>(src + Lay<A>::kROff);
+        } else {
+          static_cast<float*>(io.q_dump)[seg.e0 + e] =
+              static_cast<float>(*reinterpret_cast<const Msg*>(src));
+          static_cast<float*>(io.r_dump)[seg.e0 + e] =
+              static_cast<float>(*reinterpret_cast<const Msg*>(src + Lay<A>::kROff));
+        }
+      }
+    }
+    __syncthreads();
+    {
+      uint32_t* dst = cluster.map_shared_rank(area, 0) + s * area_stride;
+      for (uint32_t w = tid; w < pw; w += T) dst[w] = par[w];
+      for (uint32_t w = tid; w < ew; w += T) dst[pw + w] = ehat[w];
+      if (tid == 0) {
+        dst[pw + ew] = still_unsat ? 0u : 1u;
+        dst[pw + ew + 1] = iter;
+      }
+    }
+    cluster.sync();
+
+    // ---------------- leader: merge into the packed layout and publish ----------------
+    if (s == 0) {
+      for (uint32_t w = tid; w < P.est_w32; w += T) out_est[w] = 0;
+      for (uint32_t w = tid; w < P.syn_w32; w += T) out_res[w] = 0;
+      __syncthreads();
+      // one warp per segment: local word w of segment r lands at global bit b0 + 32 w
+      for (uint32_t r = warp; r < nseg; r += (T >> 5)) {
+        const SegmentDev sr = P.segs[r];
+        const uint32_t* src = area + r * area_stride;
+        const uint32_t mr = sr.c1 - sr.c0, nr = sr.v1 - sr.v0;
+        for (uint32_t w = lane; w < ((mr + 31u) >> 5); w += 32u) {
+          const uint32_t v = src[w], b0 = sr.c0 + 32u * w, sh = b0 & 31u;
+          if (v) {
+            atomicOr(&out_res[b0 >> 5], v << sh);
+            if (sh && (v >> (32u - sh))) atomicOr(&out_res[(b0 >> 5) + 1], v >> (32u - sh));
+          }
+        }
+        for (uint32_t w = lane; w < ((nr + 31u) >> 5); w += 32u) {
+          const uint32_t v = src[pw + w], b0 = sr.v0 + 32u * w, sh = b0 & 31u;
+          if (v) {
+            atomicOr(&out_est[b0 >> 5], v << sh);
+            if (sh && (v >> (32u - sh))) atomicOr(&out_est[(b0 >> 5) + 1], v >> (32u - sh));
+          }
+        }
+      }
+      __syncthreads();
+      for (uint32_t w = tid; w < P.est_w32; w += T) io.est[w] = out_est[w];
+      if (io.resid) {
+        for (uint32_t w = tid; w < P.syn_w32; w += T) io.resid[w] = out_res[w];
+      }
+      if (tid < nseg) {
+        io.conv[tid] = static_cast<uint8_t>(area[tid * area_stride + pw + ew]);
+        io.iters[tid] = area[tid * area_stride + pw + ew + 1];
+      }
+      if (io.flag) {
+        __threadfence_system();
+        __syncthreads();
+        if (tid == 0) {
+          // warp 0 lane 0 took t_begin; it is thread 0
+          *io.kernel_ns = globaltimer_ns() - t_begin;
+          __threadfence_system();
+          *io.flag = cmd;
+        }
+      }
+      t_idle0 = globaltimer_ns();
+    }
+    last = cmd;
+    if (ctl.mode != 2u) break;
+  }
+  if (ctl.mode == 2u && s == 0 && tid == 0 && ctl.alive) {
+    *ctl.alive = 0u;
+    __threadfence_system();
+  }
+  cluster.sync();  // no CTA leaves while a peer may still address its shared memory
+}
+
+__host__ __device__ inline size_t lean_latency_smem_bytes(uint32_t seg_mmax, uint32_t seg_nmax,
+                                                          uint32_t syn_w32, uint32_t est_w32,
+                                                          int arith) {
+  const size_t msg = (static_cast<size_t>(seg_mmax + 1) * lean_stride(arith) + 15) & ~size_t(15);
+  const size_t pw = lean_pw(seg_mmax), ew = lean_pw(seg_nmax);
+  const size_t words = pw + ew + 2 + 34 + kMaxSegments * (pw + ew + 2) + est_w32 + syn_w32 + 8;
+  return msg + 4 * words;
+}
+
 }  // namespace qb

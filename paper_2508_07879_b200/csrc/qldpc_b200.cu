@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -78,6 +79,7 @@ size_t msg_bytes_of(int arith) {
 }  // namespace
 
 using KernelFn = void (*)(DecodeParams, ShotIO);
+using LatKernelFn = void (*)(DecodeParams, ShotIO, LatencyCtl, SynInline);
 
 struct LaunchPlan {
   KernelFn kernel = nullptr;
@@ -127,6 +129,14 @@ struct qb_decoder {
   // options
   int64_t opt_kernel = 0, opt_latency_io = 0, opt_latency_shape = 0, opt_group_threads = 0,
           opt_batch_ctas = 0, opt_batch_npt = 0, opt_latency_npt = 0, opt_batch_shape = 0;
+  // lean single-shot cluster kernel (kernel_lean.cuh) and its persistent doorbell mode
+  LatKernelFn lat_lean_kernel = nullptr;
+  unsigned lat_lean_block = 0;
+  size_t lat_lean_smem = 0;
+  uint32_t* h_db = nullptr;   // mapped: doorbell block [32] + alive word [32]
+  uint32_t* d_db = nullptr;
+  bool db_running = false;
+  int64_t opt_idle_ms = 200;
   bool regular63 = false;  // every check degree 6, every variable degree 3
   bool fast_ok = false;    // uniform prior (and, for fp32, provably clamp-free)
   int64_t opt_fast = 1;
@@ -154,6 +164,11 @@ void free_batch(qb_decoder* h) {
 void destroy(qb_decoder* h) {
   if (!h) return;
   cudaSetDevice(h->device);
+  if (h->db_running && h->h_db) {
+    volatile uint32_t* db = h->h_db;
+    for (int k = 0; k < 4; ++k) db[8 * k] = 0xffffffffu;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+  }
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (void* p : h->dev_allocs) cudaFree(p);
   cudaFree(h->d_sched);
@@ -162,6 +177,7 @@ void destroy(qb_decoder* h) {
   cudaFree(h->d_qdump);
   cudaFree(h->d_rdump);
   cudaFree(h->d_probs);
+  if (h->h_db) cudaFreeHost(h->h_db);
   if (h->h_in) cudaFreeHost(h->h_in);
   if (h->h_out) cudaFreeHost(h->h_out);
   free_batch(h);
@@ -324,6 +340,29 @@ KernelFn lean_kernel(int arith, int variant, bool fast) {
   }
 }
 
+template <class A, bool kFast>
+LatKernelFn lean_latency_kernel_tf(int npt) {
+  return npt == 1 ? decode_lean_latency_kernel<A, 1, 2, kFast>
+                  : decode_lean_latency_kernel<A, 2, 4, kFast>;
+}
+
+LatKernelFn lean_latency_kernel(int arith, int npt, bool fast) {
+  switch (arith) {
+    case QB_ARITH_FLOAT:
+      return fast ? lean_latency_kernel_tf<ArithF32, true>(npt)
+                  : lean_latency_kernel_tf<ArithF32, false>(npt);
+    case QB_ARITH_INT8:
+      return fast ? lean_latency_kernel_tf<ArithI8, true>(npt)
+                  : lean_latency_kernel_tf<ArithI8, false>(npt);
+    case QB_ARITH_INT16:
+      return fast ? lean_latency_kernel_tf<ArithI16, true>(npt)
+                  : lean_latency_kernel_tf<ArithI16, false>(npt);
+    default:
+      return fast ? lean_latency_kernel_tf<ArithF16, true>(npt)
+                  : lean_latency_kernel_tf<ArithF16, false>(npt);
+  }
+}
+
 uint32_t round_up32(uint32_t x) { return (x + 31u) & ~31u; }
 
 // Threads per segment group so that T*cpt covers the checks and T*vpt the
@@ -399,6 +438,24 @@ void make_plans(qb_decoder* h) {
   // single shot: fewest nodes per thread that fits; a cluster when there is more
   // than one segment (unless the caller pins the shape)
   const bool want_cluster = h->opt_latency_shape == 2 || (h->opt_latency_shape == 0 && P.nseg > 1);
+  h->lat_lean_kernel = nullptr;
+  if (h->opt_latency_shape != 1 && h->opt_kernel != 3 && P.seg_mmax <= 960 &&
+      P.seg_nmax <= 960 * 2 && P.syn_w32 <= kInlineSynWords) {
+    for (int npt : {1, 2}) {
+      if (h->opt_latency_npt && npt != h->opt_latency_npt) continue;
+      const uint32_t T = regular_group_threads(P, npt, 2 * npt);
+      if (T > 1024) continue;
+      h->lat_lean_kernel =
+          lean_latency_kernel(h->arith, npt, h->fast_ok && h->opt_fast != 0);
+      h->lat_lean_block = T;
+      h->lat_lean_smem = lean_latency_smem_bytes(P.seg_mmax, P.seg_nmax, P.syn_w32, P.est_w32,
+                                                 h->arith == QB_ARITH_HALF ? 3 : h->arith);
+      CUDA_TRY(cudaFuncSetAttribute(h->lat_lean_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(h->lat_lean_smem)));
+      break;
+    }
+  }
   bool lat_done = false;
   for (int npt : {1, 2, 4}) {
     if (h->opt_latency_npt && npt != h->opt_latency_npt) continue;
@@ -526,14 +583,71 @@ qb_status guarded(qb_decoder* h, F&& f) {
   }
 }
 
+void launch_lean_latency(qb_decoder* h, const ShotIO& io, const LatencyCtl& ctl,
+                         const SynInline& syn) {
+  DecodeParams P = h->P;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(P.nseg);
+  cfg.blockDim = dim3(h->lat_lean_block);
+  cfg.dynamicSmemBytes = h->lat_lean_smem;
+  cfg.stream = h->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = P.nseg;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, h->lat_lean_kernel, P, io, ctl, syn));
+  ++h->launches;
+}
+
+// Retires the persistent doorbell kernel (if any) and waits for it.
+void stop_doorbell(qb_decoder* h) {
+  if (!h->db_running) return;
+  volatile uint32_t* db = h->h_db;
+  for (int k = 0; k < 4; ++k) db[8 * k] = kDoorbellExit;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  cudaStreamSynchronize(h->stream);
+  h->db_running = false;
+}
+
+void spin_for_flag(qb_decoder* h, volatile uint32_t* h_flag, uint32_t seq, bool persistent) {
+  // Spin on the completion word the kernel writes last; no stream sync on the
+  // fast path.  A watchdog falls back to the runtime for diagnosis.
+  const auto t0 = std::chrono::steady_clock::now();
+  uint64_t spins = 0;
+  while (*h_flag != seq) {
+    if ((++spins & 0xffff) == 0) {
+      const cudaError_t q = cudaStreamQuery(h->stream);
+      if (q != cudaErrorNotReady) {
+        CUDA_TRY(cudaStreamSynchronize(h->stream));
+        if (*h_flag == seq) break;
+        if (persistent) {
+          h->db_running = false;  // retired while we were ringing: caller relaunches
+          fail(QB_RUNTIME_ERROR, "doorbell kernel retired");
+        }
+        fail(QB_RUNTIME_ERROR, "decode kernel finished without signalling completion");
+      }
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20)) {
+        fail(QB_RUNTIME_ERROR, "decode kernel timed out");
+      }
+    }
+  }
+}
+
 void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, uint64_t* residual,
                  uint8_t* converged, uint32_t* iterations, bool debug) {
   const DecodeParams& P = h->P;
   if (!syndrome || !estimate || !converged || !iterations) {
     fail(QB_INVALID_ARGUMENT, "decode: NULL buffer");
   }
-  std::memcpy(h->h_in, syndrome, P.syn_w32 * 4);
+  const int io_mode = static_cast<int>(h->opt_latency_io);
+  const bool lean = h->lat_lean_kernel != nullptr;
+  const bool doorbell = io_mode == 2 && lean && !debug && P.syn_w32 <= 28;
+  if (!doorbell) stop_doorbell(h);
   const uint32_t seq = ++h->seq;
+  if (seq == kDoorbellExit) h->seq = 0;
   ShotIO io{};
   io.nshots = 1;
   io.sched = h->d_sched;
@@ -543,9 +657,8 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
     io.r_dump = h->d_rdump;
   }
   volatile uint32_t* h_flag = reinterpret_cast<volatile uint32_t*>(h->h_out + h->off_flag);
-  const bool mapped = h->opt_latency_io == 0;
+  const bool mapped = io_mode != 1;
   unsigned char* out = mapped ? h->d_out_map : h->d_out_dev;
-  io.syn = mapped ? h->d_in_map : h->d_in_dev;
   io.est = reinterpret_cast<uint32_t*>(out);
   io.resid = reinterpret_cast<uint32_t*>(out + h->off_res);
   io.conv = out + h->off_conv;
@@ -553,31 +666,71 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
   io.kernel_ns = reinterpret_cast<uint64_t*>(out + h->off_ns);
   io.flag = reinterpret_cast<volatile uint32_t*>(out + h->off_flag);
 
-  if (mapped) {
-    launch_plan(h, h->lat, io, h->lat.cluster ? h->P.nseg : 1, h->stream);
-    // Spin on the completion word the kernel writes last; no stream sync on
-    // the fast path.  A watchdog falls back to the runtime for diagnosis.
-    const auto t0 = std::chrono::steady_clock::now();
-    uint64_t spins = 0;
-    while (*h_flag != seq) {
-      if ((++spins & 0xffff) == 0) {
-        if (cudaStreamQuery(h->stream) != cudaErrorNotReady) {
-          CUDA_TRY(cudaStreamSynchronize(h->stream));
-          if (*h_flag == seq) break;
-          fail(QB_RUNTIME_ERROR, "decode kernel finished without signalling completion");
-        }
-        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20)) {
-          fail(QB_RUNTIME_ERROR, "decode kernel timed out");
-        }
+  if (doorbell) {
+    // ---- persistent cluster: ring the doorbell, spin on the completion word
+    volatile uint32_t* db = h->h_db;
+    volatile uint32_t* alive = h->h_db + 32;
+    const uint32_t* syn32 = reinterpret_cast<const uint32_t*>(syndrome);
+    for (int attempt = 0;; ++attempt) {
+      if (!h->db_running || *alive == 0u) {
+        if (h->db_running) CUDA_TRY(cudaStreamSynchronize(h->stream));
+        for (int k = 0; k < 32; ++k) db[k] = 0;
+        *alive = 1u;
+        std::atomic_thread_fence(std::memory_order_seq_cst);
+        LatencyCtl ctl{};
+        ctl.mode = 2;
+        ctl.first_seq = seq;
+        ctl.doorbell = h->d_db;
+        ctl.alive = h->d_db + 32;
+        ctl.idle_ns = static_cast<uint64_t>(h->opt_idle_ms) * 1000000ull;
+        SynInline none{};
+        launch_lean_latency(h, io, ctl, none);
+        h->db_running = true;
+      }
+      for (uint32_t i = 0; i < P.syn_w32; ++i) db[doorbell_pos(i)] = syn32[i];
+      std::atomic_thread_fence(std::memory_order_release);
+      for (int k = 0; k < 4; ++k) db[8 * k] = seq;
+      try {
+        spin_for_flag(h, h_flag, seq, true);
+        break;
+      } catch (const StatusError&) {
+        if (h->db_running || attempt >= 2) throw;  // a real failure, or retiring repeatedly
       }
     }
+  } else if (lean) {
+    LatencyCtl ctl{};
+    ctl.first_seq = seq;
+    SynInline syn{};
+    if (mapped) {
+      ctl.mode = 0;  // syndrome travels in the kernel parameters
+      std::memcpy(syn.w, syndrome, P.syn_w32 * 4);
+      launch_lean_latency(h, io, ctl, syn);
+      spin_for_flag(h, h_flag, seq, false);
+    } else {
+      ctl.mode = 1;  // the paper's protocol: H2D copy, kernel, D2H copy, synchronize
+      std::memcpy(h->h_in, syndrome, P.syn_w32 * 4);
+      io.syn = h->d_in_dev;
+      CUDA_TRY(cudaMemcpyAsync(h->d_in_dev, h->h_in, P.syn_w32 * 4, cudaMemcpyHostToDevice,
+                               h->stream));
+      launch_lean_latency(h, io, ctl, syn);
+      CUDA_TRY(cudaMemcpyAsync(h->h_out, h->d_out_dev, h->out_bytes, cudaMemcpyDeviceToHost,
+                               h->stream));
+      CUDA_TRY(cudaStreamSynchronize(h->stream));
+    }
   } else {
-    CUDA_TRY(cudaMemcpyAsync(h->d_in_dev, h->h_in, P.syn_w32 * 4, cudaMemcpyHostToDevice,
-                             h->stream));
-    launch_plan(h, h->lat, io, h->lat.cluster ? h->P.nseg : 1, h->stream);
-    CUDA_TRY(cudaMemcpyAsync(h->h_out, h->d_out_dev, h->out_bytes, cudaMemcpyDeviceToHost,
-                             h->stream));
-    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    std::memcpy(h->h_in, syndrome, P.syn_w32 * 4);
+    io.syn = mapped ? h->d_in_map : h->d_in_dev;
+    if (mapped) {
+      launch_plan(h, h->lat, io, h->lat.cluster ? h->P.nseg : 1, h->stream);
+      spin_for_flag(h, h_flag, seq, false);
+    } else {
+      CUDA_TRY(cudaMemcpyAsync(h->d_in_dev, h->h_in, P.syn_w32 * 4, cudaMemcpyHostToDevice,
+                               h->stream));
+      launch_plan(h, h->lat, io, h->lat.cluster ? h->P.nseg : 1, h->stream);
+      CUDA_TRY(cudaMemcpyAsync(h->h_out, h->d_out_dev, h->out_bytes, cudaMemcpyDeviceToHost,
+                               h->stream));
+      CUDA_TRY(cudaStreamSynchronize(h->stream));
+    }
   }
   std::memcpy(estimate, h->h_out, P.est_w32 * 4);
   if (residual) std::memcpy(residual, h->h_out + h->off_res, P.syn_w32 * 4);
@@ -819,8 +972,10 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
     }
     h->smem_bytes = generic_smem_bytes(E, P.syn_w32, P.est_w32, P.nseg, msg_bytes_of(arith));
     P.seg_mmax = 0;
+    P.seg_nmax = 0;
     for (uint32_t k = 0; k < P.nseg; ++k) {
       P.seg_mmax = std::max(P.seg_mmax, P.segs[k].c1 - P.segs[k].c0);
+      P.seg_nmax = std::max(P.seg_nmax, P.segs[k].v1 - P.segs[k].v0);
     }
     h->smem_lean = lean_smem_bytes(P.seg_mmax, arith == QB_ARITH_HALF ? 3 : arith);
     if (h->smem_bytes > static_cast<size_t>(h->max_smem_optin)) {
@@ -893,6 +1048,9 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
     std::memset(h->h_out, 0, h->out_bytes);
     CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_in_map), h->h_in, 0));
     CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_out_map), h->h_out, 0));
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h->h_db), 64 * 4, cudaHostAllocMapped));
+    std::memset(h->h_db, 0, 64 * 4);
+    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_db), h->h_db, 0));
     CUDA_TRY(cudaMalloc(&h->d_in_dev, P.syn_w32 * 4));
     CUDA_TRY(cudaMalloc(&h->d_out_dev, h->out_bytes));
     CUDA_TRY(cudaMemset(h->d_out_dev, 0, h->out_bytes));
@@ -912,7 +1070,7 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
   return guarded(h, [&] {
     switch (option) {
       case QB_OPT_KERNEL:
-        if (value < 0 || value > 2) fail(QB_INVALID_ARGUMENT, "QB_OPT_KERNEL: 0, 1 or 2");
+        if (value < 0 || value > 3) fail(QB_INVALID_ARGUMENT, "QB_OPT_KERNEL: 0 .. 3");
         h->opt_kernel = value;
         break;
       case QB_OPT_BATCH_VARIANT:
@@ -925,6 +1083,11 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
         if (value < 0 || value > 2) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_SHAPE: 0, 1 or 2");
         h->opt_batch_shape = value;
         break;
+      case QB_OPT_DOORBELL_IDLE_MS:
+        if (value < 1 || value > 60000) fail(QB_INVALID_ARGUMENT, "QB_OPT_DOORBELL_IDLE_MS: 1..60000");
+        stop_doorbell(h);
+        h->opt_idle_ms = value;
+        break;
       case QB_OPT_FAST_PATH:
         if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_FAST_PATH: 0 or 1");
         h->opt_fast = value;
@@ -936,7 +1099,8 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
         h->opt_latency_npt = value;
         break;
       case QB_OPT_LATENCY_IO:
-        if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_LATENCY_IO: 0 or 1");
+        if (value < 0 || value > 2) fail(QB_INVALID_ARGUMENT, "QB_OPT_LATENCY_IO: 0, 1 or 2");
+        stop_doorbell(h);
         h->opt_latency_io = value;
         break;
       case QB_OPT_LATENCY_SHAPE:
@@ -954,6 +1118,7 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
       default:
         fail(QB_INVALID_ARGUMENT, "unknown option");
     }
+    stop_doorbell(h);
     make_plans(h);
   });
 }
@@ -969,12 +1134,14 @@ int64_t qb_get_option(const qb_decoder* h, int option) {
     case QB_OPT_LATENCY_NODES_PER_THREAD: return h->lat.regular ? h->lat.npt : 0;
     case QB_OPT_INFO_BATCH_CTAS_PER_SM: return h->bat.ctas_per_sm;
     case QB_OPT_INFO_BATCH_BLOCK: return h->bat.block;
-    case QB_OPT_INFO_LATENCY_BLOCK: return h->lat.block;
-    case QB_OPT_INFO_LATENCY_CLUSTER: return h->lat.cluster ? 1 : 0;
+    case QB_OPT_INFO_LATENCY_BLOCK: return h->lat_lean_kernel ? h->lat_lean_block : h->lat.block;
+    case QB_OPT_INFO_LATENCY_CLUSTER: return (h->lat_lean_kernel || h->lat.cluster) ? 1 : 0;
     case QB_OPT_INFO_BATCH_REGULAR: return h->bat.regular ? 1 : 0;
     case QB_OPT_FAST_PATH: return h->opt_fast;
     case QB_OPT_BATCH_SHAPE: return h->bat.lean ? 2 : 1;
     case QB_OPT_INFO_FAST_ELIGIBLE: return h->fast_ok ? 1 : 0;
+    case QB_OPT_DOORBELL_IDLE_MS: return h->opt_idle_ms;
+    case QB_OPT_INFO_LATENCY_LEAN: return h->lat_lean_kernel ? 1 : 0;
     case QB_OPT_BATCH_CTAS_PER_SM: return h->opt_batch_ctas;
     default: return -1;
   }

@@ -63,7 +63,7 @@ def test_latency_harness_digest_equals_reference_run_bench(ref, mode):
         pool = ref.syndrome_pool(rc, 0.02, 1, 256)
         cfg = DecoderConfig(max_iterations=iters, early_termination=early, arithmetic=mode)
         with Decoder(code, cfg) as dec:
-            for io_mode in (0, 1):
+            for io_mode in (0, 1, 2):
                 dec.set_option(1, io_mode)
                 wall, kern, digest = dec.latency_run(pool, 100, 200)
                 assert digest == r["digest"]

@@ -287,7 +287,7 @@ def test_large_batch_soundness_properties():
 
 OPT_KERNEL, OPT_LATENCY_IO, OPT_LATENCY_SHAPE, OPT_GROUP_THREADS = 0, 1, 2, 3
 OPT_BATCH_CTAS, OPT_BATCH_NPT, OPT_LATENCY_NPT, OPT_FAST_PATH, OPT_BATCH_SHAPE = 4, 5, 6, 7, 8
-INFO_BATCH_REGULAR, INFO_LATENCY_CLUSTER = 104, 103
+INFO_BATCH_REGULAR, INFO_LATENCY_CLUSTER, INFO_LATENCY_LEAN = 104, 103, 106
 
 
 @pytest.mark.parametrize("mode", REF_MODES)
@@ -309,11 +309,21 @@ def test_regular_and_cluster_kernels_match_oracle(oracle, name, mode):
                 dec.set_option(OPT_LATENCY_SHAPE, shape)
                 assert dec.get_option(INFO_LATENCY_CLUSTER) == (1 if shape == 2 else 0)
                 for npt in (1, 2, 4):
-                    if name == "bb784" and shape == 1 and npt == 1 and False:
-                        continue
                     dec.set_option(OPT_LATENCY_NPT, npt)
                     assert_matches_oracle(oracle, g, cfg, syn[:6], code.segments, dec=dec,
                                           messages=True)
+            # lean cluster kernel: every way of delivering the syndrome, incl. the
+            # persistent doorbell (no launch per shot)
+            dec.set_option(OPT_LATENCY_SHAPE, 0)
+            dec.set_option(OPT_LATENCY_NPT, 0)
+            assert dec.get_option(INFO_LATENCY_LEAN) == 1
+            for io_mode in (0, 1, 2):
+                dec.set_option(OPT_LATENCY_IO, io_mode)
+                launches = dec.launch_count()
+                assert_matches_oracle(oracle, g, cfg, syn[:12], code.segments, dec=dec)
+                if io_mode == 2:
+                    assert dec.launch_count() - launches <= 2, "doorbell mode must not launch per shot"
+            dec.set_option(OPT_LATENCY_IO, 0)
             for bshape in (1, 2):  # CTA per shot / CTA per (shot, segment) work item
                 dec.set_option(OPT_BATCH_SHAPE, bshape)
                 assert dec.get_option(OPT_BATCH_SHAPE) == bshape
