@@ -447,31 +447,35 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
 
 // =============================================================================
 // Single-shot latency kernel: one thread-block CLUSTER per shot, CTA rank s
-// decodes segment s on its own SM (segments are independent graphs, so the
-// iteration loop needs no cross-CTA traffic).  DSMEM carries the control plane
-// and the result merge: the leader (rank 0) obtains the syndrome, drops each
-// rank's packed words and a "go" word into that rank's mailbox, every rank
-// decodes its segment with the lean item loop above, then deposits its
-// segment-local estimate / residual words and (converged, iterations) in the
-// leader's shared memory; after ONE cluster barrier the leader shifts the
-// pieces into the reference's packed layout, writes them to (mapped host)
-// memory, fences and raises the completion word.
+// decodes segment s on its own SM with the lean item loop above (segments are
+// independent graphs, so the iteration loop needs no cross-CTA traffic).
 //
-// Three ways to obtain the syndrome (LatencyCtl::mode):
-//   0  passed BY VALUE in the kernel parameters (no load at all on the device);
+// Getting the syndrome in (LatencyCtl::mode):
+//   0  passed BY VALUE in the kernel parameters - no load at all on the device;
 //   1  read from io.syn (device memory after an explicit H2D copy - the paper's
 //      protocol - or mapped host memory);
-//   2  PERSISTENT: the cluster stays resident and polls a doorbell block in
-//      mapped host memory; each 32-byte sector of the block carries the
-//      sequence number in its first word, so one 128-byte read that shows the
+//   2  PERSISTENT: the cluster stays resident and every CTA polls a 128-byte
+//      doorbell block in mapped host memory.  Each 32-byte sector of the block
+//      carries the sequence number in its first word, so ONE read that shows the
 //      expected number in all four sectors already holds a consistent syndrome
-//      (host: data words first, sequence words last).  Removes the kernel launch
-//      from the critical path; the kernel retires by itself after idle_ns.
+//      (host: data words first, sequence words last).  No kernel launch on the
+//      critical path; the leader retires the cluster after idle_ns without work
+//      by raising an exit word in every peer's shared memory over DSMEM.
+//
+// Getting the result out: every CTA writes a SECTORED RECORD for its segment
+// straight to (mapped host) memory - 32-byte sectors [seq | 7 data words], each
+// written by eight adjacent lanes of one store instruction - holding the
+// segment-local estimate and residual words, (converged, iterations) and the
+// device time.  The host accepts a record when all of its sectors show the
+// shot's sequence number, so the kernel needs no system-scope fence, no cluster
+// barrier and no merge pass after the last iteration; shifting the two
+// segment-local pieces into the reference's packed layout costs the host a few
+// dozen word operations.
 // =============================================================================
 
 constexpr uint32_t kInlineSynWords = 64;
 constexpr uint32_t kDoorbellWords = 32;         // one 128-byte block
-constexpr uint32_t kDoorbellDataPerSector = 7;  // words 1..7 of each 8-word sector
+constexpr uint32_t kSectorData = 7;             // data words per 8-word sector
 constexpr uint32_t kDoorbellExit = 0xffffffffu;
 
 struct SynInline {
@@ -479,11 +483,13 @@ struct SynInline {
 };
 
 struct LatencyCtl {
-  uint32_t mode;                    // 0 inline, 1 pointer, 2 persistent doorbell
-  uint32_t first_seq;               // sequence number of the first shot served
+  uint32_t mode;                      // 0 inline, 1 pointer, 2 persistent doorbell
+  uint32_t first_seq;                 // sequence number of the first shot served
   const volatile uint32_t* doorbell;  // mode 2: mapped host memory, kDoorbellWords words
-  volatile uint32_t* alive;         // mode 2: set to 0 (after a system fence) when the kernel retires
-  uint64_t idle_ns;                 // mode 2: retire after this long without a doorbell
+  volatile uint32_t* alive;           // mode 2: cleared when the cluster retires
+  uint64_t idle_ns;                   // mode 2: retire after this long without a doorbell
+  uint32_t* rec;                      // result records, rec_stride words per segment
+  uint32_t rec_stride;
 };
 
 __device__ __forceinline__ uint32_t ld_volatile_global(const volatile uint32_t* p) {
@@ -492,15 +498,19 @@ __device__ __forceinline__ uint32_t ld_volatile_global(const volatile uint32_t* 
   return v;
 }
 
-// position of packed syndrome word `idx` inside the doorbell block
-__host__ __device__ inline uint32_t doorbell_pos(uint32_t idx) {
-  return 8u * (idx / kDoorbellDataPerSector) + 1u + idx % kDoorbellDataPerSector;
+// position of data word `idx` inside a sectored block / record
+__host__ __device__ inline uint32_t sector_pos(uint32_t idx) {
+  return 8u * (idx / kSectorData) + 1u + idx % kSectorData;
 }
-
-struct LatMailbox {
-  uint32_t go;       // sequence number of the shot to decode (kDoorbellExit = retire)
-  uint32_t raw[32];  // this rank's packed syndrome words (global word gw0 + i)
-};
+// words of a sectored record holding `n` data words
+__host__ __device__ inline uint32_t sector_words(uint32_t n) {
+  return 8u * ((n + kSectorData - 1) / kSectorData);
+}
+// data words of one segment's record: estimate words, residual words, converged,
+// iterations, device ns (lo, hi)
+__host__ __device__ inline uint32_t record_data_words(uint32_t nvars, uint32_t nchecks) {
+  return ((nvars + 31u) >> 5) + ((nchecks + 31u) >> 5) + 4u;
+}
 
 template <class A, int CPT, int VPT, bool kFast>
 __global__ void __launch_bounds__(1024, 1)
@@ -518,23 +528,20 @@ decode_lean_latency_kernel(const __grid_constant__ DecodeParams P,
   const uint32_t s = cluster.block_rank();  // == segment
   const SegmentDev seg = P.segs[s];
   const uint32_t Ms = seg.c1 - seg.c0, Ns = seg.v1 - seg.v0;
-  const uint32_t pw = lean_pw(P.seg_mmax);       // words of a local check bitmap
-  const uint32_t ew = lean_pw(P.seg_nmax);       // words of a local variable bitmap
-  const uint32_t pws = (Ms + 31u) >> 5;
+  const uint32_t pw = lean_pw(P.seg_mmax);  // words of a local check bitmap
+  const uint32_t ew = lean_pw(P.seg_nmax);  // words of a local variable bitmap
+  const uint32_t pws = (Ms + 31u) >> 5, ews = (Ns + 31u) >> 5;
   const uint32_t gw0 = seg.c0 >> 5, gspan = ((seg.c1 - 1) >> 5) - gw0 + 1, cshift = seg.c0 & 31u;
 
-  // ---- shared memory: messages | par | ehat | unsat | mailbox | (leader) result area + out
+  // ---- shared memory: messages | par | ehat | unsat | exit word
   unsigned char* const msgs = smem_raw;
   const size_t msg_bytes = (static_cast<size_t>(P.seg_mmax + 1) * kStride + 15) & ~size_t(15);
   uint32_t* const bits = reinterpret_cast<uint32_t*>(smem_raw + msg_bytes);
   uint32_t* const par = bits;                       // [pw]
   uint32_t* const ehat = bits + pw;                 // [ew]
-  volatile uint32_t* const unsat = bits + pw + ew;  // [1] (+1 pad)
-  LatMailbox* const mbox = reinterpret_cast<LatMailbox*>(bits + pw + ew + 2);
-  uint32_t* const area = bits + pw + ew + 2 + 34;   // leader: [nseg][pw + ew + 2]
-  const uint32_t area_stride = pw + ew + 2;
-  uint32_t* const out_est = area + kMaxSegments * area_stride;  // leader: [est_w32]
-  uint32_t* const out_res = out_est + P.est_w32;                // leader: [syn_w32]
+  volatile uint32_t* const unsat = bits + pw + ew;  // [1]
+  volatile uint32_t* const exit_word = bits + pw + ew + 1;
+  uint32_t* const cmd_word = bits + pw + ew + 2;
 
   // ---- per-thread tables
   uint32_t eo[VPT][kDV], co[CPT], cl[CPT], valid = 0;
@@ -563,68 +570,54 @@ decode_lean_latency_kernel(const __grid_constant__ DecodeParams P,
     }
   }
   for (uint32_t b = tid; b < kStride; b += T) msgs[P.seg_mmax * kStride + b] = 0;
-  if (tid == 0) mbox->go = ctl.first_seq - 1u;
+  if (tid == 0) *exit_word = 0u;
   __syncthreads();
-  cluster.sync();  // every mailbox is initialised before the leader may write into it
+  if (ctl.mode == 2u) cluster.sync();  // exit words exist before the leader may raise them
 
+  uint32_t* const rec = ctl.rec + s * ctl.rec_stride;
+  const uint32_t ndata = ews + pws + 4u;
+  const uint32_t nrec = sector_words(ndata);
   uint32_t last = ctl.first_seq - 1u;
   uint64_t t_idle0 = globaltimer_ns();
   for (;;) {
-    // ---------------- obtain the shot (leader) and hand it out ----------------
+    // ---------------- obtain the shot: warp 0 ends up with packed word gw0 + lane -------
+    uint32_t cmd = last + 1u;
+    uint32_t raw = 0;
     uint64_t t_begin = 0;
-    if (s == 0 && warp == 0) {
-      uint32_t cmd = last + 1u;
-      uint32_t val = 0;  // mode 2: doorbell word `lane`
+    if (warp == 0) {
       if (ctl.mode == 2u) {
-        uint32_t spins = 0;
+        uint32_t spins = 0, val = 0;
         for (;;) {
           val = ld_volatile_global(ctl.doorbell + lane);
           const uint32_t sq = __shfl_sync(0xffffffffu, val, lane & ~7u);  // my sector's number
           if (__all_sync(0xffffffffu, sq == cmd)) break;
-          if (__any_sync(0xffffffffu, sq == kDoorbellExit)) {
+          if (__any_sync(0xffffffffu, sq == kDoorbellExit) || *exit_word != 0u) {
             cmd = kDoorbellExit;
             break;
           }
-          if ((++spins & 63u) == 0u && globaltimer_ns() - t_idle0 > ctl.idle_ns) {
+          if (s == 0 && (++spins & 63u) == 0u && globaltimer_ns() - t_idle0 > ctl.idle_ns) {
+            // leader: retire the whole cluster
+            if (lane < nseg) *cluster.map_shared_rank(const_cast<uint32_t*>(exit_word), lane) = 1u;
             cmd = kDoorbellExit;
             break;
           }
         }
+        const uint32_t src = lane < gspan ? sector_pos(gw0 + lane) : 0u;
+        raw = __shfl_sync(0xffffffffu, val, src & 31u);
+      } else if (lane < gspan) {
+        raw = ctl.mode == 0u ? syn_in.w[gw0 + lane] : io.syn[gw0 + lane];
       }
+      if (lane >= gspan) raw = 0;
       t_begin = globaltimer_ns();
-      for (uint32_t r = 0; r < nseg; ++r) {
-        const SegmentDev sr = P.segs[r];
-        const uint32_t g0 = sr.c0 >> 5, span = ((sr.c1 - 1) >> 5) - g0 + 1;
-        uint32_t word = 0;
-        if (ctl.mode == 2u) {
-          const uint32_t src = lane < span ? doorbell_pos(g0 + lane) : 0u;
-          word = __shfl_sync(0xffffffffu, val, src & 31u);
-        } else if (lane < span) {
-          word = ctl.mode == 0u ? syn_in.w[g0 + lane] : io.syn[g0 + lane];
-        }
-        if (lane >= span) word = 0;
-        LatMailbox* mb = cluster.map_shared_rank(mbox, r);
-        mb->raw[lane] = word;
-      }
-      __threadfence();  // order the words before the go flags (cluster scope included)
-      if (lane < nseg) {
-        LatMailbox* mb = cluster.map_shared_rank(mbox, lane);
-        *reinterpret_cast<volatile uint32_t*>(&mb->go) = cmd;
+      if (lane == 0) {
+        cmd_word[0] = cmd;
+        cmd_word[1] = static_cast<uint32_t>(t_begin);
+        cmd_word[2] = static_cast<uint32_t>(t_begin >> 32);
       }
     }
-    // ---------------- wait for the go word ----------------
-    if (warp == 0) {
-      while (*reinterpret_cast<volatile uint32_t*>(&mbox->go) == last) {
-      }
-      __threadfence();
-    }
-    __syncthreads();
-    const uint32_t cmd = *reinterpret_cast<volatile uint32_t*>(&mbox->go);
-    if (cmd == kDoorbellExit) break;
 
     // ---------------- prologue ----------------
     if (warp == 0) {
-      const uint32_t raw = mbox->raw[lane];
       uint32_t nb = __shfl_down_sync(0xffffffffu, raw, 1);
       if (lane + 1 >= gspan) nb = 0;
       uint32_t loc = cshift ? __funnelshift_r(raw, nb, cshift) : raw;
@@ -652,6 +645,9 @@ decode_lean_latency_kernel(const __grid_constant__ DecodeParams P,
     }
     uint32_t eprev = 0;
     __syncthreads();
+    cmd = cmd_word[0];
+    if (cmd == kDoorbellExit) break;
+    t_begin = static_cast<uint64_t>(cmd_word[1]) | (static_cast<uint64_t>(cmd_word[2]) << 32);
     uint32_t synbits = 0;
 #pragma unroll
     for (int k = 0; k < CPT; ++k) synbits |= ((par[cl[k] >> 5] >> (cl[k] & 31u)) & 1u) << k;
@@ -695,7 +691,7 @@ decode_lean_latency_kernel(const __grid_constant__ DecodeParams P,
       if ((P.early && !still_unsat) || iter >= P.max_iter) break;
     }
 
-    // ---------------- deposit this segment's result with the leader ----------------
+    // ---------------- publish this segment's record ----------------
     if (eprev) {
 #pragma unroll
       for (int k = 0; k < VPT; ++k) {
@@ -722,79 +718,48 @@ decode_lean_latency_kernel(const __grid_constant__ DecodeParams P,
     }
     __syncthreads();
     {
-      uint32_t* dst = cluster.map_shared_rank(area, 0) + s * area_stride;
-      for (uint32_t w = tid; w < pw; w += T) dst[w] = par[w];
-      for (uint32_t w = tid; w < ew; w += T) dst[pw + w] = ehat[w];
-      if (tid == 0) {
-        dst[pw + ew] = still_unsat ? 0u : 1u;
-        dst[pw + ew + 1] = iter;
-      }
-    }
-    cluster.sync();
-
-    // ---------------- leader: merge into the packed layout and publish ----------------
-    if (s == 0) {
-      for (uint32_t w = tid; w < P.est_w32; w += T) out_est[w] = 0;
-      for (uint32_t w = tid; w < P.syn_w32; w += T) out_res[w] = 0;
-      __syncthreads();
-      // one warp per segment: local word w of segment r lands at global bit b0 + 32 w
-      for (uint32_t r = warp; r < nseg; r += (T >> 5)) {
-        const SegmentDev sr = P.segs[r];
-        const uint32_t* src = area + r * area_stride;
-        const uint32_t mr = sr.c1 - sr.c0, nr = sr.v1 - sr.v0;
-        for (uint32_t w = lane; w < ((mr + 31u) >> 5); w += 32u) {
-          const uint32_t v = src[w], b0 = sr.c0 + 32u * w, sh = b0 & 31u;
-          if (v) {
-            atomicOr(&out_res[b0 >> 5], v << sh);
-            if (sh && (v >> (32u - sh))) atomicOr(&out_res[(b0 >> 5) + 1], v >> (32u - sh));
+      const uint64_t ns = globaltimer_ns() - t_begin;
+      for (uint32_t w = tid; w < nrec; w += T) {
+        const uint32_t slot = w & 7u;
+        uint32_t v = cmd;
+        if (slot) {
+          const uint32_t d = (w >> 3) * kSectorData + slot - 1u;
+          if (d < ews) {
+            v = ehat[d];
+          } else if (d < ews + pws) {
+            v = par[d - ews];
+          } else if (d == ews + pws) {
+            v = still_unsat ? 0u : 1u;
+          } else if (d == ews + pws + 1u) {
+            v = iter;
+          } else if (d == ews + pws + 2u) {
+            v = static_cast<uint32_t>(ns);
+          } else if (d == ews + pws + 3u) {
+            v = static_cast<uint32_t>(ns >> 32);
+          } else {
+            v = 0u;
           }
         }
-        for (uint32_t w = lane; w < ((nr + 31u) >> 5); w += 32u) {
-          const uint32_t v = src[pw + w], b0 = sr.v0 + 32u * w, sh = b0 & 31u;
-          if (v) {
-            atomicOr(&out_est[b0 >> 5], v << sh);
-            if (sh && (v >> (32u - sh))) atomicOr(&out_est[(b0 >> 5) + 1], v >> (32u - sh));
-          }
-        }
+        rec[w] = v;
       }
-      __syncthreads();
-      for (uint32_t w = tid; w < P.est_w32; w += T) io.est[w] = out_est[w];
-      if (io.resid) {
-        for (uint32_t w = tid; w < P.syn_w32; w += T) io.resid[w] = out_res[w];
-      }
-      if (tid < nseg) {
-        io.conv[tid] = static_cast<uint8_t>(area[tid * area_stride + pw + ew]);
-        io.iters[tid] = area[tid * area_stride + pw + ew + 1];
-      }
-      if (io.flag) {
-        __threadfence_system();
-        __syncthreads();
-        if (tid == 0) {
-          // warp 0 lane 0 took t_begin; it is thread 0
-          *io.kernel_ns = globaltimer_ns() - t_begin;
-          __threadfence_system();
-          *io.flag = cmd;
-        }
-      }
-      t_idle0 = globaltimer_ns();
     }
+    t_idle0 = globaltimer_ns();
     last = cmd;
     if (ctl.mode != 2u) break;
   }
-  if (ctl.mode == 2u && s == 0 && tid == 0 && ctl.alive) {
-    *ctl.alive = 0u;
-    __threadfence_system();
+  if (ctl.mode == 2u) {
+    if (s == 0 && tid == 0 && ctl.alive) {
+      *ctl.alive = 0u;
+      __threadfence_system();
+    }
+    cluster.sync();  // no CTA leaves while the leader may still raise its exit word
   }
-  cluster.sync();  // no CTA leaves while a peer may still address its shared memory
 }
 
 __host__ __device__ inline size_t lean_latency_smem_bytes(uint32_t seg_mmax, uint32_t seg_nmax,
-                                                          uint32_t syn_w32, uint32_t est_w32,
                                                           int arith) {
   const size_t msg = (static_cast<size_t>(seg_mmax + 1) * lean_stride(arith) + 15) & ~size_t(15);
-  const size_t pw = lean_pw(seg_mmax), ew = lean_pw(seg_nmax);
-  const size_t words = pw + ew + 2 + 34 + kMaxSegments * (pw + ew + 2) + est_w32 + syn_w32 + 8;
-  return msg + 4 * words;
+  return msg + 4 * (static_cast<size_t>(lean_pw(seg_mmax)) + lean_pw(seg_nmax) + 8);
 }
 
 }  // namespace qb

@@ -135,6 +135,10 @@ struct qb_decoder {
   size_t lat_lean_smem = 0;
   uint32_t* h_db = nullptr;   // mapped: doorbell block [32] + alive word [32]
   uint32_t* d_db = nullptr;
+  uint32_t* h_rec = nullptr;  // mapped: sectored result records, rec_stride words per segment
+  uint32_t* d_rec_map = nullptr;
+  uint32_t* d_rec_dev = nullptr;
+  uint32_t rec_stride = 0;
   bool db_running = false;
   int64_t opt_idle_ms = 200;
   bool regular63 = false;  // every check degree 6, every variable degree 3
@@ -178,6 +182,8 @@ void destroy(qb_decoder* h) {
   cudaFree(h->d_rdump);
   cudaFree(h->d_probs);
   if (h->h_db) cudaFreeHost(h->h_db);
+  if (h->h_rec) cudaFreeHost(h->h_rec);
+  cudaFree(h->d_rec_dev);
   if (h->h_in) cudaFreeHost(h->h_in);
   if (h->h_out) cudaFreeHost(h->h_out);
   free_batch(h);
@@ -448,7 +454,7 @@ void make_plans(qb_decoder* h) {
       h->lat_lean_kernel =
           lean_latency_kernel(h->arith, npt, h->fast_ok && h->opt_fast != 0);
       h->lat_lean_block = T;
-      h->lat_lean_smem = lean_latency_smem_bytes(P.seg_mmax, P.seg_nmax, P.syn_w32, P.est_w32,
+      h->lat_lean_smem = lean_latency_smem_bytes(P.seg_mmax, P.seg_nmax,
                                                  h->arith == QB_ARITH_HALF ? 3 : h->arith);
       CUDA_TRY(cudaFuncSetAttribute(h->lat_lean_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -612,17 +618,17 @@ void stop_doorbell(qb_decoder* h) {
   h->db_running = false;
 }
 
-void spin_for_flag(qb_decoder* h, volatile uint32_t* h_flag, uint32_t seq, bool persistent) {
-  // Spin on the completion word the kernel writes last; no stream sync on the
-  // fast path.  A watchdog falls back to the runtime for diagnosis.
+// Waits until `ready()` holds, with a watchdog that falls back to the runtime.
+template <typename Ready>
+void spin_until(qb_decoder* h, Ready&& ready, bool persistent) {
   const auto t0 = std::chrono::steady_clock::now();
   uint64_t spins = 0;
-  while (*h_flag != seq) {
+  while (!ready()) {
     if ((++spins & 0xffff) == 0) {
       const cudaError_t q = cudaStreamQuery(h->stream);
       if (q != cudaErrorNotReady) {
         CUDA_TRY(cudaStreamSynchronize(h->stream));
-        if (*h_flag == seq) break;
+        if (ready()) break;
         if (persistent) {
           h->db_running = false;  // retired while we were ringing: caller relaunches
           fail(QB_RUNTIME_ERROR, "doorbell kernel retired");
@@ -636,6 +642,55 @@ void spin_for_flag(qb_decoder* h, volatile uint32_t* h_flag, uint32_t seq, bool 
   }
 }
 
+// True when every sector of every segment's record carries `seq`.
+bool records_ready(const qb_decoder* h, uint32_t seq) {
+  const DecodeParams& P = h->P;
+  const volatile uint32_t* rec = h->h_rec;
+  for (uint32_t s = P.nseg; s-- > 0;) {
+    const uint32_t nd = record_data_words(P.segs[s].v1 - P.segs[s].v0, P.segs[s].c1 - P.segs[s].c0);
+    for (uint32_t k = sector_words(nd) / 8; k-- > 0;) {
+      if (rec[s * h->rec_stride + 8 * k] != seq) return false;
+    }
+  }
+  return true;
+}
+
+// OR `words` local words (bit 0 = global bit `bit0`) into a packed vector.
+void or_shifted(uint32_t* dst, uint32_t dst_words, const uint32_t* rec, uint32_t first_data,
+                uint32_t words, uint32_t bit0) {
+  for (uint32_t w = 0; w < words; ++w) {
+    const uint32_t v = rec[sector_pos(first_data + w)];
+    if (!v) continue;
+    const uint32_t b = bit0 + 32u * w, sh = b & 31u, i = b >> 5;
+    dst[i] |= v << sh;
+    if (sh && i + 1 < dst_words) dst[i + 1] |= v >> (32u - sh);
+  }
+}
+
+// Sectored per-segment records -> the reference's packed layout.
+void unpack_records(qb_decoder* h, uint64_t* estimate, uint64_t* residual, uint8_t* converged,
+                    uint32_t* iterations) {
+  const DecodeParams& P = h->P;
+  uint32_t* est = reinterpret_cast<uint32_t*>(estimate);
+  uint32_t* res = reinterpret_cast<uint32_t*>(residual);
+  std::memset(est, 0, P.est_w32 * 4);
+  if (res) std::memset(res, 0, P.syn_w32 * 4);
+  uint64_t ns_max = 0;
+  for (uint32_t s = 0; s < P.nseg; ++s) {
+    const uint32_t* rec = h->h_rec + s * h->rec_stride;
+    const uint32_t nv = P.segs[s].v1 - P.segs[s].v0, nc = P.segs[s].c1 - P.segs[s].c0;
+    const uint32_t ews = (nv + 31u) >> 5, pws = (nc + 31u) >> 5;
+    or_shifted(est, P.est_w32, rec, 0, ews, P.segs[s].v0);
+    if (res) or_shifted(res, P.syn_w32, rec, ews, pws, P.segs[s].c0);
+    converged[s] = static_cast<uint8_t>(rec[sector_pos(ews + pws)]);
+    iterations[s] = rec[sector_pos(ews + pws + 1)];
+    const uint64_t ns = static_cast<uint64_t>(rec[sector_pos(ews + pws + 2)]) |
+                        (static_cast<uint64_t>(rec[sector_pos(ews + pws + 3)]) << 32);
+    ns_max = std::max(ns_max, ns);
+  }
+  h->last_kernel_ns = ns_max;
+}
+
 void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, uint64_t* residual,
                  uint8_t* converged, uint32_t* iterations, bool debug) {
   const DecodeParams& P = h->P;
@@ -646,8 +701,8 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
   const bool lean = h->lat_lean_kernel != nullptr;
   const bool doorbell = io_mode == 2 && lean && !debug && P.syn_w32 <= 28;
   if (!doorbell) stop_doorbell(h);
-  const uint32_t seq = ++h->seq;
-  if (seq == kDoorbellExit) h->seq = 0;
+  uint32_t seq = ++h->seq;
+  if (seq == kDoorbellExit || seq == 0) seq = h->seq = 1;
   ShotIO io{};
   io.nshots = 1;
   io.sched = h->d_sched;
@@ -656,56 +711,47 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
     io.q_dump = h->d_qdump;
     io.r_dump = h->d_rdump;
   }
-  volatile uint32_t* h_flag = reinterpret_cast<volatile uint32_t*>(h->h_out + h->off_flag);
   const bool mapped = io_mode != 1;
-  unsigned char* out = mapped ? h->d_out_map : h->d_out_dev;
-  io.est = reinterpret_cast<uint32_t*>(out);
-  io.resid = reinterpret_cast<uint32_t*>(out + h->off_res);
-  io.conv = out + h->off_conv;
-  io.iters = reinterpret_cast<uint32_t*>(out + h->off_iters);
-  io.kernel_ns = reinterpret_cast<uint64_t*>(out + h->off_ns);
-  io.flag = reinterpret_cast<volatile uint32_t*>(out + h->off_flag);
 
-  if (doorbell) {
-    // ---- persistent cluster: ring the doorbell, spin on the completion word
-    volatile uint32_t* db = h->h_db;
-    volatile uint32_t* alive = h->h_db + 32;
-    const uint32_t* syn32 = reinterpret_cast<const uint32_t*>(syndrome);
-    for (int attempt = 0;; ++attempt) {
-      if (!h->db_running || *alive == 0u) {
-        if (h->db_running) CUDA_TRY(cudaStreamSynchronize(h->stream));
-        for (int k = 0; k < 32; ++k) db[k] = 0;
-        *alive = 1u;
-        std::atomic_thread_fence(std::memory_order_seq_cst);
-        LatencyCtl ctl{};
-        ctl.mode = 2;
-        ctl.first_seq = seq;
-        ctl.doorbell = h->d_db;
-        ctl.alive = h->d_db + 32;
-        ctl.idle_ns = static_cast<uint64_t>(h->opt_idle_ms) * 1000000ull;
-        SynInline none{};
-        launch_lean_latency(h, io, ctl, none);
-        h->db_running = true;
-      }
-      for (uint32_t i = 0; i < P.syn_w32; ++i) db[doorbell_pos(i)] = syn32[i];
-      std::atomic_thread_fence(std::memory_order_release);
-      for (int k = 0; k < 4; ++k) db[8 * k] = seq;
-      try {
-        spin_for_flag(h, h_flag, seq, true);
-        break;
-      } catch (const StatusError&) {
-        if (h->db_running || attempt >= 2) throw;  // a real failure, or retiring repeatedly
-      }
-    }
-  } else if (lean) {
+  if (lean) {
     LatencyCtl ctl{};
     ctl.first_seq = seq;
+    ctl.rec = mapped ? h->d_rec_map : h->d_rec_dev;
+    ctl.rec_stride = h->rec_stride;
     SynInline syn{};
-    if (mapped) {
+    if (doorbell) {
+      // ---- persistent cluster: ring the doorbell, wait for the records
+      volatile uint32_t* db = h->h_db;
+      volatile uint32_t* alive = h->h_db + 32;
+      const uint32_t* syn32 = reinterpret_cast<const uint32_t*>(syndrome);
+      for (int attempt = 0;; ++attempt) {
+        if (!h->db_running || *alive == 0u) {
+          if (h->db_running) CUDA_TRY(cudaStreamSynchronize(h->stream));
+          for (int k = 0; k < 32; ++k) db[k] = 0;
+          *alive = 1u;
+          std::atomic_thread_fence(std::memory_order_seq_cst);
+          ctl.mode = 2;
+          ctl.doorbell = h->d_db;
+          ctl.alive = h->d_db + 32;
+          ctl.idle_ns = static_cast<uint64_t>(h->opt_idle_ms) * 1000000ull;
+          launch_lean_latency(h, io, ctl, syn);
+          h->db_running = true;
+        }
+        for (uint32_t i = 0; i < P.syn_w32; ++i) db[sector_pos(i)] = syn32[i];
+        std::atomic_thread_fence(std::memory_order_release);
+        for (int k = 0; k < 4; ++k) db[8 * k] = seq;
+        try {
+          spin_until(h, [&] { return records_ready(h, seq); }, true);
+          break;
+        } catch (const StatusError&) {
+          if (h->db_running || attempt >= 2) throw;  // a real failure, or retiring repeatedly
+        }
+      }
+    } else if (mapped) {
       ctl.mode = 0;  // syndrome travels in the kernel parameters
       std::memcpy(syn.w, syndrome, P.syn_w32 * 4);
       launch_lean_latency(h, io, ctl, syn);
-      spin_for_flag(h, h_flag, seq, false);
+      spin_until(h, [&] { return records_ready(h, seq); }, false);
     } else {
       ctl.mode = 1;  // the paper's protocol: H2D copy, kernel, D2H copy, synchronize
       std::memcpy(h->h_in, syndrome, P.syn_w32 * 4);
@@ -713,24 +759,37 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
       CUDA_TRY(cudaMemcpyAsync(h->d_in_dev, h->h_in, P.syn_w32 * 4, cudaMemcpyHostToDevice,
                                h->stream));
       launch_lean_latency(h, io, ctl, syn);
-      CUDA_TRY(cudaMemcpyAsync(h->h_out, h->d_out_dev, h->out_bytes, cudaMemcpyDeviceToHost,
-                               h->stream));
+      CUDA_TRY(cudaMemcpyAsync(h->h_rec, h->d_rec_dev,
+                               static_cast<size_t>(h->rec_stride) * P.nseg * 4,
+                               cudaMemcpyDeviceToHost, h->stream));
       CUDA_TRY(cudaStreamSynchronize(h->stream));
+      if (!records_ready(h, seq)) fail(QB_RUNTIME_ERROR, "decode kernel produced no record");
     }
+    unpack_records(h, estimate, residual, converged, iterations);
+    return;
+  }
+
+  // ---- graphs the lean kernel does not cover: generic / regular kernels
+  volatile uint32_t* h_flag = reinterpret_cast<volatile uint32_t*>(h->h_out + h->off_flag);
+  unsigned char* out = mapped ? h->d_out_map : h->d_out_dev;
+  io.est = reinterpret_cast<uint32_t*>(out);
+  io.resid = reinterpret_cast<uint32_t*>(out + h->off_res);
+  io.conv = out + h->off_conv;
+  io.iters = reinterpret_cast<uint32_t*>(out + h->off_iters);
+  io.kernel_ns = reinterpret_cast<uint64_t*>(out + h->off_ns);
+  io.flag = reinterpret_cast<volatile uint32_t*>(out + h->off_flag);
+  std::memcpy(h->h_in, syndrome, P.syn_w32 * 4);
+  io.syn = mapped ? h->d_in_map : h->d_in_dev;
+  if (mapped) {
+    launch_plan(h, h->lat, io, h->lat.cluster ? h->P.nseg : 1, h->stream);
+    spin_until(h, [&] { return *h_flag == seq; }, false);
   } else {
-    std::memcpy(h->h_in, syndrome, P.syn_w32 * 4);
-    io.syn = mapped ? h->d_in_map : h->d_in_dev;
-    if (mapped) {
-      launch_plan(h, h->lat, io, h->lat.cluster ? h->P.nseg : 1, h->stream);
-      spin_for_flag(h, h_flag, seq, false);
-    } else {
-      CUDA_TRY(cudaMemcpyAsync(h->d_in_dev, h->h_in, P.syn_w32 * 4, cudaMemcpyHostToDevice,
-                               h->stream));
-      launch_plan(h, h->lat, io, h->lat.cluster ? h->P.nseg : 1, h->stream);
-      CUDA_TRY(cudaMemcpyAsync(h->h_out, h->d_out_dev, h->out_bytes, cudaMemcpyDeviceToHost,
-                               h->stream));
-      CUDA_TRY(cudaStreamSynchronize(h->stream));
-    }
+    CUDA_TRY(cudaMemcpyAsync(h->d_in_dev, h->h_in, P.syn_w32 * 4, cudaMemcpyHostToDevice,
+                             h->stream));
+    launch_plan(h, h->lat, io, h->lat.cluster ? h->P.nseg : 1, h->stream);
+    CUDA_TRY(cudaMemcpyAsync(h->h_out, h->d_out_dev, h->out_bytes, cudaMemcpyDeviceToHost,
+                             h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
   }
   std::memcpy(estimate, h->h_out, P.est_w32 * 4);
   if (residual) std::memcpy(residual, h->h_out + h->off_res, P.syn_w32 * 4);
@@ -1051,6 +1110,13 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
     CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h->h_db), 64 * 4, cudaHostAllocMapped));
     std::memset(h->h_db, 0, 64 * 4);
     CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_db), h->h_db, 0));
+    h->rec_stride = sector_words(record_data_words(P.seg_nmax, P.seg_mmax));
+    const size_t rec_bytes = static_cast<size_t>(h->rec_stride) * P.nseg * 4;
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h->h_rec), rec_bytes, cudaHostAllocMapped));
+    std::memset(h->h_rec, 0, rec_bytes);
+    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_rec_map), h->h_rec, 0));
+    CUDA_TRY(cudaMalloc(&h->d_rec_dev, rec_bytes));
+    CUDA_TRY(cudaMemset(h->d_rec_dev, 0, rec_bytes));
     CUDA_TRY(cudaMalloc(&h->d_in_dev, P.syn_w32 * 4));
     CUDA_TRY(cudaMalloc(&h->d_out_dev, h->out_bytes));
     CUDA_TRY(cudaMemset(h->d_out_dev, 0, h->out_bytes));
@@ -1152,6 +1218,7 @@ uint32_t qb_num_vars(const qb_decoder* h) { return h ? h->P.N : 0; }
 uint32_t qb_num_segments(const qb_decoder* h) { return h ? h->P.nseg : 0; }
 uint64_t qb_last_kernel_ns(const qb_decoder* h) { return h ? h->last_kernel_ns : 0; }
 uint64_t qb_launch_count(const qb_decoder* h) { return h ? h->launches : 0; }
+
 
 qb_status qb_decode(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate,
                     uint64_t* residual, uint8_t* converged, uint32_t* iterations) {
