@@ -222,6 +222,31 @@ qb_status qb_generate_syndromes(qb_decoder* h, uint64_t seed, double p,
                                 uint64_t* d_syndromes, uint64_t* d_errors,
                                 void* stream);
 
+/* Monte-Carlo campaign on the device (reference: run_campaign,
+ * proj/src/noise.cpp:217-338): sample -> syndrome -> decode -> classify, with
+ * nothing but ten counters crossing PCIe.
+ *
+ * qb_set_logicals supplies the residual tests for a two-segment (CSS) decoder:
+ * `x_tests` / `z_tests` are `n_x` / `n_z` packed vectors over ALL num_vars
+ * variables (combined layout, host memory); a converged X (Z) residual counts
+ * as a logical error iff it has odd overlap with at least one x_test (z_test).
+ * With the code's logical Z operators placed on the X-error variables as
+ * x_tests (and logical X operators on the Z-error variables as z_tests) this is
+ * exactly the reference's row-space membership test for zero-syndrome residuals.
+ *
+ * qb_campaign_run decodes trials [first_trial, first_trial + trials) of
+ * NoiseModel{independent-xz, p, seed} and ADDS to `counters` (host, 10 words):
+ *   [0] exact [1] stabilizer [2] logical_x [3] logical_z [4] logical_both
+ *   [5] non_converged [6] baseline failures (identity decoder) [7] trials with
+ *   both components converged [8] sum over trials of max(iterations_x,
+ *   iterations_z) [9] trials.
+ * Float / int8 / int16 results are identical to the reference's counts. */
+qb_status qb_set_logicals(qb_decoder* h, const uint64_t* x_tests, uint32_t n_x,
+                          const uint64_t* z_tests, uint32_t n_z);
+qb_status qb_campaign_run(qb_decoder* h, uint64_t seed, double p,
+                          const double* probs, uint64_t first_trial,
+                          uint64_t trials, uint64_t* counters);
+
 /* Pinned (page-locked, device-mapped) host memory for batch I/O. */
 qb_status qb_host_alloc(void** out, size_t bytes);
 void qb_host_free(void* p);

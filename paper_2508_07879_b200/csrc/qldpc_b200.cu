@@ -24,6 +24,7 @@
 #include "kernel_lean.cuh"
 #include "kernel_noise.cuh"
 #include "kernel_bw.cuh"
+#include "kernel_classify.cuh"
 
 using namespace qb;
 
@@ -125,6 +126,11 @@ struct qb_decoder {
   // debug dumps
   void *d_qdump = nullptr, *d_rdump = nullptr;
   double* d_probs = nullptr;  // per-variable flip probabilities of the noise generator
+  // campaign state
+  uint32_t *d_tests_x = nullptr, *d_tests_z = nullptr;
+  uint32_t n_tests_x = 0, n_tests_z = 0;
+  uint32_t* c_err = nullptr;  // [batch_cap][est_w32] sampled errors
+  unsigned long long* d_counters = nullptr;
 
   // options
   int64_t opt_kernel = 0, opt_latency_io = 0, opt_latency_shape = 0, opt_group_threads = 0,
@@ -160,6 +166,8 @@ void free_batch(qb_decoder* h) {
   cudaFree(h->b_res);
   cudaFree(h->b_iters);
   cudaFree(h->b_conv);
+  cudaFree(h->c_err);
+  h->c_err = nullptr;
   h->b_syn = h->b_est = h->b_res = h->b_iters = nullptr;
   h->b_conv = nullptr;
   h->batch_cap = 0;
@@ -181,6 +189,9 @@ void destroy(qb_decoder* h) {
   cudaFree(h->d_qdump);
   cudaFree(h->d_rdump);
   cudaFree(h->d_probs);
+  cudaFree(h->d_tests_x);
+  cudaFree(h->d_tests_z);
+  cudaFree(h->d_counters);
   if (h->h_db) cudaFreeHost(h->h_db);
   if (h->h_rec) cudaFreeHost(h->h_rec);
   cudaFree(h->d_rec_dev);
@@ -541,6 +552,7 @@ void ensure_batch(qb_decoder* h, uint64_t shots, bool want_resid) {
   CUDA_TRY(cudaMalloc(&h->b_res, cap * P.syn_w32 * 4));
   CUDA_TRY(cudaMalloc(&h->b_iters, cap * P.nseg * 4));
   CUDA_TRY(cudaMalloc(&h->b_conv, cap * P.nseg));
+  CUDA_TRY(cudaMalloc(&h->c_err, cap * P.est_w32 * 4));
   h->batch_cap = cap;
 }
 
@@ -1346,6 +1358,78 @@ qb_status qb_generate_syndromes(qb_decoder* h, uint64_t seed, double p, const do
     noise_syndrome_kernel<<<grid, kNoiseWarps * 32, smem, st>>>(P, np);
     CUDA_TRY(cudaGetLastError());
     ++h->launches;
+  });
+}
+
+qb_status qb_set_logicals(qb_decoder* h, const uint64_t* x_tests, uint32_t n_x,
+                          const uint64_t* z_tests, uint32_t n_z) {
+  if (!h) return QB_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    const DecodeParams& P = h->P;
+    if (P.nseg != 2) fail(QB_INVALID_ARGUMENT, "set_logicals: decoder was not built from a CssCode");
+    if ((n_x && !x_tests) || (n_z && !z_tests)) fail(QB_INVALID_ARGUMENT, "set_logicals: NULL tests");
+    auto upload = [&](const uint64_t* src, uint32_t n, uint32_t*& dst) {
+      cudaFree(dst);
+      dst = nullptr;
+      const size_t bytes = std::max<size_t>(static_cast<size_t>(n) * P.est_w32 * 4, 4);
+      CUDA_TRY(cudaMalloc(&dst, bytes));
+      if (n) CUDA_TRY(cudaMemcpy(dst, src, static_cast<size_t>(n) * P.est_w32 * 4, cudaMemcpyHostToDevice));
+    };
+    upload(x_tests, n_x, h->d_tests_x);
+    upload(z_tests, n_z, h->d_tests_z);
+    h->n_tests_x = n_x;
+    h->n_tests_z = n_z;
+  });
+}
+
+qb_status qb_campaign_run(qb_decoder* h, uint64_t seed, double p, const double* probs,
+                          uint64_t first_trial, uint64_t trials, uint64_t* counters) {
+  if (!h) return QB_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    const DecodeParams& P = h->P;
+    if (!counters) fail(QB_INVALID_ARGUMENT, "campaign_run: NULL counters");
+    if (P.nseg != 2 || !h->d_tests_x || !h->d_tests_z) {
+      fail(QB_INVALID_ARGUMENT, "campaign_run: call qb_set_logicals on a CssCode decoder first");
+    }
+    if (!(p >= 0.0 && p <= 1.0)) fail(QB_INVALID_ARGUMENT, "NoiseModel: p must lie in [0, 1]");
+    if (trials == 0) return;
+    if (!h->d_counters) CUDA_TRY(cudaMalloc(&h->d_counters, 10 * sizeof(unsigned long long)));
+    cudaStream_t st = h->stream;
+    CUDA_TRY(cudaMemsetAsync(h->d_counters, 0, 10 * sizeof(unsigned long long), st));
+    const uint64_t chunk = std::min<uint64_t>(trials, 1ull << 20);
+    ensure_batch(h, chunk, false);
+    for (uint64_t done = 0; done < trials; done += chunk) {
+      const uint64_t n = std::min<uint64_t>(chunk, trials - done);
+      // sample + syndrome (kernel_noise.cuh), decode (batch plan), classify
+      qb_status stc = qb_generate_syndromes(h, seed, p, probs, 1, first_trial + done, n,
+                                            reinterpret_cast<uint64_t*>(h->b_syn),
+                                            reinterpret_cast<uint64_t*>(h->c_err), st);
+      if (stc != QB_OK) fail(stc, h->err);
+      run_batch_device(h, n, h->b_syn, h->b_est, nullptr, h->b_conv, h->b_iters, st);
+      ClassifyParams cp{};
+      cp.nshots = n;
+      cp.err = h->c_err;
+      cp.est = h->b_est;
+      cp.syn = h->b_syn;
+      cp.conv = h->b_conv;
+      cp.iters = h->b_iters;
+      cp.tests_x = h->d_tests_x;
+      cp.tests_z = h->d_tests_z;
+      cp.n_x = h->n_tests_x;
+      cp.n_z = h->n_tests_z;
+      cp.counters = h->d_counters;
+      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(
+          (n + kClassifyWarps - 1) / kClassifyWarps, static_cast<uint64_t>(h->sm_count) * 8));
+      const size_t smem = static_cast<size_t>(kClassifyWarps) * 2 * P.est_w32 * 4;
+      classify_kernel<<<grid, kClassifyWarps * 32, smem, st>>>(P, cp);
+      CUDA_TRY(cudaGetLastError());
+      ++h->launches;
+    }
+    unsigned long long host_counters[10];
+    CUDA_TRY(cudaMemcpyAsync(host_counters, h->d_counters, sizeof(host_counters),
+                             cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (int k = 0; k < 10; ++k) counters[k] += host_counters[k];
   });
 }
 

@@ -1,0 +1,67 @@
+"""Device campaign (sample -> syndrome -> decode -> classify on the GPU) against
+the reference's run_campaign (proj/src/noise.cpp:217-338) through the prebuilt
+compiled reference: because the sampler and the decoder are bit-exact, every
+counter must be IDENTICAL, not merely statistically compatible."""
+import numpy as np
+import pytest
+
+from paper_2508_07879_b200 import DecoderConfig, codes
+from paper_2508_07879_b200.campaign import Campaign, CampaignResult, run_campaign, shard
+
+pytestmark = pytest.mark.gpu
+
+
+def _same(ours: CampaignResult, theirs: dict):
+    for key in ("trials", "exact", "stabilizer", "logical_x", "logical_z", "logical_both",
+                "non_converged"):
+        assert getattr(ours, key) == theirs[key], key
+    for key in ("logical_error_rate", "baseline_logical_rate", "convergence_rate",
+                "mean_iterations"):
+        assert abs(getattr(ours, key) - theirs[key]) < 1e-12, key
+
+
+@pytest.mark.parametrize("mode", ["float", "int8", "int16"])
+def test_campaign_counts_equal_reference_bb72(ref, mode):
+    """acceptance check 7's configuration (proj/tests/acceptance.cpp:288-314) and a
+    high-noise point where logical misclassifications actually occur."""
+    code = codes.make_code("bb72")
+    rc = ref.code("bb72")
+    for p, seed, trials, iters in ((0.01, 20260822, 4000, 10), (0.06, 7, 3000, 30)):
+        cfg = DecoderConfig(max_iterations=iters, arithmetic=mode)
+        theirs = ref.run_campaign(rc, 0, p, seed, trials, cfg, workers=0)
+        ours = run_campaign(code, p, seed, trials, cfg)
+        _same(ours, theirs)
+    assert theirs["logical_x"] + theirs["logical_z"] + theirs["logical_both"] > 0
+
+
+def test_campaign_counts_equal_reference_bb784(ref):
+    code = codes.make_code("bb784")
+    rc = ref.code("bb784")
+    cfg = DecoderConfig(max_iterations=50)
+    theirs = ref.run_campaign(rc, 0, 0.02, 12345, 1500, cfg, workers=0)
+    ours = run_campaign(code, 0.02, 12345, 1500, cfg)
+    _same(ours, theirs)
+
+
+def test_campaign_is_independent_of_the_partition():
+    """Deterministic for a fixed seed, independent of the worker / rank count
+    (proj/tests/test_noise.cpp:372-434): per-shard counters add up exactly."""
+    code = codes.make_code("bb144")
+    cfg = DecoderConfig(max_iterations=20)
+    camp = Campaign(code, cfg)
+    try:
+        whole = camp.run_range(0.03, 99, 0, 5000)
+        for world in (2, 3, 8):
+            total = np.zeros_like(whole)
+            for rank in range(world):
+                lo, hi = shard(5000, world, rank)
+                total += camp.run_range(0.03, 99, lo, hi - lo)
+            assert np.array_equal(total, whole)
+    finally:
+        camp.close()
+
+
+def test_decoder_beats_the_identity_baseline():
+    """proj/tests/test_noise.cpp:446-457: LER < 0.05 and baseline > 0.5 at p = 0.01 on bb72."""
+    r = run_campaign(codes.make_code("bb72"), 0.01, 20260822, 10000, DecoderConfig())
+    assert r.logical_error_rate < 0.05 and r.baseline_logical_rate > 0.5
