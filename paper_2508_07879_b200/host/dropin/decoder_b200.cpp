@@ -1,0 +1,276 @@
+// DROP-IN replacement for the reference's proj/src/decoder.cpp: defines every
+// symbol proj/include/qldpc/decoder.hpp declares, on top of the C-ABI
+// (include/qldpc_b200.h), so the rest of the reference library - run_campaign,
+// run_bench, the CLI, the acceptance runner - links against the GPU decoder
+// without a source change.  Compiled against the reference's own headers
+// (INTEGRATION.md); nothing is copied from the reference: the engine lives in
+// CUDA behind the ABI and the definitional node operations below are restated
+// from their documented contracts (decoder.hpp:48-70).
+#include "qldpc/decoder.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <stdexcept>
+#include <string>
+
+#include "qldpc_b200.h"
+
+namespace qldpc {
+
+namespace {
+
+[[noreturn]] void raise(qb_status st, const qb_decoder* h) {
+  const std::string msg = qb_last_error(h);
+  if (st == QB_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+void assign_bits(Gf2Vector& dst, std::size_t len, const std::uint64_t* words) {
+  if (dst.size() != len) dst = Gf2Vector(len);
+  auto w = dst.words();
+  std::copy(words, words + w.size(), w.begin());
+}
+
+int arith_code(Arithmetic a) {
+  switch (a) {
+    case Arithmetic::kFloat: return QB_ARITH_FLOAT;
+    case Arithmetic::kInt8: return QB_ARITH_INT8;
+    case Arithmetic::kInt16: return QB_ARITH_INT16;
+  }
+  throw std::invalid_argument("DecoderConfig: unknown arithmetic mode");
+}
+
+qb_decoder* make_handle(const TannerGraph& graph, const DecoderConfig& cfg,
+                        const std::vector<qb_segment>& segs) {
+  qb_graph g{static_cast<std::uint32_t>(graph.num_checks),
+             static_cast<std::uint32_t>(graph.num_vars),
+             static_cast<std::uint32_t>(graph.num_edges()), graph.edge_var.data(),
+             graph.check_offsets.data(), graph.var_offsets.data(), graph.var_edges.data()};
+  qb_config c{cfg.max_iterations, cfg.alpha, cfg.early_termination ? 1 : 0,
+              arith_code(cfg.arithmetic), cfg.quant_scale,
+              cfg.priors.empty() ? nullptr : cfg.priors.data(), cfg.priors.size()};
+  qb_decoder* h = nullptr;
+  const qb_status st = qb_decoder_create(&g, segs.empty() ? nullptr : segs.data(),
+                                         static_cast<std::uint32_t>(segs.size()), &c, 0, &h);
+  if (st != QB_OK) raise(st, nullptr);
+  return h;
+}
+
+}  // namespace
+
+std::string_view arithmetic_name(Arithmetic mode) {
+  return mode == Arithmetic::kFloat ? "float" : mode == Arithmetic::kInt8 ? "int8"
+         : mode == Arithmetic::kInt16 ? "int16" : "unknown";
+}
+
+Arithmetic parse_arithmetic(std::string_view name) {
+  for (Arithmetic a : {Arithmetic::kFloat, Arithmetic::kInt8, Arithmetic::kInt16}) {
+    if (name == arithmetic_name(a)) return a;
+  }
+  throw std::invalid_argument("unknown arithmetic mode '" + std::string(name) +
+                              "' (expected float, int8 or int16)");
+}
+
+// ---- definitional node operations (host side; decoder.hpp:48-70) ----------------
+
+int syndrome_sign(int s_bit) {
+  if (s_bit == 0) return 1;
+  if (s_bit == 1) return -1;
+  throw std::invalid_argument("syndrome_sign: bit must be 0 or 1");
+}
+
+std::vector<double> check_node_update(std::span<const double> q_in, int s_bit, double alpha) {
+  if (q_in.empty()) throw std::invalid_argument("check_node_update: at least one input message required");
+  if (!(alpha > 0.0 && alpha <= 1.0)) throw std::invalid_argument("check_node_update: alpha must lie in (0, 1]");
+  const double scaled_sign = alpha * syndrome_sign(s_bit);
+  const std::size_t d = q_in.size();
+  if (d == 1) return {scaled_sign * 64.0};  // a lone edge is pinned to the syndrome value
+  std::vector<double> out(d);
+  for (std::size_t e = 0; e < d; ++e) {
+    double smallest = std::numeric_limits<double>::infinity();
+    bool odd_negatives = false;
+    for (std::size_t o = 0; o < d; ++o) {
+      if (o == e) continue;
+      odd_negatives ^= q_in[o] < 0.0;
+      smallest = std::min(smallest, std::fabs(q_in[o]));
+    }
+    const double magnitude = scaled_sign * smallest;
+    out[e] = odd_negatives ? -magnitude : magnitude;
+  }
+  return out;
+}
+
+std::vector<double> variable_node_update(double gamma, std::span<const double> r_in) {
+  if (r_in.size() == 1) return {gamma};
+  double total = gamma;
+  for (double r : r_in) total += r;
+  std::vector<double> out(r_in.size());
+  for (std::size_t e = 0; e < r_in.size(); ++e) out[e] = total - r_in[e];
+  return out;
+}
+
+std::pair<double, int> posterior_and_decision(double gamma, std::span<const double> r_in) {
+  double total = gamma;
+  for (double r : r_in) total += r;
+  return {total, total < 0.0 ? 1 : 0};
+}
+
+std::int32_t quantize_saturate(double value, double scale, std::int32_t limit) {
+  const double x = value * scale;
+  if (std::isnan(x)) throw std::invalid_argument("quantize_saturate: value is NaN");
+  if (x >= static_cast<double>(limit)) return limit;
+  if (x <= -static_cast<double>(limit)) return -limit;
+  return static_cast<std::int32_t>(std::llround(x));
+}
+
+// ---- Decoder over the C-ABI ---------------------------------------------------
+
+struct Decoder::Impl {
+  DecoderConfig cfg;
+  qb_decoder* h = nullptr;
+  std::size_t m = 0, n = 0;
+  std::vector<qb_segment> segs;
+  std::vector<std::uint64_t> est, res;
+  std::vector<std::uint8_t> conv;
+  std::vector<std::uint32_t> its;
+
+  Impl(const TannerGraph& graph, DecoderConfig config, std::vector<qb_segment> segments)
+      : cfg(std::move(config)), m(graph.num_checks), n(graph.num_vars), segs(std::move(segments)) {
+    h = make_handle(graph, cfg, segs);
+    const std::size_t ns = std::max<std::size_t>(segs.size(), 1);
+    est.resize((n + 63) / 64);
+    res.resize((m + 63) / 64);
+    conv.resize(ns);
+    its.resize(ns);
+  }
+  ~Impl() { qb_decoder_destroy(h); }
+
+  void run(const Gf2Vector& syndrome) {
+    const qb_status st =
+        qb_decode(h, syndrome.words().data(), est.data(), res.data(), conv.data(), its.data());
+    if (st != QB_OK) raise(st, h);
+  }
+};
+
+Decoder::Decoder(const TannerGraph& graph, DecoderConfig cfg)
+    : impl_(std::make_unique<Impl>(graph, std::move(cfg), std::vector<qb_segment>{})) {}
+
+Decoder::Decoder(const CssCode& code, DecoderConfig cfg) {
+  const auto mz = static_cast<std::uint32_t>(code.hz().rows());
+  const auto mx = static_cast<std::uint32_t>(code.hx().rows());
+  const auto n = static_cast<std::uint32_t>(code.num_qubits());
+  impl_ = std::make_unique<Impl>(code.combined_graph(), std::move(cfg),
+                                 std::vector<qb_segment>{{0, mz, 0, n}, {mz, mz + mx, n, 2 * n}});
+}
+
+Decoder::~Decoder() = default;
+Decoder::Decoder(Decoder&&) noexcept = default;
+Decoder& Decoder::operator=(Decoder&&) noexcept = default;
+
+const DecoderConfig& Decoder::config() const { return impl_->cfg; }
+std::size_t Decoder::num_checks() const { return impl_->m; }
+std::size_t Decoder::num_vars() const { return impl_->n; }
+std::uint64_t Decoder::last_kernel_ns() const { return qb_last_kernel_ns(impl_->h); }
+
+DecodeOutcome Decoder::decode(const Gf2Vector& syndrome) {
+  DecodeOutcome out;
+  decode_into(syndrome, out);
+  return out;
+}
+
+void Decoder::decode_into(const Gf2Vector& syndrome, DecodeOutcome& out) {
+  Impl& I = *impl_;
+  if (syndrome.size() != I.m) {
+    throw std::invalid_argument("decode: syndrome has " + std::to_string(syndrome.size()) +
+                                " bits but the graph has " + std::to_string(I.m) + " checks");
+  }
+  I.run(syndrome);
+  assign_bits(out.error_estimate, I.n, I.est.data());
+  assign_bits(out.syndrome_residual, I.m, I.res.data());
+  out.converged = std::all_of(I.conv.begin(), I.conv.end(), [](std::uint8_t c) { return c != 0; });
+  out.iterations_used = *std::max_element(I.its.begin(), I.its.end());
+}
+
+void Decoder::decode_css_into(const Gf2Vector& s_x, const Gf2Vector& s_z, DecodeOutcome& out_x,
+                              DecodeOutcome& out_z) {
+  Impl& I = *impl_;
+  if (I.segs.size() != 2) {
+    throw std::invalid_argument("decode_css_into: decoder was not built from a CssCode");
+  }
+  const qb_segment &sx = I.segs[0], &sz = I.segs[1];
+  const std::size_t xc = sx.check_end - sx.check_begin, zc = sz.check_end - sz.check_begin;
+  if (s_x.size() != xc || s_z.size() != zc) {
+    throw std::invalid_argument("decode_css_into: syndrome lengths (" + std::to_string(s_x.size()) +
+                                ", " + std::to_string(s_z.size()) +
+                                ") do not match the code's check counts (" + std::to_string(xc) +
+                                ", " + std::to_string(zc) + ")");
+  }
+  I.run(s_x.concat(s_z));
+  Gf2Vector est, res;
+  assign_bits(est, I.n, I.est.data());
+  assign_bits(res, I.m, I.res.data());
+  out_x.error_estimate = est.slice(sx.var_begin, sx.var_end);
+  out_x.syndrome_residual = res.slice(sx.check_begin, sx.check_end);
+  out_x.converged = I.conv[0] != 0;
+  out_x.iterations_used = I.its[0];
+  out_z.error_estimate = est.slice(sz.var_begin, sz.var_end);
+  out_z.syndrome_residual = res.slice(sz.check_begin, sz.check_end);
+  out_z.converged = I.conv[1] != 0;
+  out_z.iterations_used = I.its[1];
+}
+
+DecodeOutcome decode(const TannerGraph& graph, const Gf2Vector& syndrome, const DecoderConfig& cfg) {
+  Decoder decoder(graph, cfg);
+  return decoder.decode(syndrome);
+}
+
+std::vector<DecodeOutcome> decode_batch(const TannerGraph& graph,
+                                        std::span<const Gf2Vector> syndromes,
+                                        const DecoderConfig& cfg, unsigned /*num_workers*/) {
+  // One persistent-kernel launch decodes the whole batch; num_workers names CPU
+  // threads in the reference and has no meaning here.
+  for (std::size_t i = 0; i < syndromes.size(); ++i) {
+    if (syndromes[i].size() != graph.num_checks) {
+      throw std::invalid_argument("decode_batch: syndrome " + std::to_string(i) + " has " +
+                                  std::to_string(syndromes[i].size()) +
+                                  " bits but the graph has " + std::to_string(graph.num_checks) +
+                                  " checks");
+    }
+  }
+  std::vector<DecodeOutcome> out(syndromes.size());
+  if (syndromes.empty()) return out;
+  struct Handle {
+    qb_decoder* h;
+    ~Handle() { qb_decoder_destroy(h); }
+  } handle{make_handle(graph, cfg, {})};
+  const std::size_t shots = syndromes.size(), sw = (graph.num_checks + 63) / 64,
+                    ew = (graph.num_vars + 63) / 64;
+  std::vector<std::uint64_t> syn(shots * sw), est(shots * ew), res(shots * sw);
+  std::vector<std::uint8_t> conv(shots);
+  std::vector<std::uint32_t> its(shots);
+  for (std::size_t i = 0; i < shots; ++i) {
+    std::copy(syndromes[i].words().begin(), syndromes[i].words().end(), syn.begin() + i * sw);
+  }
+  qb_decoder* h = handle.h;
+  const qb_status st = qb_decode_batch(h, shots, syn.data(), est.data(), res.data(), conv.data(),
+                                       its.data());
+  if (st != QB_OK) raise(st, h);
+  for (std::size_t i = 0; i < shots; ++i) {
+    assign_bits(out[i].error_estimate, graph.num_vars, est.data() + i * ew);
+    assign_bits(out[i].syndrome_residual, graph.num_checks, res.data() + i * sw);
+    out[i].converged = conv[i] != 0;
+    out[i].iterations_used = its[i];
+  }
+  return out;
+}
+
+CssDecodeResult decode_css(const CssCode& code, const Gf2Vector& s_x, const Gf2Vector& s_z,
+                           const DecoderConfig& cfg) {
+  Decoder decoder(code, cfg);
+  CssDecodeResult result;
+  decoder.decode_css_into(s_x, s_z, result.x, result.z);
+  return result;
+}
+
+}  // namespace qldpc
