@@ -213,7 +213,9 @@ def run_ours(args):
     g = code.combined_graph
     cfg = DecoderConfig(max_iterations=args.max_iterations,
                         early_termination=not args.no_early_stop, arithmetic=args.arithmetic)
-    dec = Decoder(code, cfg, device=local)
+    from paper_2508_07879_b200.campaign import COUNTER_NAMES, Campaign, CampaignResult
+    camp = Campaign(code, cfg, device=local)  # decoder + residual tests (logical operators)
+    dec = camp.decoder
     lib = _lib.load()
     shots = args.shots
     sw, ew, nseg = gf2.num_words(g.num_checks), gf2.num_words(g.num_vars), dec.num_segments
@@ -256,17 +258,21 @@ def run_ours(args):
     total_ms = float(t.item())
     value = world * shots * args.steps / (total_ms * 1e-3)
 
-    # ---- outcome counters: the only data-path collective
+    # ---- outcome counters: the only data-path collective.  The batch is
+    # classified on the device (exact / stabilizer / logical / non-converged, as the
+    # reference's run_campaign does) and the ten counters + the edge-update count are summed
+    # over ranks with ONE all-reduce.
     seg_edges = [int(g.check_offsets[c1] - g.check_offsets[c0]) for c0, c1, _, _ in code.segments]
     its64 = d_its.to(torch.int64)
     edge_updates = sum(int(its64[:, s].sum().item()) * seg_edges[s] for s in range(nseg))
-    conv_all = d_conv.min(dim=1).values
-    counters = torch.tensor([shots, int((conv_all == 0).sum().item()),
-                             int(its64.max(dim=1).values.sum().item()), edge_updates],
-                            dtype=torch.int64, device=dev)
+    cls = camp.classify_device(shots, d_err.data_ptr(), d_est.data_ptr(), d_syn.data_ptr(),
+                               d_conv.data_ptr(), d_its.data_ptr(), stream)
+    counters = torch.tensor([int(x) for x in cls] + [edge_updates], dtype=torch.int64, device=dev)
     if dist is not None:
         dist.all_reduce(counters, op=dist.ReduceOp.SUM)
-    tot_shots, non_conv, iter_sum, edge_updates_all = [int(x) for x in counters.tolist()]
+    totals = [int(x) for x in counters.tolist()]
+    result = CampaignResult.from_counters(totals[:len(COUNTER_NAMES)])
+    edge_updates_all = totals[-1]
 
     if rank != 0:
         if dist is not None:
@@ -314,9 +320,16 @@ def run_ours(args):
                    "l2": "inputs+outputs per step exceed L2 (no flush needed)",
                    "generator": "on-device SplitMix64 (reference-exact), seed %d" % args.seed},
         "roofline": roofline, "gpu_launches": int(launches), "clocks": clocks,
-        "outcomes": {"shots": tot_shots, "non_converged": non_conv,
-                     "mean_iterations": iter_sum / max(tot_shots, 1),
-                     "logical_error_rate_nonconv": non_conv / max(tot_shots, 1)},
+        "outcomes": {"shots": result.trials, "exact": result.exact,
+                     "stabilizer": result.stabilizer, "logical_x": result.logical_x,
+                     "logical_z": result.logical_z, "logical_both": result.logical_both,
+                     "non_converged": result.non_converged,
+                     "logical_error_rate": result.logical_error_rate,
+                     "baseline_logical_rate": result.baseline_logical_rate,
+                     "convergence_rate": result.convergence_rate,
+                     "mean_iterations": result.mean_iterations,
+                     "edge_updates_all_ranks_per_step": edge_updates_all,
+                     "reduction": "one all_reduce(SUM) of 11 int64 counters"},
     }
 
     # ---- e2e: the public batch call on HOST (pinned) buffers, copies inside the timed region

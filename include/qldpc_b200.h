@@ -246,6 +246,16 @@ qb_status qb_set_logicals(qb_decoder* h, const uint64_t* x_tests, uint32_t n_x,
 qb_status qb_campaign_run(qb_decoder* h, uint64_t seed, double p,
                           const double* probs, uint64_t first_trial,
                           uint64_t trials, uint64_t* counters);
+/* The classification step alone, on buffers already resident in DEVICE memory
+ * (errors from qb_generate_syndromes, outputs of qb_decode_batch_device);
+ * ADDS to the same ten host counters. */
+qb_status qb_classify_batch_device(qb_decoder* h, uint64_t shots,
+                                   const uint64_t* d_errors,
+                                   const uint64_t* d_estimates,
+                                   const uint64_t* d_syndromes,
+                                   const uint8_t* d_converged,
+                                   const uint32_t* d_iterations,
+                                   uint64_t* counters, void* stream);
 
 /* Pinned (page-locked, device-mapped) host memory for batch I/O. */
 qb_status qb_host_alloc(void** out, size_t bytes);

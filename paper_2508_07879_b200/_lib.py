@@ -75,6 +75,8 @@ SYMBOLS = {
     "qb_set_logicals": (C.c_int, [C.c_void_p, u64p, C.c_uint32, u64p, C.c_uint32]),
     "qb_campaign_run": (C.c_int, [C.c_void_p, C.c_uint64, C.c_double, f64p, C.c_uint64,
                                   C.c_uint64, u64p]),
+    "qb_classify_batch_device": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
+                                           C.c_void_p, C.c_void_p, C.c_void_p, u64p, C.c_void_p]),
     "qb_last_kernel_ns": (C.c_uint64, [C.c_void_p]),
     "qb_launch_count": (C.c_uint64, [C.c_void_p]),
 }

@@ -192,6 +192,17 @@ class Campaign:
             _raise(st, self.decoder._h)
         return counters
 
+    def classify_device(self, shots: int, d_err: int, d_est: int, d_syn: int, d_conv: int,
+                        d_its: int, stream: int = 0) -> np.ndarray:
+        """qb_classify_batch_device on resident buffers -> the ten counters."""
+        counters = np.zeros(len(COUNTER_NAMES), dtype=np.uint64)
+        st = _lib.load().qb_classify_batch_device(self.decoder._h, shots, d_err, d_est, d_syn,
+                                                  d_conv, d_its,
+                                                  counters.ctypes.data_as(_lib.u64p), stream)
+        if st != _lib.QB_OK:
+            _raise(st, self.decoder._h)
+        return counters
+
     def close(self) -> None:
         self.decoder.close()
 

@@ -82,6 +82,9 @@ size_t msg_bytes_of(int arith) {
 using KernelFn = void (*)(DecodeParams, ShotIO);
 using LatKernelFn = void (*)(DecodeParams, ShotIO, LatencyCtl, SynInline);
 
+constexpr int kPipeSlots = 3;                      // qb_decode_batch: chunks in flight
+constexpr int kSchedWords = 2 + kMaxSegments;      // scheduler words per concurrent launch
+
 struct LaunchPlan {
   KernelFn kernel = nullptr;
   const char* name = "";
@@ -102,6 +105,8 @@ struct qb_decoder {
   int sm_count = 0;
   int max_smem_optin = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t pipe_stream[kPipeSlots] = {};
+  cudaEvent_t pipe_event[kPipeSlots] = {};
   DecodeParams P{};
   int arith = 0;
   std::vector<void*> dev_allocs;  // tables, freed in the destructor
@@ -198,6 +203,10 @@ void destroy(qb_decoder* h) {
   if (h->h_in) cudaFreeHost(h->h_in);
   if (h->h_out) cudaFreeHost(h->h_out);
   free_batch(h);
+  for (int k = 0; k < kPipeSlots; ++k) {
+    if (h->pipe_stream[k]) cudaStreamDestroy(h->pipe_stream[k]);
+    if (h->pipe_event[k]) cudaEventDestroy(h->pipe_event[k]);
+  }
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -569,7 +578,8 @@ unsigned batch_grid(qb_decoder* h, uint64_t shots) {
 }
 
 void run_batch_device(qb_decoder* h, uint64_t shots, const uint32_t* d_syn, uint32_t* d_est,
-                      uint32_t* d_res, uint8_t* d_conv, uint32_t* d_iters, cudaStream_t stream) {
+                      uint32_t* d_res, uint8_t* d_conv, uint32_t* d_iters, cudaStream_t stream,
+                      int sched_slot = 0) {
   if (shots == 0) return;
   if (shots > 0x7fff0000ull) fail(QB_INVALID_ARGUMENT, "too many shots for one launch");
   ShotIO io{};
@@ -579,7 +589,7 @@ void run_batch_device(qb_decoder* h, uint64_t shots, const uint32_t* d_syn, uint
   io.resid = d_res;
   io.conv = d_conv;
   io.iters = d_iters;
-  io.sched = h->d_sched;
+  io.sched = h->d_sched + sched_slot * kSchedWords;  // concurrent launches need their own tickets
   launch_plan(h, h->bat, io, batch_grid(h, shots), stream);
 }
 
@@ -1102,8 +1112,12 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
     }
     make_plans(h);
 
-    CUDA_TRY(cudaMalloc(&h->d_sched, (2 + kMaxSegments) * sizeof(unsigned int)));
-    CUDA_TRY(cudaMemset(h->d_sched, 0, (2 + kMaxSegments) * sizeof(unsigned int)));
+    CUDA_TRY(cudaMalloc(&h->d_sched, kPipeSlots * kSchedWords * sizeof(unsigned int)));
+    CUDA_TRY(cudaMemset(h->d_sched, 0, kPipeSlots * kSchedWords * sizeof(unsigned int)));
+    for (int k = 0; k < kPipeSlots; ++k) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&h->pipe_stream[k], cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&h->pipe_event[k], cudaEventDisableTiming));
+    }
 
     // ---- single-shot staging
     auto align8 = [](size_t x) { return (x + 7) & ~static_cast<size_t>(7); };
@@ -1382,6 +1396,49 @@ qb_status qb_set_logicals(qb_decoder* h, const uint64_t* x_tests, uint32_t n_x,
   });
 }
 
+qb_status qb_classify_batch_device(qb_decoder* h, uint64_t shots, const uint64_t* d_errors,
+                                   const uint64_t* d_estimates, const uint64_t* d_syndromes,
+                                   const uint8_t* d_converged, const uint32_t* d_iterations,
+                                   uint64_t* counters, void* stream) {
+  if (!h) return QB_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    const DecodeParams& P = h->P;
+    if (!counters || !d_errors || !d_estimates || !d_syndromes || !d_converged || !d_iterations) {
+      fail(QB_INVALID_ARGUMENT, "classify_batch_device: NULL buffer");
+    }
+    if (P.nseg != 2 || !h->d_tests_x || !h->d_tests_z) {
+      fail(QB_INVALID_ARGUMENT, "classify_batch_device: call qb_set_logicals on a CssCode decoder first");
+    }
+    if (shots == 0) return;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (!h->d_counters) CUDA_TRY(cudaMalloc(&h->d_counters, 10 * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemsetAsync(h->d_counters, 0, 10 * sizeof(unsigned long long), st));
+    ClassifyParams cp{};
+    cp.nshots = shots;
+    cp.err = reinterpret_cast<const uint32_t*>(d_errors);
+    cp.est = reinterpret_cast<const uint32_t*>(d_estimates);
+    cp.syn = reinterpret_cast<const uint32_t*>(d_syndromes);
+    cp.conv = d_converged;
+    cp.iters = d_iterations;
+    cp.tests_x = h->d_tests_x;
+    cp.tests_z = h->d_tests_z;
+    cp.n_x = h->n_tests_x;
+    cp.n_z = h->n_tests_z;
+    cp.counters = h->d_counters;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(
+        (shots + kClassifyWarps - 1) / kClassifyWarps, static_cast<uint64_t>(h->sm_count) * 8));
+    const size_t smem = static_cast<size_t>(kClassifyWarps) * 2 * P.est_w32 * 4;
+    classify_kernel<<<grid, kClassifyWarps * 32, smem, st>>>(P, cp);
+    CUDA_TRY(cudaGetLastError());
+    ++h->launches;
+    unsigned long long host_counters[10];
+    CUDA_TRY(cudaMemcpyAsync(host_counters, h->d_counters, sizeof(host_counters),
+                             cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (int k = 0; k < 10; ++k) counters[k] += host_counters[k];
+  });
+}
+
 qb_status qb_campaign_run(qb_decoder* h, uint64_t seed, double p, const double* probs,
                           uint64_t first_trial, uint64_t trials, uint64_t* counters) {
   if (!h) return QB_INVALID_ARGUMENT;
@@ -1443,54 +1500,46 @@ qb_status qb_decode_batch(qb_decoder* h, uint64_t shots, const uint64_t* syndrom
       fail(QB_INVALID_ARGUMENT, "decode_batch: NULL buffer");
     }
     const DecodeParams& P = h->P;
-    // Chunked so that H2D of chunk i+1, the kernel of chunk i and D2H of
-    // chunk i-1 overlap when the host buffers are pinned.
-    const uint64_t kMaxChunk = 1ull << 18;
+    // Chunks rotate over kPipeSlots streams, each with its own device buffers and
+    // scheduler words, so that with pinned host buffers the H2D copy of chunk i+1,
+    // the kernel of chunk i and the D2H copy of chunk i-1 run concurrently (one
+    // copy engine per direction).
+    const uint64_t kMaxChunk = 1ull << 17;
     const uint64_t chunk = std::min<uint64_t>(shots, kMaxChunk);
-    ensure_batch(h, chunk * 2, residuals != nullptr);
-    cudaStream_t st = h->stream;
+    ensure_batch(h, chunk * kPipeSlots, residuals != nullptr);
+    bool used[kPipeSlots] = {};
     uint64_t done = 0;
-    int slot = 0;
-    cudaEvent_t ev[2];
-    CUDA_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
-    bool used[2] = {false, false};
-    try {
-      while (done < shots) {
-        const uint64_t n = std::min<uint64_t>(chunk, shots - done);
-        const uint64_t off = static_cast<uint64_t>(slot) * chunk;
-        if (used[slot]) CUDA_TRY(cudaEventSynchronize(ev[slot]));
-        uint32_t* d_syn = h->b_syn + off * P.syn_w32;
-        uint32_t* d_est = h->b_est + off * P.est_w32;
-        uint32_t* d_res = h->b_res + off * P.syn_w32;
-        uint8_t* d_conv = h->b_conv + off * P.nseg;
-        uint32_t* d_it = h->b_iters + off * P.nseg;
-        CUDA_TRY(cudaMemcpyAsync(d_syn, reinterpret_cast<const uint32_t*>(syndromes) + done * P.syn_w32,
-                                 n * P.syn_w32 * 4, cudaMemcpyHostToDevice, st));
-        run_batch_device(h, n, d_syn, d_est, residuals ? d_res : nullptr, d_conv, d_it, st);
-        CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(estimates) + done * P.est_w32, d_est,
-                                 n * P.est_w32 * 4, cudaMemcpyDeviceToHost, st));
-        if (residuals) {
-          CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(residuals) + done * P.syn_w32, d_res,
-                                   n * P.syn_w32 * 4, cudaMemcpyDeviceToHost, st));
-        }
-        CUDA_TRY(cudaMemcpyAsync(converged + done * P.nseg, d_conv, n * P.nseg,
-                                 cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaMemcpyAsync(iterations + done * P.nseg, d_it, n * P.nseg * 4,
-                                 cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaEventRecord(ev[slot], st));
-        used[slot] = true;
-        slot ^= 1;
-        done += n;
+    for (int slot = 0; done < shots; slot = (slot + 1) % kPipeSlots) {
+      const uint64_t n = std::min<uint64_t>(chunk, shots - done);
+      const uint64_t off = static_cast<uint64_t>(slot) * chunk;
+      cudaStream_t st = h->pipe_stream[slot];
+      if (used[slot]) CUDA_TRY(cudaEventSynchronize(h->pipe_event[slot]));
+      uint32_t* d_syn = h->b_syn + off * P.syn_w32;
+      uint32_t* d_est = h->b_est + off * P.est_w32;
+      uint32_t* d_res = h->b_res + off * P.syn_w32;
+      uint8_t* d_conv = h->b_conv + off * P.nseg;
+      uint32_t* d_it = h->b_iters + off * P.nseg;
+      CUDA_TRY(cudaMemcpyAsync(d_syn,
+                               reinterpret_cast<const uint32_t*>(syndromes) + done * P.syn_w32,
+                               n * P.syn_w32 * 4, cudaMemcpyHostToDevice, st));
+      run_batch_device(h, n, d_syn, d_est, residuals ? d_res : nullptr, d_conv, d_it, st, slot);
+      CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(estimates) + done * P.est_w32, d_est,
+                               n * P.est_w32 * 4, cudaMemcpyDeviceToHost, st));
+      if (residuals) {
+        CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(residuals) + done * P.syn_w32, d_res,
+                                 n * P.syn_w32 * 4, cudaMemcpyDeviceToHost, st));
       }
-      CUDA_TRY(cudaStreamSynchronize(st));
-    } catch (...) {
-      cudaEventDestroy(ev[0]);
-      cudaEventDestroy(ev[1]);
-      throw;
+      CUDA_TRY(cudaMemcpyAsync(converged + done * P.nseg, d_conv, n * P.nseg,
+                               cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaMemcpyAsync(iterations + done * P.nseg, d_it, n * P.nseg * 4,
+                               cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaEventRecord(h->pipe_event[slot], st));
+      used[slot] = true;
+      done += n;
     }
-    cudaEventDestroy(ev[0]);
-    cudaEventDestroy(ev[1]);
+    for (int slot = 0; slot < kPipeSlots; ++slot) {
+      if (used[slot]) CUDA_TRY(cudaEventSynchronize(h->pipe_event[slot]));
+    }
   });
 }
 
