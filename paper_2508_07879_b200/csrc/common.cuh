@@ -48,6 +48,12 @@ struct DecodeParams {
   double gamma_d;     // (double)float(gamma)
   float gamma_f;
   int32_t gamma_i;
+  // first-iteration constants of the uniform-prior path: every check sends +-S
+  double it1_d;     // fp32 mode: (double)float(alpha * |gamma|)
+  float it1_f;      // fp16 mode: float(half(alpha * |half(gamma)|))
+  float gamma_h;    // fp16 mode: the prior as the kernels add it
+  int32_t it1_i;    // int modes: scale_q16(|gamma|)
+  uint32_t it1_neg; // 1 when gamma < 0 (its sign multiplies every first message)
   // CSR tables (device global memory, read-only)
   const uint32_t* check_off;   // [M + 1]
   const uint32_t* var_off;     // [N + 1]

@@ -240,6 +240,86 @@ __device__ __forceinline__ uint32_t vn3_off(const DecodeParams& P, ArithI16, uns
   return vn3_off_int<kFast, ArithI16>(P, base, eo, gamma);
 }
 
+// ---- first iteration with a uniform prior --------------------------------------
+// Every q equals gamma before the first check stage, so check m sends
+// r = (-1)^(s_m) * sign(gamma) * S on all of its edges, with one constant
+// S = float(alpha * |gamma|) (resp. the Q16 / fp16 analogue) computed by the
+// loader.  The first variable stage can therefore be evaluated directly from the
+// three syndrome bits of a variable's checks: no q initialisation, no check stage,
+// no barrier between them, and no widening conversions (S is a constant).  The
+// arithmetic below is the same sequence of operations the regular stages perform,
+// so the stored q and the decisions are bit-identical.
+__device__ __forceinline__ uint32_t syn_bit_of_edge(const uint32_t* par, uint32_t off,
+                                                     uint32_t stride) {
+  const uint32_t lm = off / stride;
+  return (par[lm >> 5] >> (lm & 31u)) & 1u;
+}
+
+__device__ __forceinline__ uint32_t vn3_first(const DecodeParams& P, ArithF32, unsigned char* base,
+                                              const uint32_t (&eo)[3], const uint32_t* par) {
+  const uint32_t hi0 = static_cast<uint32_t>(__double2hiint(P.it1_d));
+  const int lo = __double2loint(P.it1_d);
+  double r[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const uint32_t flip = syn_bit_of_edge(par, eo[i], Lay<ArithF32>::kStride) ^ P.it1_neg;
+    r[i] = __hiloint2double(static_cast<int>(hi0 ^ (flip << 31)), lo);
+  }
+  double total = P.gamma_d;
+  total += r[0];
+  total += r[1];
+  total += r[2];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    *reinterpret_cast<float*>(base + eo[i]) = static_cast<float>(total - r[i]);
+  }
+  return static_cast<uint32_t>(__double2hiint(total)) >> 31;
+}
+
+__device__ __forceinline__ uint32_t vn3_first(const DecodeParams& P, ArithF16, unsigned char* base,
+                                              const uint32_t (&eo)[3], const uint32_t* par) {
+  float r[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const uint32_t flip = syn_bit_of_edge(par, eo[i], Lay<ArithF16>::kStride) ^ P.it1_neg;
+    r[i] = flip ? -P.it1_f : P.it1_f;
+  }
+  const float total = P.gamma_h + r[0] + r[1] + r[2];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    *reinterpret_cast<__half*>(base + eo[i]) =
+        __float2half_rn(fminf(fmaxf(total - r[i], -kHalfClamp), kHalfClamp));
+  }
+  return total < 0.0f ? 1u : 0u;
+}
+
+template <class A>
+__device__ __forceinline__ uint32_t vn3_first_int(const DecodeParams& P, unsigned char* base,
+                                                  const uint32_t (&eo)[3], const uint32_t* par) {
+  using MsgI = typename A::Msg;
+  int32_t r[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const uint32_t flip = syn_bit_of_edge(par, eo[i], Lay<A>::kStride) ^ P.it1_neg;
+    r[i] = flip ? -P.it1_i : P.it1_i;
+  }
+  const int32_t total = P.gamma_i + r[0] + r[1] + r[2];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    *reinterpret_cast<MsgI*>(base + eo[i]) =
+        static_cast<MsgI>(max(-P.kmax, min(P.kmax, total - r[i])));
+  }
+  return static_cast<uint32_t>(total) >> 31;
+}
+__device__ __forceinline__ uint32_t vn3_first(const DecodeParams& P, ArithI8, unsigned char* base,
+                                              const uint32_t (&eo)[3], const uint32_t* par) {
+  return vn3_first_int<ArithI8>(P, base, eo, par);
+}
+__device__ __forceinline__ uint32_t vn3_first(const DecodeParams& P, ArithI16, unsigned char* base,
+                                              const uint32_t (&eo)[3], const uint32_t* par) {
+  return vn3_first_int<ArithI16>(P, base, eo, par);
+}
+
 // ---- the kernel ---------------------------------------------------------------
 
 template <class A, int CPT, int VPT, bool kFast, int MAXT, int MINB>
@@ -337,18 +417,15 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
         }
       }
     }
-    // q[e] = gamma[var(e)] (decoder.cpp:156-158)
+    // q[e] = gamma[var(e)] (decoder.cpp:156-158) - not needed when the first iteration
+    // is evaluated from the syndrome (uniform prior)
+    if constexpr (!kFast) {
 #pragma unroll
-    for (int k = 0; k < VPT; ++k) {
-      Gam g;
-      if constexpr (kFast) {
-        if constexpr (A::kInt) g = P.gamma_i; else g = P.gamma_f;
-      } else {
-        g = gam[k];
+      for (int k = 0; k < VPT; ++k) {
+        const Msg init = prior_as_msg<A>(gam[k]);
+#pragma unroll
+        for (int i = 0; i < kDV; ++i) *reinterpret_cast<Msg*>(msgs + eo[k][i]) = init;
       }
-      const Msg init = prior_as_msg<A>(g);
-#pragma unroll
-      for (int i = 0; i < kDV; ++i) *reinterpret_cast<Msg*>(msgs + eo[k][i]) = init;
     }
     uint32_t eprev = 0;
     __syncthreads();
@@ -366,15 +443,21 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
     bool still_unsat;
     for (;;) {
       ++iter;
-#pragma unroll
-      for (int k = 0; k < CPT; ++k) cn6_block(P, A{}, msgs + co[k], (synbits >> k) & 1u);
-      __syncthreads();
       uint32_t eb = 0;
+      if (kFast && iter == 1u) {
 #pragma unroll
-      for (int k = 0; k < VPT; ++k) {
-        Gam g{};
-        if constexpr (!kFast) g = gam[k];
-        eb |= vn3_off<kFast>(P, A{}, msgs, eo[k], g) << k;
+        for (int k = 0; k < VPT; ++k) eb |= vn3_first(P, A{}, msgs, eo[k], par) << k;
+        __syncthreads();  // every thread has read its syndrome bits before any toggle
+      } else {
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) cn6_block(P, A{}, msgs + co[k], (synbits >> k) & 1u);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+          Gam g{};
+          if constexpr (!kFast) g = gam[k];
+          eb |= vn3_off<kFast>(P, A{}, msgs, eo[k], g) << k;
+        }
       }
       eb &= valid;
       const uint32_t changed = eb ^ eprev;
@@ -631,17 +714,21 @@ decode_lean_latency_kernel(const __grid_constant__ DecodeParams P,
       if (lane == 0) *unsat = cnt;
     }
     for (uint32_t w = tid; w < ew; w += T) ehat[w] = 0;
+    // the debug dump wants r of the first check stage too, so it takes the long way
+    const bool first_from_syndrome = kFast && io.q_dump == nullptr;
+    if (!first_from_syndrome) {
 #pragma unroll
-    for (int k = 0; k < VPT; ++k) {
-      Gam g;
-      if constexpr (kFast) {
-        if constexpr (A::kInt) g = P.gamma_i; else g = P.gamma_f;
-      } else {
-        g = gam[k];
+      for (int k = 0; k < VPT; ++k) {
+        Gam g;
+        if constexpr (kFast) {
+          if constexpr (A::kInt) g = P.gamma_i; else g = P.gamma_f;
+        } else {
+          g = gam[k];
+        }
+        const Msg init = prior_as_msg<A>(g);
+#pragma unroll
+        for (int i = 0; i < kDV; ++i) *reinterpret_cast<Msg*>(msgs + eo[k][i]) = init;
       }
-      const Msg init = prior_as_msg<A>(g);
-#pragma unroll
-      for (int i = 0; i < kDV; ++i) *reinterpret_cast<Msg*>(msgs + eo[k][i]) = init;
     }
     uint32_t eprev = 0;
     __syncthreads();
@@ -657,15 +744,21 @@ decode_lean_latency_kernel(const __grid_constant__ DecodeParams P,
     bool still_unsat;
     for (;;) {
       ++iter;
-#pragma unroll
-      for (int k = 0; k < CPT; ++k) cn6_block(P, A{}, msgs + co[k], (synbits >> k) & 1u);
-      __syncthreads();
       uint32_t eb = 0;
+      if (first_from_syndrome && iter == 1u) {
 #pragma unroll
-      for (int k = 0; k < VPT; ++k) {
-        Gam g{};
-        if constexpr (!kFast) g = gam[k];
-        eb |= vn3_off<kFast>(P, A{}, msgs, eo[k], g) << k;
+        for (int k = 0; k < VPT; ++k) eb |= vn3_first(P, A{}, msgs, eo[k], par) << k;
+        __syncthreads();  // every thread has read its syndrome bits before any toggle
+      } else {
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) cn6_block(P, A{}, msgs + co[k], (synbits >> k) & 1u);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+          Gam g{};
+          if constexpr (!kFast) g = gam[k];
+          eb |= vn3_off<kFast>(P, A{}, msgs, eo[k], g) << k;
+        }
       }
       eb &= valid;
       const uint32_t changed = eb ^ eprev;

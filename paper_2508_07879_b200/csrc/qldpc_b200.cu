@@ -1099,6 +1099,23 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
         }
       }
       h->fast_ok = uniform && clamp_free;
+      // constants of the first iteration on the uniform-prior path (kernel_lean.cuh)
+      if (!gamma_f.empty()) {
+        const float g0 = gamma_f[0];
+        P.it1_neg = g0 < 0.0f ? 1u : 0u;
+        P.it1_d = static_cast<double>(
+            static_cast<float>(config->alpha * static_cast<double>(std::fabs(g0))));
+        // fp16: q starts as half(clamp(gamma)); the check scales its magnitude in fp32
+        const float gclamp = std::fmin(std::fmax(g0, -kHalfClamp), kHalfClamp);
+        const float qh = __half2float(__float2half_rn(gclamp));
+        P.it1_f = __half2float(__float2half_rn(static_cast<float>(config->alpha) * std::fabs(qh)));
+        P.gamma_h = g0;
+      } else {
+        const int32_t g0 = gamma_i[0];
+        P.it1_neg = g0 < 0 ? 1u : 0u;
+        P.it1_i = static_cast<int32_t>(
+            (static_cast<int64_t>(g0 < 0 ? -g0 : g0) * alpha_fx + 32768) >> 16);
+      }
     }
     {
       bool reg = P.nseg <= 8;
