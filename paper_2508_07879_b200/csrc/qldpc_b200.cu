@@ -338,6 +338,9 @@ constexpr LeanVariant kLeanVariants[] = {
     {3, 5, 192, 5},   // 4
     {4, 8, 128, 6},   // 5
     {2, 4, 512, 2},   // 6
+    {3, 5, 160, 5},   // 7: 80 registers, five 5-warp CTAs per SM
+    {3, 5, 160, 4},   // 8: 102 registers
+    {2, 4, 224, 4},   // 9: 72 registers, four 7-warp CTAs per SM
 };
 constexpr int kNumLeanVariants = sizeof(kLeanVariants) / sizeof(kLeanVariants[0]);
 
@@ -349,6 +352,9 @@ KernelFn lean_kernel_tf(int variant) {
     case 3: return decode_lean_kernel<A, 2, 4, kFast, 256, 3>;
     case 4: return decode_lean_kernel<A, 3, 5, kFast, 192, 5>;
     case 5: return decode_lean_kernel<A, 4, 8, kFast, 128, 6>;
+    case 7: return decode_lean_kernel<A, 3, 5, kFast, 160, 5>;
+    case 8: return decode_lean_kernel<A, 3, 5, kFast, 160, 4>;
+    case 9: return decode_lean_kernel<A, 2, 4, kFast, 224, 4>;
     default: return decode_lean_kernel<A, 2, 4, kFast, 512, 2>;
   }
 }
@@ -1184,7 +1190,7 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
         break;
       case QB_OPT_BATCH_VARIANT:
         if (value < 0 || value > kNumLeanVariants) {
-          fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_VARIANT: 0 .. 6");
+          fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_VARIANT: 0 .. 9");
         }
         h->opt_batch_npt = value;
         break;
