@@ -486,6 +486,21 @@ class Ref:
         out.update(digest=int(meta[0]), min_iterations=int(meta[1]), max_iterations=int(meta[2]))
         return out
 
+    def read_bench_csv_file(self, path: str):
+        """The reference's validating CSV reader -> (row count, p99 of the first row)."""
+        rows, p99 = C.c_uint64(), C.c_double()
+        self._check(self.lib.ref_read_bench_csv_file(path.encode(), C.byref(rows), C.byref(p99)))
+        return int(rows.value), float(p99.value)
+
+    def load_alist(self, text: str):
+        """The reference's load_alist -> (rows, cols, (nnz, 2) COO array)."""
+        rows, cols, nnz = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        buf = np.zeros((max(len(text), 16), 2), dtype=np.uint32)
+        self._check(self.lib.ref_load_alist(text.encode(), C.byref(rows), C.byref(cols),
+                                            _p(buf, u32p), C.c_uint64(buf.shape[0]),
+                                            C.byref(nnz)))
+        return int(rows.value), int(cols.value), buf[:int(nnz.value)].copy()
+
     def host_descriptor(self) -> str:
         buf = C.create_string_buffer(512)
         self._check(self.lib.ref_host_descriptor(buf, C.c_uint64(512)))

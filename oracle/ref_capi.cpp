@@ -18,6 +18,7 @@
 #include <string>
 #include <vector>
 
+#include "qldpc/alist.hpp"
 #include "qldpc/bench.hpp"
 #include "qldpc/css_code.hpp"
 #include "qldpc/decoder.hpp"
@@ -508,6 +509,34 @@ int ref_run_bench(const void* code, int arith, double alpha,
     meta[0] = r.output_digest;
     meta[1] = r.min_iterations_used;
     meta[2] = r.max_iterations_used;
+  });
+}
+
+// Validating reader of the reference (read_bench_csv_file): returns the row count.
+int ref_read_bench_csv_file(const char* path, std::uint64_t* rows, double* first_p99) {
+  return guarded([&] {
+    const std::vector<BenchRecord> recs = read_bench_csv_file(path);
+    *rows = recs.size();
+    if (first_p99 && !recs.empty()) *first_p99 = recs[0].p99_us;
+  });
+}
+
+// load_alist on a text; returns the matrix as COO (row, col) pairs.
+int ref_load_alist(const char* text, std::uint64_t* rows, std::uint64_t* cols,
+                   std::uint32_t* rc, std::uint64_t cap, std::uint64_t* nnz) {
+  return guarded([&] {
+    const SparseGf2Matrix h = load_alist(std::string(text));
+    *rows = h.rows();
+    *cols = h.cols();
+    *nnz = h.nnz();
+    if (h.nnz() > cap) throw std::runtime_error("ref_load_alist: buffer too small");
+    std::size_t k = 0;
+    for (std::size_t r = 0; r < h.rows(); ++r) {
+      for (std::uint32_t c : h.row_support(r)) {
+        rc[k++] = static_cast<std::uint32_t>(r);
+        rc[k++] = c;
+      }
+    }
   });
 }
 

@@ -65,3 +65,24 @@ def test_decoder_beats_the_identity_baseline():
     """proj/tests/test_noise.cpp:446-457: LER < 0.05 and baseline > 0.5 at p = 0.01 on bb72."""
     r = run_campaign(codes.make_code("bb72"), 0.01, 20260822, 10000, DecoderConfig())
     assert r.logical_error_rate < 0.05 and r.baseline_logical_rate > 0.5
+
+
+def test_half_precision_ler_within_reference_ci(ref):
+    """north star: the reduced-precision (fp16) path has no bit-level oracle; its
+    logical error rate must lie within the 95 % binomial confidence interval of the
+    reference decoder's (float) on the same noise model."""
+    import math
+    code = codes.make_code("bb144")
+    rc = ref.code("bb144")
+    for p, iters in ((0.02, 30), (0.04, 30)):
+        trials_ref = 12000
+        rr = ref.run_campaign(rc, 0, p, 4242, trials_ref, DecoderConfig(max_iterations=iters),
+                              workers=0)
+        k = rr["logical_x"] + rr["logical_z"] + rr["logical_both"] + rr["non_converged"]
+        ph, z = k / trials_ref, 1.96
+        den = 1 + z * z / trials_ref
+        c = (ph + z * z / (2 * trials_ref)) / den
+        hw = z * math.sqrt(ph * (1 - ph) / trials_ref + z * z / (4 * trials_ref ** 2)) / den
+        ours = run_campaign(code, p, 4242, 200000,
+                            DecoderConfig(max_iterations=iters, arithmetic="half"))
+        assert c - hw <= ours.logical_error_rate <= c + hw, (p, ours.logical_error_rate, c, hw)
