@@ -116,6 +116,10 @@ typedef enum {
    * drawn from per-segment queues (the lean item kernel; the auto choice). */
   QB_OPT_BATCH_SHAPE = 8,
   QB_OPT_DOORBELL_IDLE_MS = 9,
+  /* Half mode, batch calls: 1 (default) = decode two shots per thread in the two
+   * lanes of packed fp16 instructions; 0 = one shot per thread.  Results are
+   * identical either way. */
+  QB_OPT_HALF_PAIRS = 10,
   /* Read-only (qb_get_option): the launch plans actually in use. */
   QB_OPT_INFO_BATCH_CTAS_PER_SM = 100,
   QB_OPT_INFO_BATCH_BLOCK = 101,

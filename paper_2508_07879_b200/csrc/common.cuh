@@ -38,7 +38,11 @@ struct DecodeParams {
   uint32_t group_threads;  // threads per group, multiple of 32
   // arithmetic constants
   double alpha;       // float mode: fp64 multiply, one rounding (decoder.cpp:302-307)
-  float alpha_f;      // half mode
+  float alpha_f;      // (unused by the kernels; kept for diagnostics)
+  uint16_t alpha_h;   // half mode: half(alpha)
+  uint16_t deg1_h;    // half mode: half(alpha * 64)
+  uint16_t gamma_hb;  // half mode, uniform prior: half(clamp(gamma))
+  uint16_t it1_h;     // half mode, uniform prior: alpha_h * |gamma_h|
   float deg1_f;       // float(alpha * 64)           (decoder.cpp:256)
   float clamp_f;      // float(1e30)                 (decoder.cpp:23, :238-241)
   uint32_t alpha_fx;  // lround(alpha * 65536)       (decoder.cpp:89)
@@ -50,8 +54,6 @@ struct DecodeParams {
   int32_t gamma_i;
   // first-iteration constants of the uniform-prior path: every check sends +-S
   double it1_d;     // fp32 mode: (double)float(alpha * |gamma|)
-  float it1_f;      // fp16 mode: float(half(alpha * |half(gamma)|))
-  float gamma_h;    // fp16 mode: the prior as the kernels add it
   int32_t it1_i;    // int modes: scale_q16(|gamma|)
   uint32_t it1_neg; // 1 when gamma < 0 (its sign multiplies every first message)
   // CSR tables (device global memory, read-only)
@@ -137,8 +139,23 @@ __device__ __forceinline__ int32_t scale_q16(uint32_t mag, uint32_t alpha_fx) {
   return static_cast<int32_t>((mag * alpha_fx + 32768u) >> 16);
 }
 
-// Half-mode symmetric clamp keeps stored messages finite in fp16 (the analogue
-// of the reference's 1e30 clamp for fp32 storage).
+// Half mode (an extension without a reference counterpart): fp16 storage AND fp16
+// arithmetic, so that the batch kernel can run two shots per thread in the two
+// lanes of a half2 with results identical, lane by lane, to the scalar kernels:
+//   gamma_h = half(clamp(gamma));  r = +-(alpha_h * |q|min)   (one fp16 multiply)
+//   total = ((gamma_h + r0) + r1) + r2   (fp16 adds, ascending edge order)
+//   q = clamp(total - r_e) to +-60000 (keeps stored messages finite, the analogue
+//   of the reference's 1e30 clamp);  decision = sign bit of total.
 constexpr float kHalfClamp = 60000.0f;
+
+__device__ __forceinline__ __half h_clamp(__half x) {
+  const __half c = __ushort_as_half(0x7b53);  // 60000
+  return __hmax(__hmin(x, c), __hneg(c));
+}
+__device__ __forceinline__ __half2 h2_clamp(__half2 x) {
+  const __half2 c = __half2half2(__ushort_as_half(0x7b53));
+  return __hmax2(__hmin2(x, c), __hneg2(c));
+}
+__device__ __forceinline__ bool h_neg(__half x) { return (__half_as_ushort(x) & 0x8000u) != 0; }
 
 }  // namespace qb

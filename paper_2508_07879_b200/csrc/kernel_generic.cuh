@@ -101,16 +101,16 @@ __device__ __forceinline__ void cn_update(const DecodeParams& P, const float* q,
 __device__ __forceinline__ void cn_update(const DecodeParams& P, const __half* q, __half* r,
                                           uint32_t b, uint32_t e1, bool sneg) {
   if (e1 - b == 1) {
-    r[b] = __float2half_rn(sneg ? -P.deg1_f : P.deg1_f);
+    r[b] = __ushort_as_half(static_cast<unsigned short>(P.deg1_h ^ (sneg ? 0x8000u : 0u)));
     return;
   }
-  float m1 = __int_as_float(0x7f800000), m2 = m1;
+  uint32_t m1 = 0x7c00u, m2 = 0x7c00u;  // +inf as an fp16 magnitude key
   uint32_t arg = b;
   uint32_t neg = 0;
   for (uint32_t e = b; e < e1; ++e) {
-    const float v = __half2float(q[e]);
-    neg += v < 0.0f;
-    const float a = fabsf(v);
+    const uint32_t u = __half_as_ushort(q[e]);
+    neg += u >> 15;
+    const uint32_t a = u & 0x7fffu;  // finite fp16 magnitudes order like their bit patterns
     if (a < m1) {
       m2 = m1;
       m1 = a;
@@ -119,12 +119,14 @@ __device__ __forceinline__ void cn_update(const DecodeParams& P, const __half* q
       m2 = a;
     }
   }
-  const float r1 = P.alpha_f * m1, r2 = P.alpha_f * m2;
+  const __half alpha = __ushort_as_half(P.alpha_h);
+  const uint32_t r1 = __half_as_ushort(__hmul(alpha, __ushort_as_half(static_cast<unsigned short>(m1))));
+  const uint32_t r2 = __half_as_ushort(__hmul(alpha, __ushort_as_half(static_cast<unsigned short>(m2))));
   for (uint32_t e = b; e < e1; ++e) {
-    const uint32_t self = __half2float(q[e]) < 0.0f;
+    const uint32_t self = __half_as_ushort(q[e]) >> 15;
     const bool flip = ((neg - self) & 1u) != 0;
-    const float mag = e == arg ? r2 : r1;
-    r[e] = __float2half_rn((sneg != flip) ? -mag : mag);
+    const uint32_t mag = e == arg ? r2 : r1;
+    r[e] = __ushort_as_half(static_cast<unsigned short>(mag | ((sneg != flip) ? 0x8000u : 0u)));
   }
 }
 
@@ -194,18 +196,18 @@ __device__ __forceinline__ bool vn_update(const DecodeParams& P, float* q, const
 __device__ __forceinline__ bool vn_update(const DecodeParams&, __half* q, const __half* r,
                                           const uint32_t* ve, uint32_t b, uint32_t e1,
                                           float gamma) {
-  float total = gamma;
-  for (uint32_t i = b; i < e1; ++i) total += __half2float(r[ve[i]]);
+  const __half g = __float2half_rn(fminf(fmaxf(gamma, -kHalfClamp), kHalfClamp));
+  __half total = g;
+  for (uint32_t i = b; i < e1; ++i) total = __hadd(total, r[ve[i]]);
   if (e1 - b == 1) {
-    q[ve[b]] = __float2half_rn(fminf(fmaxf(gamma, -kHalfClamp), kHalfClamp));
+    q[ve[b]] = g;
   } else {
     for (uint32_t i = b; i < e1; ++i) {
       const uint32_t e = ve[i];
-      const float x = total - __half2float(r[e]);
-      q[e] = __float2half_rn(fminf(fmaxf(x, -kHalfClamp), kHalfClamp));
+      q[e] = h_clamp(__hsub(total, r[e]));
     }
   }
-  return total < 0.0f;
+  return h_neg(total);
 }
 
 template <class MsgI>

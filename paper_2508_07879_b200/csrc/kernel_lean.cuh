@@ -103,10 +103,11 @@ __device__ __forceinline__ void cn6_block(const DecodeParams& P, ArithF16, unsig
   for (int j = 0; j < 6; ++j) a[j] = static_cast<int32_t>(u[j] & 0x7fffu);
   int32_t m1, m2;
   two_smallest6(a, m1, m2);
-  const uint32_t s1 = __half_as_ushort(__float2half_rn(
-      P.alpha_f * __half2float(__ushort_as_half(static_cast<unsigned short>(m1)))));
-  const uint32_t s2 = __half_as_ushort(__float2half_rn(
-      P.alpha_f * __half2float(__ushort_as_half(static_cast<unsigned short>(m2)))));
+  const __half alpha = __ushort_as_half(P.alpha_h);
+  const uint32_t s1 =
+      __half_as_ushort(__hmul(alpha, __ushort_as_half(static_cast<unsigned short>(m1))));
+  const uint32_t s2 =
+      __half_as_ushort(__hmul(alpha, __ushort_as_half(static_cast<unsigned short>(m2))));
   const uint32_t sx = u[0] ^ u[1] ^ u[2] ^ u[3] ^ u[4] ^ u[5] ^ (syn_bit << 15);
   uint32_t* rp = reinterpret_cast<uint32_t*>(blk + Lay<ArithF16>::kROff);
 #pragma unroll
@@ -202,17 +203,16 @@ template <bool kFast>
 __device__ __forceinline__ uint32_t vn3_off(const DecodeParams& P, ArithF16, unsigned char* base,
                                             const uint32_t (&eo)[3], float gamma) {
   constexpr uint32_t R = Lay<ArithF16>::kROff;
-  const float r0 = __half2float(*reinterpret_cast<const __half*>(base + eo[0] + R));
-  const float r1 = __half2float(*reinterpret_cast<const __half*>(base + eo[1] + R));
-  const float r2 = __half2float(*reinterpret_cast<const __half*>(base + eo[2] + R));
-  const float total = (kFast ? P.gamma_f : gamma) + r0 + r1 + r2;
-  *reinterpret_cast<__half*>(base + eo[0]) =
-      __float2half_rn(fminf(fmaxf(total - r0, -kHalfClamp), kHalfClamp));
-  *reinterpret_cast<__half*>(base + eo[1]) =
-      __float2half_rn(fminf(fmaxf(total - r1, -kHalfClamp), kHalfClamp));
-  *reinterpret_cast<__half*>(base + eo[2]) =
-      __float2half_rn(fminf(fmaxf(total - r2, -kHalfClamp), kHalfClamp));
-  return total < 0.0f ? 1u : 0u;
+  const __half r0 = *reinterpret_cast<const __half*>(base + eo[0] + R);
+  const __half r1 = *reinterpret_cast<const __half*>(base + eo[1] + R);
+  const __half r2 = *reinterpret_cast<const __half*>(base + eo[2] + R);
+  const __half g = kFast ? __ushort_as_half(P.gamma_hb)
+                         : __float2half_rn(fminf(fmaxf(gamma, -kHalfClamp), kHalfClamp));
+  const __half total = __hadd(__hadd(__hadd(g, r0), r1), r2);
+  *reinterpret_cast<__half*>(base + eo[0]) = h_clamp(__hsub(total, r0));
+  *reinterpret_cast<__half*>(base + eo[1]) = h_clamp(__hsub(total, r1));
+  *reinterpret_cast<__half*>(base + eo[2]) = h_clamp(__hsub(total, r2));
+  return h_neg(total) ? 1u : 0u;
 }
 
 template <bool kFast, class A>
@@ -278,19 +278,18 @@ __device__ __forceinline__ uint32_t vn3_first(const DecodeParams& P, ArithF32, u
 
 __device__ __forceinline__ uint32_t vn3_first(const DecodeParams& P, ArithF16, unsigned char* base,
                                               const uint32_t (&eo)[3], const uint32_t* par) {
-  float r[3];
+  __half r[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     const uint32_t flip = syn_bit_of_edge(par, eo[i], Lay<ArithF16>::kStride) ^ P.it1_neg;
-    r[i] = flip ? -P.it1_f : P.it1_f;
+    r[i] = __ushort_as_half(static_cast<unsigned short>(P.it1_h ^ (flip << 15)));
   }
-  const float total = P.gamma_h + r[0] + r[1] + r[2];
+  const __half total = __hadd(__hadd(__hadd(__ushort_as_half(P.gamma_hb), r[0]), r[1]), r[2]);
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    *reinterpret_cast<__half*>(base + eo[i]) =
-        __float2half_rn(fminf(fmaxf(total - r[i], -kHalfClamp), kHalfClamp));
+    *reinterpret_cast<__half*>(base + eo[i]) = h_clamp(__hsub(total, r[i]));
   }
-  return total < 0.0f ? 1u : 0u;
+  return h_neg(total) ? 1u : 0u;
 }
 
 template <class A>

@@ -1,0 +1,366 @@
+// Reduced-precision throughput kernel: TWO shots per thread in the two lanes of
+// a half2 ((6,3)-regular codes, fp16 messages, fp16 arithmetic).
+//
+// Same structure as decode_lean_kernel (work item per segment, interleaved
+// message blocks, counter-based stop test, first iteration from the syndrome),
+// but every message word holds the values of shots 2k (low half) and 2k+1 (high
+// half), and the node updates use the packed fp16 instructions (HADD2, HMUL2,
+// HMNMX2, HSET2): one instruction advances both shots, there are no conversions
+// at all, and the edge tables in registers are shared by the pair.  Lane by lane
+// the operations are exactly those of the scalar half-mode kernels, so a batch
+// decoded here equals shot-by-shot decoding bit for bit.
+//
+// The two shots of a pair stop independently: a finished lane is frozen (its
+// parity bitmap, counter and decisions are no longer touched) while the other
+// iterates on; the pair is released when both are done.
+#pragma once
+
+#include "common.cuh"
+#include "kernel_lean.cuh"
+
+namespace qb {
+
+constexpr uint32_t kH2Stride = 56, kH2ROff = 24;  // [6 x half2 q | 6 x half2 r | pad]
+
+__host__ __device__ inline size_t lean_h2_smem_bytes(uint32_t seg_mmax) {
+  const size_t msg = (static_cast<size_t>(seg_mmax + 1) * kH2Stride + 15) & ~size_t(15);
+  return msg + 4 * (4 * static_cast<size_t>(lean_pw(seg_mmax)) + 16);
+}
+
+__device__ __forceinline__ __half2 u2h2(uint32_t u) {
+  return *reinterpret_cast<__half2*>(&u);
+}
+__device__ __forceinline__ uint32_t h22u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+// min1 / min2 of six non-negative half2 values, lane-wise (13 packed min/max).
+__device__ __forceinline__ void two_smallest6_h2(const __half2 (&a)[6], __half2& m1, __half2& m2) {
+  const __half2 l0 = __hmin2(a[0], a[1]), h0 = __hmax2(a[0], a[1]);
+  const __half2 l1 = __hmin2(a[2], a[3]), h1 = __hmax2(a[2], a[3]);
+  const __half2 l2 = __hmin2(a[4], a[5]), h2 = __hmax2(a[4], a[5]);
+  m1 = __hmin2(__hmin2(l0, l1), l2);
+  const __half2 med = __hmax2(__hmin2(l0, l1), __hmin2(__hmax2(l0, l1), l2));
+  m2 = __hmin2(med, __hmin2(__hmin2(h0, h1), h2));
+}
+
+// syn_pair: bit 15 = syndrome bit of the low-half shot, bit 31 = of the high-half shot
+__device__ __forceinline__ void cn6_h2(const DecodeParams& P, unsigned char* blk, uint32_t syn_pair) {
+  const uint2* qp = reinterpret_cast<const uint2*>(blk);
+  uint32_t u[6];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const uint2 v = qp[j];
+    u[2 * j] = v.x;
+    u[2 * j + 1] = v.y;
+  }
+  __half2 a[6];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) a[j] = u2h2(u[j] & 0x7fff7fffu);
+  __half2 m1, m2;
+  two_smallest6_h2(a, m1, m2);
+  const __half2 alpha = __half2half2(__ushort_as_half(P.alpha_h));
+  const uint32_t s1 = h22u(__hmul2(alpha, m1)), s2 = h22u(__hmul2(alpha, m2));
+  const uint32_t sx = u[0] ^ u[1] ^ u[2] ^ u[3] ^ u[4] ^ u[5] ^ syn_pair;
+  uint32_t o[6];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) {
+    const uint32_t eq = __heq2_mask(a[j], m1);  // 0xffff in each lane whose magnitude is the minimum
+    o[j] = ((s2 & eq) | (s1 & ~eq)) | ((sx ^ u[j]) & 0x80008000u);
+  }
+  uint2* rp = reinterpret_cast<uint2*>(blk + kH2ROff);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) rp[j] = make_uint2(o[2 * j], o[2 * j + 1]);
+}
+
+// returns the sign bits of the two posteriors (bit 15 / bit 31)
+__device__ __forceinline__ uint32_t vn3_h2(unsigned char* base, const uint32_t (&eo)[3],
+                                           __half2 gamma2) {
+  const __half2 r0 = *reinterpret_cast<const __half2*>(base + eo[0] + kH2ROff);
+  const __half2 r1 = *reinterpret_cast<const __half2*>(base + eo[1] + kH2ROff);
+  const __half2 r2 = *reinterpret_cast<const __half2*>(base + eo[2] + kH2ROff);
+  const __half2 total = __hadd2(__hadd2(__hadd2(gamma2, r0), r1), r2);
+  *reinterpret_cast<__half2*>(base + eo[0]) = h2_clamp(__hsub2(total, r0));
+  *reinterpret_cast<__half2*>(base + eo[1]) = h2_clamp(__hsub2(total, r1));
+  *reinterpret_cast<__half2*>(base + eo[2]) = h2_clamp(__hsub2(total, r2));
+  return h22u(total) & 0x80008000u;
+}
+
+__device__ __forceinline__ uint32_t vn3_first_h2(const DecodeParams& P, unsigned char* base,
+                                                 const uint32_t (&eo)[3], const uint32_t* par_a,
+                                                 const uint32_t* par_b, __half2 gamma2) {
+  const uint32_t mag = static_cast<uint32_t>(P.it1_h) * 0x00010001u;
+  __half2 r[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const uint32_t fa = syn_bit_of_edge(par_a, eo[i], kH2Stride) ^ P.it1_neg;
+    const uint32_t fb = syn_bit_of_edge(par_b, eo[i], kH2Stride) ^ P.it1_neg;
+    r[i] = u2h2(mag ^ (fa << 15) ^ (fb << 31));
+  }
+  const __half2 total = __hadd2(__hadd2(__hadd2(gamma2, r[0]), r[1]), r[2]);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    *reinterpret_cast<__half2*>(base + eo[i]) = h2_clamp(__hsub2(total, r[i]));
+  }
+  return h22u(total) & 0x80008000u;
+}
+
+template <int CPT, int VPT, bool kFast, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB)
+decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_constant__ ShotIO io) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t tid = threadIdx.x, T = blockDim.x, lane = tid & 31u, warp = tid >> 5;
+  const uint32_t nwarps = T >> 5;
+  const uint32_t nseg = P.nseg;
+  const uint32_t s = blockIdx.x % nseg;
+  const uint32_t peer = blockIdx.x / nseg;
+  const uint32_t peers = (gridDim.x - s + nseg - 1) / nseg;
+  const SegmentDev seg = P.segs[s];
+  const uint32_t Ms = seg.c1 - seg.c0;
+  const uint32_t pw = lean_pw(P.seg_mmax);
+  const uint32_t pws = (Ms + 31u) >> 5;
+  const uint32_t gw0 = seg.c0 >> 5, gspan = ((seg.c1 - 1) >> 5) - gw0 + 1, cshift = seg.c0 & 31u;
+  const uint32_t vw0 = seg.v0 >> 5, vspan = ((seg.v1 - 1) >> 5) - vw0 + 1;
+  const uint64_t npairs = (io.nshots + 1) / 2;
+
+  unsigned char* const msgs = smem_raw;
+  const size_t msg_bytes = (static_cast<size_t>(P.seg_mmax + 1) * kH2Stride + 15) & ~size_t(15);
+  uint32_t* const bits = reinterpret_cast<uint32_t*>(smem_raw + msg_bytes);
+  // [item parity][shot lane][pw] bitmaps, then [item parity][shot lane] counters, tickets
+  uint32_t* const unsat_ctr = bits + 4 * pw;  // [2][2]
+  uint32_t* const ticket = bits + 4 * pw + 4;  // [2]
+
+  uint32_t eo[VPT][kDV], co[CPT], cl[CPT], valid = 0;
+  float gam[kFast ? 1 : VPT];
+  {
+    const float* __restrict__ gamma = static_cast<const float*>(P.gamma);
+    const uint32_t dummy = P.seg_mmax * kH2Stride;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const uint32_t n = seg.v0 + tid + k * T;
+      const bool ok = n < seg.v1;
+      valid |= (ok ? 1u : 0u) << k;
+#pragma unroll
+      for (int i = 0; i < kDV; ++i) {
+        const uint32_t e = ok ? P.var_edges[n * kDV + i] - seg.e0 : 0u;
+        eo[k][i] = ok ? (e / kDC) * kH2Stride + (e % kDC) * 4u : dummy + i * 4u;
+      }
+      if constexpr (!kFast) gam[k] = ok ? gamma[n] : 1.0f;
+    }
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+      const uint32_t m = tid + k * T;
+      cl[k] = m < Ms ? m : Ms;
+      co[k] = (m < Ms ? m : P.seg_mmax) * kH2Stride;
+    }
+  }
+  for (uint32_t b = tid; b < kH2Stride; b += T) msgs[P.seg_mmax * kH2Stride + b] = 0;
+
+  uint64_t pair = peer;
+  uint32_t raw_a = 0, raw_b = 0;
+  if (warp == 0 && lane < gspan && pair < npairs) {
+    raw_a = io.syn[(2 * pair) * P.syn_w32 + gw0 + lane];
+    if (2 * pair + 1 < io.nshots) raw_b = io.syn[(2 * pair + 1) * P.syn_w32 + gw0 + lane];
+  }
+  uint32_t ipar = 0;
+  __syncthreads();
+
+  while (pair < npairs) {
+    const uint64_t shot_a = 2 * pair, shot_b = 2 * pair + 1;
+    const bool has_b = shot_b < io.nshots;
+    uint32_t* const par_a = bits + (ipar * 2) * pw;
+    uint32_t* const par_b = bits + (ipar * 2 + 1) * pw;
+    volatile uint32_t* const unsat_a = unsat_ctr + ipar * 2;
+    volatile uint32_t* const unsat_b = unsat_ctr + ipar * 2 + 1;
+    // ---------------- prologue ----------------
+    if (warp == 0) {
+      auto localise = [&](uint32_t raw, uint32_t* par, volatile uint32_t* ctr) {
+        uint32_t nb = __shfl_down_sync(0xffffffffu, raw, 1);
+        if (lane + 1 >= gspan) nb = 0;
+        uint32_t loc = cshift ? __funnelshift_r(raw, nb, cshift) : raw;
+        if (lane >= pws) {
+          loc = 0;
+        } else if (Ms - lane * 32u < 32u) {
+          loc &= (1u << (Ms - lane * 32u)) - 1u;
+        }
+        if (lane < pw) par[lane] = loc;
+        const uint32_t cnt = __reduce_add_sync(0xffffffffu, __popc(loc));
+        if (lane == 0) *ctr = cnt;
+      };
+      localise(raw_a, par_a, unsat_a);
+      localise(raw_b, par_b, unsat_b);
+      if (lane == 0) {
+        const uint64_t t = static_cast<uint64_t>(atomicAdd(&io.sched[2 + s], 1u)) + peers;
+        ticket[ipar] = t < npairs ? static_cast<uint32_t>(t) : kNoShot;
+      }
+    }
+    if (warp == nwarps - 1) {
+      for (int which = 0; which < (has_b ? 2 : 1); ++which) {
+        uint32_t* est_g = io.est + (shot_a + which) * P.est_w32 + vw0;
+        for (uint32_t w = lane; w < vspan; w += 32u) {
+          const uint32_t mask = range_mask(vw0 + w, seg.v0, seg.v1);
+          if (mask == 0xffffffffu) {
+            est_g[w] = 0u;
+          } else {
+            atomicAnd(&est_g[w], ~mask);
+          }
+        }
+      }
+    }
+    if constexpr (!kFast) {
+#pragma unroll
+      for (int k = 0; k < VPT; ++k) {
+        const __half2 init = __half2half2(prior_as_msg<ArithF16>(gam[k]));
+#pragma unroll
+        for (int i = 0; i < kDV; ++i) *reinterpret_cast<__half2*>(msgs + eo[k][i]) = init;
+      }
+    }
+    uint32_t eprev_a = 0, eprev_b = 0;
+    __syncthreads();
+
+    uint32_t synpair[CPT];
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+      const uint32_t ba = (par_a[cl[k] >> 5] >> (cl[k] & 31u)) & 1u;
+      const uint32_t bb = (par_b[cl[k] >> 5] >> (cl[k] & 31u)) & 1u;
+      synpair[k] = (ba << 15) | (bb << 31);
+    }
+    const uint32_t next = ticket[ipar];
+    if (warp == 0 && lane < gspan) {
+      raw_a = raw_b = 0;
+      if (next != kNoShot) {
+        const uint64_t na = 2ull * next;
+        raw_a = io.syn[na * P.syn_w32 + gw0 + lane];
+        if (na + 1 < io.nshots) raw_b = io.syn[(na + 1) * P.syn_w32 + gw0 + lane];
+      }
+    }
+
+    // ---------------- iterations ----------------
+    uint32_t iter = 0, iter_a = 0, iter_b = 0;
+    bool live_a = true, live_b = true, conv_a = false, conv_b = false;
+    uint32_t fin_a = 0, fin_b = 0;  // decisions of each shot at the moment it stopped
+    for (;;) {
+      ++iter;
+      uint32_t eb_a = 0, eb_b = 0;
+      if (kFast && iter == 1u) {
+        const __half2 g2 = __half2half2(__ushort_as_half(P.gamma_hb));
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+          const uint32_t sg = vn3_first_h2(P, msgs, eo[k], par_a, par_b, g2);
+          eb_a |= ((sg >> 15) & 1u) << k;
+          eb_b |= (sg >> 31) << k;
+        }
+        __syncthreads();
+      } else {
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) cn6_h2(P, msgs + co[k], synpair[k]);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+          const __half2 g2 = kFast ? __half2half2(__ushort_as_half(P.gamma_hb))
+                                   : __half2half2(prior_as_msg<ArithF16>(gam[k]));
+          const uint32_t sg = vn3_h2(msgs, eo[k], g2);
+          eb_a |= ((sg >> 15) & 1u) << k;
+          eb_b |= (sg >> 31) << k;
+        }
+      }
+      eb_a &= valid;
+      eb_b &= valid;
+      auto toggle = [&](uint32_t changed, uint32_t* par, volatile uint32_t* ctr) {
+        int32_t delta = 0;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+          if ((changed >> k) & 1u) {
+#pragma unroll
+            for (int i = 0; i < kDV; ++i) {
+              const uint32_t lm = eo[k][i] / kH2Stride;
+              const uint32_t bit = 1u << (lm & 31u);
+              const uint32_t old = atomicXor(&par[lm >> 5], bit);
+              delta += (old & bit) ? -1 : 1;
+            }
+          }
+        }
+        atomicAdd(const_cast<uint32_t*>(ctr), static_cast<uint32_t>(delta));
+      };
+      if (live_a) {
+        const uint32_t ch = eb_a ^ eprev_a;
+        eprev_a = eb_a;
+        if (ch) toggle(ch, par_a, unsat_a);
+      }
+      if (live_b) {
+        const uint32_t ch = eb_b ^ eprev_b;
+        eprev_b = eb_b;
+        if (ch) toggle(ch, par_b, unsat_b);
+      }
+      __syncthreads();
+      const bool last = iter >= P.max_iter;
+      if (live_a) {
+        const bool uns = *unsat_a != 0u;
+        if ((P.early && !uns) || last) {
+          live_a = false;
+          conv_a = !uns;
+          iter_a = iter;
+          fin_a = eprev_a;
+        }
+      }
+      if (live_b) {
+        const bool uns = *unsat_b != 0u;
+        if ((P.early && !uns) || last) {
+          live_b = false;
+          conv_b = !uns;
+          iter_b = iter;
+          fin_b = eprev_b;
+        }
+      }
+      if (!live_a && !live_b) break;
+    }
+
+    // ---------------- epilogue ----------------
+    auto write_out = [&](uint64_t shot, const uint32_t* par, uint32_t fin, bool conv,
+                         uint32_t iters) {
+      if (warp == 0 && io.resid) {
+        const uint32_t hi = lane < pw ? par[lane] : 0u;
+        uint32_t lo = __shfl_up_sync(0xffffffffu, hi, 1);
+        if (lane == 0) lo = 0;
+        const uint32_t out = cshift ? __funnelshift_l(lo, hi, cshift) : hi;
+        if (lane < gspan) {
+          uint32_t* dst = io.resid + shot * P.syn_w32 + gw0 + lane;
+          const uint32_t mask = range_mask(gw0 + lane, seg.c0, seg.c1);
+          if (mask == 0xffffffffu) {
+            *dst = out;
+          } else {
+            atomicAnd(dst, ~mask);
+            atomicOr(dst, out & mask);
+          }
+        }
+      }
+      if (fin) {
+        uint32_t* est_g = io.est + shot * P.est_w32;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+          if ((fin >> k) & 1u) {
+            const uint32_t n = seg.v0 + tid + k * T;
+            atomicOr(&est_g[n >> 5], 1u << (n & 31u));
+          }
+        }
+      }
+      if (tid == 0) {
+        io.conv[shot * nseg + s] = conv ? 1 : 0;
+        io.iters[shot * nseg + s] = iters;
+      }
+    };
+    write_out(shot_a, par_a, fin_a, conv_a, iter_a);
+    if (has_b) write_out(shot_b, par_b, fin_b, conv_b, iter_b);
+    pair = next == kNoShot ? ~0ull : static_cast<uint64_t>(next);
+    ipar ^= 1u;
+  }
+
+  if (tid == 0) {
+    __threadfence();
+    const unsigned int done = atomicAdd(&io.sched[1], 1u);
+    if (done == gridDim.x - 1) {
+      for (uint32_t k = 0; k < 2 + kMaxSegments; ++k) io.sched[k] = 0;
+      __threadfence();
+    }
+  }
+}
+
+}  // namespace qb

@@ -100,10 +100,11 @@ __device__ __forceinline__ void cn6(const DecodeParams& P, const __half* q, __ha
   for (int j = 0; j < 6; ++j) a[j] = static_cast<int32_t>(u[j] & 0x7fffu);
   int32_t m1, m2;
   two_smallest6(a, m1, m2);
-  const uint32_t s1 = __half_as_ushort(__float2half_rn(
-      P.alpha_f * __half2float(__ushort_as_half(static_cast<unsigned short>(m1)))));
-  const uint32_t s2 = __half_as_ushort(__float2half_rn(
-      P.alpha_f * __half2float(__ushort_as_half(static_cast<unsigned short>(m2)))));
+  const __half alpha = __ushort_as_half(P.alpha_h);
+  const uint32_t s1 =
+      __half_as_ushort(__hmul(alpha, __ushort_as_half(static_cast<unsigned short>(m1))));
+  const uint32_t s2 =
+      __half_as_ushort(__hmul(alpha, __ushort_as_half(static_cast<unsigned short>(m2))));
   const uint32_t sx = u[0] ^ u[1] ^ u[2] ^ u[3] ^ u[4] ^ u[5] ^ (syn_bit << 15);
   uint32_t* r2 = reinterpret_cast<uint32_t*>(r + e0);
 #pragma unroll
@@ -193,14 +194,14 @@ __device__ __forceinline__ uint32_t vn3(const DecodeParams& P, float* q, const f
 template <bool kFast>
 __device__ __forceinline__ uint32_t vn3(const DecodeParams& P, __half* q, const __half* r,
                                         const uint32_t (&ea)[3], float gamma) {
-  const float r0 = __half2float(r[ea[0]]);
-  const float r1 = __half2float(r[ea[1]]);
-  const float r2 = __half2float(r[ea[2]]);
-  const float total = (kFast ? P.gamma_f : gamma) + r0 + r1 + r2;
-  q[ea[0]] = __float2half_rn(fminf(fmaxf(total - r0, -kHalfClamp), kHalfClamp));
-  q[ea[1]] = __float2half_rn(fminf(fmaxf(total - r1, -kHalfClamp), kHalfClamp));
-  q[ea[2]] = __float2half_rn(fminf(fmaxf(total - r2, -kHalfClamp), kHalfClamp));
-  return total < 0.0f ? 1u : 0u;
+  const __half r0 = r[ea[0]], r1 = r[ea[1]], r2 = r[ea[2]];
+  const __half g = kFast ? __ushort_as_half(P.gamma_hb)
+                         : __float2half_rn(fminf(fmaxf(gamma, -kHalfClamp), kHalfClamp));
+  const __half total = __hadd(__hadd(__hadd(g, r0), r1), r2);
+  q[ea[0]] = h_clamp(__hsub(total, r0));
+  q[ea[1]] = h_clamp(__hsub(total, r1));
+  q[ea[2]] = h_clamp(__hsub(total, r2));
+  return h_neg(total) ? 1u : 0u;
 }
 
 template <bool kFast, class MsgI>

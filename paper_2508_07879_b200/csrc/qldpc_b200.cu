@@ -22,6 +22,7 @@
 #include "kernel_generic.cuh"
 #include "kernel_regular.cuh"
 #include "kernel_lean.cuh"
+#include "kernel_lean_h2.cuh"
 #include "kernel_noise.cuh"
 #include "kernel_bw.cuh"
 #include "kernel_classify.cuh"
@@ -98,6 +99,7 @@ struct LaunchPlan {
   size_t smem = 0;
   bool items = false;          // work item = (shot, segment): grid-stride over per-segment queues
   bool lean = false;           // ... the instruction-lean single-slot variant
+  bool pair = false;           // ... two shots per thread in half2 lanes (half mode)
 };
 
 struct qb_decoder {
@@ -139,7 +141,7 @@ struct qb_decoder {
 
   // options
   int64_t opt_kernel = 0, opt_latency_io = 0, opt_latency_shape = 0, opt_group_threads = 0,
-          opt_batch_ctas = 0, opt_batch_npt = 0, opt_latency_npt = 0, opt_batch_shape = 0;
+          opt_batch_ctas = 0, opt_batch_npt = 0, opt_latency_npt = 0, opt_batch_shape = 0, opt_batch_pair = 1;
   // lean single-shot cluster kernel (kernel_lean.cuh) and its persistent doorbell mode
   LatKernelFn lat_lean_kernel = nullptr;
   unsigned lat_lean_block = 0;
@@ -372,6 +374,21 @@ KernelFn lean_kernel(int arith, int variant, bool fast) {
   }
 }
 
+template <bool kFast>
+KernelFn lean_h2_kernel_tf(int variant) {
+  switch (variant) {
+    case 1: return decode_lean_h2_kernel<1, 2, kFast, 1024, 1>;
+    case 2: return decode_lean_h2_kernel<1, 2, kFast, 448, 3>;
+    case 3: return decode_lean_h2_kernel<2, 4, kFast, 256, 3>;
+    case 4: return decode_lean_h2_kernel<3, 5, kFast, 192, 5>;
+    case 5: return decode_lean_h2_kernel<4, 8, kFast, 128, 6>;
+    case 7: return decode_lean_h2_kernel<3, 5, kFast, 160, 5>;
+    case 8: return decode_lean_h2_kernel<3, 5, kFast, 160, 4>;
+    case 9: return decode_lean_h2_kernel<2, 4, kFast, 224, 4>;
+    default: return decode_lean_h2_kernel<2, 4, kFast, 512, 2>;
+  }
+}
+
 template <class A, bool kFast>
 LatKernelFn lean_latency_kernel_tf(int npt) {
   return npt == 1 ? decode_lean_latency_kernel<A, 1, 2, kFast>
@@ -412,7 +429,7 @@ uint32_t regular_group_threads(const DecodeParams& P, uint32_t cpt, uint32_t vpt
 void finish_plan(qb_decoder* h, LaunchPlan& pl) {
   pl.block = pl.cluster ? pl.group_threads : pl.ngroups * pl.group_threads;
   if (pl.items) pl.block = pl.group_threads;
-  pl.smem = pl.lean ? h->smem_lean : h->smem_bytes;
+  pl.smem = pl.pair ? lean_h2_smem_bytes(h->P.seg_mmax) : pl.lean ? h->smem_lean : h->smem_bytes;
   CUDA_TRY(cudaFuncSetAttribute(pl.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(pl.smem)));
   if (pl.cluster) {
@@ -502,8 +519,12 @@ void make_plans(qb_decoder* h) {
   const bool fast = h->fast_ok && h->opt_fast != 0;
   if (h->opt_batch_shape != 1 && P.seg_mmax <= 960) {
     // work item = (shot, segment): lean item kernel; first variant whose CTA fits
-    const int order_auto[] = {4, 3, 5, 2, 6, 1};
-    for (int idx = 0; idx < kNumLeanVariants && !bat_done; ++idx) {
+    // (measured on [[784,24,24]]: the packed fp16 kernel prefers the spill-free
+    // 96-register build at four CTAs per SM)
+    const bool pair = h->arith == QB_ARITH_HALF && h->opt_batch_pair != 0;
+    const int order_f32[] = {4, 3, 5, 2, 6, 1}, order_h2[] = {8, 3, 5, 2, 6, 1};
+    const int* order_auto = pair ? order_h2 : order_f32;
+    for (int idx = 0; idx < 6 && !bat_done; ++idx) {
       const int variant = h->opt_batch_npt ? static_cast<int>(h->opt_batch_npt) : order_auto[idx];
       const LeanVariant& lv = kLeanVariants[variant - 1];
       const uint32_t T = regular_group_threads(P, lv.cpt, lv.vpt);
@@ -513,8 +534,11 @@ void make_plans(qb_decoder* h) {
         pl.items = true;
         pl.lean = true;
         pl.npt = variant;
-        pl.kernel = lean_kernel(h->arith, variant, fast);
-        pl.name = "decode_lean_kernel";
+        pl.pair = pair;
+        pl.kernel = !pl.pair ? lean_kernel(h->arith, variant, fast)
+                    : fast   ? lean_h2_kernel_tf<true>(variant)
+                             : lean_h2_kernel_tf<false>(variant);
+        pl.name = pl.pair ? "decode_lean_h2_kernel" : "decode_lean_kernel";
         pl.ngroups = 1;
         pl.group_threads = T;
         finish_plan(h, pl);
@@ -577,7 +601,8 @@ unsigned batch_grid(qb_decoder* h, uint64_t shots) {
   const uint64_t resident = static_cast<uint64_t>(per_sm) * h->sm_count;
   if (h->bat.items) {  // equal numbers of CTAs per segment
     const uint64_t nseg = h->P.nseg;
-    const uint64_t per_seg = std::max<uint64_t>(1, std::min<uint64_t>(resident / nseg, shots));
+    const uint64_t items = h->bat.pair ? (shots + 1) / 2 : shots;
+    const uint64_t per_seg = std::max<uint64_t>(1, std::min<uint64_t>(resident / nseg, items));
     return static_cast<unsigned>(per_seg * nseg);
   }
   return static_cast<unsigned>(std::min<uint64_t>(shots, resident));
@@ -1031,6 +1056,8 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
     P.alpha = config->alpha;
     P.alpha_f = static_cast<float>(config->alpha);
     P.deg1_f = static_cast<float>(config->alpha * 64.0);
+    P.alpha_h = __half_as_ushort(__float2half_rn(static_cast<float>(config->alpha)));
+    P.deg1_h = __half_as_ushort(__float2half_rn(static_cast<float>(config->alpha * 64.0)));
     P.clamp_f = static_cast<float>(1e30);
     P.alpha_fx = alpha_fx;
     P.kmax = kmax;
@@ -1111,11 +1138,12 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
         P.it1_neg = g0 < 0.0f ? 1u : 0u;
         P.it1_d = static_cast<double>(
             static_cast<float>(config->alpha * static_cast<double>(std::fabs(g0))));
-        // fp16: q starts as half(clamp(gamma)); the check scales its magnitude in fp32
+        // fp16 mode: every quantity is an fp16 value, products are single fp16 multiplies
         const float gclamp = std::fmin(std::fmax(g0, -kHalfClamp), kHalfClamp);
-        const float qh = __half2float(__float2half_rn(gclamp));
-        P.it1_f = __half2float(__float2half_rn(static_cast<float>(config->alpha) * std::fabs(qh)));
-        P.gamma_h = g0;
+        const __half gh = __float2half_rn(gclamp);
+        const __half ah = __float2half_rn(static_cast<float>(config->alpha));
+        P.gamma_hb = __half_as_ushort(gh);
+        P.it1_h = __half_as_ushort(__hmul(ah, __habs(gh)));
       } else {
         const int32_t g0 = gamma_i[0];
         P.it1_neg = g0 < 0 ? 1u : 0u;
@@ -1198,6 +1226,10 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
         if (value < 0 || value > 2) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_SHAPE: 0, 1 or 2");
         h->opt_batch_shape = value;
         break;
+      case QB_OPT_HALF_PAIRS:
+        if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_HALF_PAIRS: 0 or 1");
+        h->opt_batch_pair = value;
+        break;
       case QB_OPT_DOORBELL_IDLE_MS:
         if (value < 1 || value > 60000) fail(QB_INVALID_ARGUMENT, "QB_OPT_DOORBELL_IDLE_MS: 1..60000");
         stop_doorbell(h);
@@ -1256,6 +1288,7 @@ int64_t qb_get_option(const qb_decoder* h, int option) {
     case QB_OPT_BATCH_SHAPE: return h->bat.lean ? 2 : 1;
     case QB_OPT_INFO_FAST_ELIGIBLE: return h->fast_ok ? 1 : 0;
     case QB_OPT_DOORBELL_IDLE_MS: return h->opt_idle_ms;
+    case QB_OPT_HALF_PAIRS: return h->bat.pair ? 1 : 0;
     case QB_OPT_INFO_LATENCY_LEAN: return h->lat_lean_kernel ? 1 : 0;
     case QB_OPT_BATCH_CTAS_PER_SM: return h->opt_batch_ctas;
     default: return -1;

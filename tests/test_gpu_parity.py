@@ -367,3 +367,47 @@ def test_half_mode_tracks_float_decisions():
     agree = (e32 == e16).all(axis=1).mean()
     assert agree > 0.98, agree
     assert abs(c32.mean() - c16.mean()) < 0.01
+
+
+OPT_HALF_PAIRS = 10
+
+
+@pytest.mark.parametrize("name,shots,p", [("bb72", 257, 0.03), ("bb144", 1001, 0.02),
+                                          ("bb784", 600, 0.01)])
+def test_half_mode_every_kernel_gives_identical_results(name, shots, p):
+    """Half mode is fp16 arithmetic in every kernel, so the packed two-shots-per-
+    thread batch kernel, the one-shot-per-thread batch variants, the generic CSR
+    kernel and the single-shot cluster kernel must agree bit for bit (odd shot
+    counts exercise the half-empty last pair)."""
+    code = codes.make_code(name)
+    rng = np.random.default_rng(17)
+    _, _, syn = error_syndromes(code, rng, shots, p)
+    g = code.combined_graph
+    priors = (0.5 + rng.random(g.num_vars) * 4.0).tolist()
+    for cfg in (DecoderConfig(max_iterations=30, arithmetic="half"),
+                DecoderConfig(max_iterations=7, early_termination=False, arithmetic="half"),
+                DecoderConfig(max_iterations=30, arithmetic="half", priors=priors)):
+        with Decoder(code, cfg) as dec:
+            assert dec.get_option(OPT_HALF_PAIRS) == 1
+            want = dec.decode_batch_segments(syn)
+            hs = code.combined.mat_vec(gf2.unpack_bits(want[0], g.num_vars))
+            assert np.array_equal(gf2.unpack_bits(want[1], g.num_checks),
+                                  hs ^ gf2.unpack_bits(syn, g.num_checks))
+            for variant in (1, 2, 3, 4, 5, 6, 7, 9):
+                try:
+                    dec.set_option(OPT_BATCH_NPT, variant)
+                except ValueError:
+                    continue  # CTA shape does not fit this code
+                got = dec.decode_batch_segments(syn)
+                assert all(np.array_equal(a, b) for a, b in zip(got, want)), variant
+            dec.set_option(OPT_BATCH_NPT, 0)
+            dec.set_option(OPT_HALF_PAIRS, 0)
+            assert dec.get_option(OPT_HALF_PAIRS) == 0
+            got = dec.decode_batch_segments(syn)
+            assert all(np.array_equal(a, b) for a, b in zip(got, want)), "unpaired"
+            for k in range(0, shots, max(1, shots // 40)):
+                one = dec.decode_segments(syn[k])
+                assert all(np.array_equal(a, b[k]) for a, b in zip(one, want)), k
+            dec.set_option(OPT_KERNEL, 1)
+            got = dec.decode_batch_segments(syn)
+            assert all(np.array_equal(a, b) for a, b in zip(got, want)), "generic"

@@ -14,6 +14,7 @@ ap.add_argument("--ctas", default="0")
 ap.add_argument("--iters", default="50:1,10:0")
 ap.add_argument("--kernel", type=int, default=0)
 ap.add_argument("--shapes", default="2")
+ap.add_argument("--pairs", type=int, default=1)
 args = ap.parse_args()
 code = codes.make_code(args.code)
 g = code.combined_graph
@@ -32,6 +33,7 @@ for spec in args.iters.split(","):
         with Decoder(code, cfg) as dec:
             dec.generate_syndromes(1, args.p, shots, d_syn.data_ptr(), None, stream=stream)
             if args.kernel: dec.set_option(0, args.kernel)
+            dec.set_option(10, args.pairs)
             for shape, npt in [(int(sh), int(x)) for sh in args.shapes.split(",") for x in args.npts.split(",")]:
                 for ctas in [int(x) for x in args.ctas.split(",")]:
                     dec.set_option(8, shape); dec.set_option(5, npt); dec.set_option(4, ctas)
