@@ -127,7 +127,10 @@ typedef enum {
   QB_OPT_INFO_LATENCY_CLUSTER = 103,
   QB_OPT_INFO_BATCH_REGULAR = 104,
   QB_OPT_INFO_FAST_ELIGIBLE = 105,
-  QB_OPT_INFO_LATENCY_LEAN = 106
+  QB_OPT_INFO_LATENCY_LEAN = 106,
+  /* 100 * DC + DV of the degree-padded batch kernel in use (irregular graphs whose
+   * degrees fit an instantiated bound), 0 when another kernel serves batches. */
+  QB_OPT_INFO_BATCH_ELL = 107
 } qb_option;
 
 /* Builds a decoder: validates like Decoder::Decoder (decoder.cpp:373-404,

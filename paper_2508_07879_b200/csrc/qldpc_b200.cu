@@ -23,6 +23,7 @@
 #include "kernel_regular.cuh"
 #include "kernel_lean.cuh"
 #include "kernel_lean_h2.cuh"
+#include "kernel_ell.cuh"
 #include "kernel_noise.cuh"
 #include "kernel_bw.cuh"
 #include "kernel_classify.cuh"
@@ -100,6 +101,7 @@ struct LaunchPlan {
   bool items = false;          // work item = (shot, segment): grid-stride over per-segment queues
   bool lean = false;           // ... the instruction-lean single-slot variant
   bool pair = false;           // ... two shots per thread in half2 lanes (half mode)
+  int ell = 0;                 // degree-padded kernel: 100 * DC + DV (0 = not that kernel)
 };
 
 struct qb_decoder {
@@ -155,6 +157,7 @@ struct qb_decoder {
   bool db_running = false;
   int64_t opt_idle_ms = 200;
   bool regular63 = false;  // every check degree 6, every variable degree 3
+  uint32_t max_dc = 0, max_dv = 0;  // largest check / variable degree of the graph
   bool fast_ok = false;    // uniform prior (and, for fp32, provably clamp-free)
   int64_t opt_fast = 1;
   LaunchPlan lat, bat;
@@ -412,6 +415,39 @@ LatKernelFn lean_latency_kernel(int arith, int npt, bool fast) {
   }
 }
 
+// Degree-padded (ELL) batch kernels for irregular graphs: the degree bounds and
+// nodes-per-thread shapes that are instantiated (kernel_ell.cuh).  The loader
+// takes the first entry whose bounds cover the graph and whose CTA fits.
+struct EllVariant {
+  int dc, dv, cpt, vpt, maxt;
+};
+constexpr EllVariant kEllVariants[] = {
+    {4, 2, 1, 2, 1024},   // e.g. the toy 3x6 fixture, repetition / surface-like checks
+    {7, 3, 3, 8, 192},    // [H | I] extension of a (6,3)-regular code (phenomenological noise)
+    {8, 4, 2, 4, 512},
+    {12, 6, 1, 2, 1024},
+};
+constexpr int kNumEllVariants = sizeof(kEllVariants) / sizeof(kEllVariants[0]);
+
+template <class A>
+KernelFn ell_kernel_t(int idx) {
+  switch (idx) {
+    case 0: return decode_ell_kernel<A, 4, 2, 1, 2, 1024, 1>;
+    case 1: return decode_ell_kernel<A, 7, 3, 3, 8, 192, 4>;
+    case 2: return decode_ell_kernel<A, 8, 4, 2, 4, 512, 2>;
+    default: return decode_ell_kernel<A, 12, 6, 1, 2, 1024, 1>;
+  }
+}
+
+KernelFn ell_kernel(int arith, int idx) {
+  switch (arith) {
+    case QB_ARITH_FLOAT: return ell_kernel_t<ArithF32>(idx);
+    case QB_ARITH_INT8: return ell_kernel_t<ArithI8>(idx);
+    case QB_ARITH_INT16: return ell_kernel_t<ArithI16>(idx);
+    default: return ell_kernel_t<ArithF16>(idx);
+  }
+}
+
 uint32_t round_up32(uint32_t x) { return (x + 31u) & ~31u; }
 
 // Threads per segment group so that T*cpt covers the checks and T*vpt the
@@ -429,7 +465,11 @@ uint32_t regular_group_threads(const DecodeParams& P, uint32_t cpt, uint32_t vpt
 void finish_plan(qb_decoder* h, LaunchPlan& pl) {
   pl.block = pl.cluster ? pl.group_threads : pl.ngroups * pl.group_threads;
   if (pl.items) pl.block = pl.group_threads;
-  pl.smem = pl.pair ? lean_h2_smem_bytes(h->P.seg_mmax) : pl.lean ? h->smem_lean : h->smem_bytes;
+  pl.smem = pl.ell    ? ell_smem_bytes(h->P.seg_mmax, static_cast<uint32_t>(msg_bytes_of(h->arith)),
+                                       static_cast<uint32_t>(pl.ell / 100))
+            : pl.pair ? lean_h2_smem_bytes(h->P.seg_mmax)
+            : pl.lean ? h->smem_lean
+                      : h->smem_bytes;
   CUDA_TRY(cudaFuncSetAttribute(pl.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(pl.smem)));
   if (pl.cluster) {
@@ -465,6 +505,29 @@ void make_plans(qb_decoder* h) {
   }
   if (!use_regular) {
     h->lat = h->bat = generic_plan(h);
+    // batch: degree-padded item kernel when the degrees fit an instantiated bound
+    if (h->opt_kernel != 1 && h->opt_batch_shape != 1 && P.seg_mmax <= 960 && P.nseg <= kMaxSegments) {
+      for (int idx = 0; idx < kNumEllVariants; ++idx) {
+        const EllVariant& ev = kEllVariants[idx];
+        if (h->max_dc > static_cast<uint32_t>(ev.dc) || h->max_dv > static_cast<uint32_t>(ev.dv)) continue;
+        const uint32_t T = regular_group_threads(P, ev.cpt, ev.vpt);
+        if (T > static_cast<uint32_t>(ev.maxt)) continue;
+        const size_t smem = ell_smem_bytes(P.seg_mmax, static_cast<uint32_t>(msg_bytes_of(h->arith)),
+                                           static_cast<uint32_t>(ev.dc));
+        if (smem > static_cast<size_t>(h->max_smem_optin)) continue;
+        LaunchPlan pl{};
+        pl.items = true;
+        pl.lean = true;
+        pl.ell = 100 * ev.dc + ev.dv;
+        pl.kernel = ell_kernel(h->arith, idx);
+        pl.name = "decode_ell_kernel";
+        pl.ngroups = 1;
+        pl.group_threads = T;
+        finish_plan(h, pl);
+        h->bat = pl;
+        break;
+      }
+    }
     return;
   }
   auto regular_plan = [&](int npt, bool cluster) {
@@ -1160,6 +1223,12 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
         reg = graph->var_offsets[n + 1] - graph->var_offsets[n] == 3;
       }
       h->regular63 = reg;
+      for (uint32_t m = 0; m < M; ++m) {
+        h->max_dc = std::max(h->max_dc, graph->check_offsets[m + 1] - graph->check_offsets[m]);
+      }
+      for (uint32_t n = 0; n < N; ++n) {
+        h->max_dv = std::max(h->max_dv, graph->var_offsets[n + 1] - graph->var_offsets[n]);
+      }
     }
     make_plans(h);
 
@@ -1290,6 +1359,7 @@ int64_t qb_get_option(const qb_decoder* h, int option) {
     case QB_OPT_DOORBELL_IDLE_MS: return h->opt_idle_ms;
     case QB_OPT_HALF_PAIRS: return h->bat.pair ? 1 : 0;
     case QB_OPT_INFO_LATENCY_LEAN: return h->lat_lean_kernel ? 1 : 0;
+    case QB_OPT_INFO_BATCH_ELL: return h->bat.ell;
     case QB_OPT_BATCH_CTAS_PER_SM: return h->opt_batch_ctas;
     default: return -1;
   }
