@@ -116,8 +116,10 @@ typedef enum {
    * drawn from per-segment queues (the lean item kernel; the auto choice). */
   QB_OPT_BATCH_SHAPE = 8,
   QB_OPT_DOORBELL_IDLE_MS = 9,
-  /* Half mode, batch calls: 1 (default) = decode two shots per thread in the two
-   * lanes of packed fp16 instructions; 0 = one shot per thread.  Results are
+  /* Half and int8 modes, batch calls on (6,3)-regular codes: 1 (default) = decode
+   * two shots per thread in the two lanes of packed fp16 instructions (int8
+   * values are exact fp16 integers; used only when the loader has verified the
+   * Q16 scaling for all 128 magnitudes); 0 = one shot per thread.  Results are
    * identical either way. */
   QB_OPT_HALF_PAIRS = 10,
   /* Read-only (qb_get_option): the launch plans actually in use. */

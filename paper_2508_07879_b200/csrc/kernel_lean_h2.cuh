@@ -13,6 +13,20 @@
 // The two shots of a pair stop independently: a finished lane is frozen (its
 // parity bitmap, counter and decisions are no longer touched) while the other
 // iterates on; the pair is released when both are done.
+//
+// kI8 = true runs the reference's INT8 mode (decoder.cpp:260-283, bit-exact) on
+// the same packed instructions: every int8-mode quantity is an integer of
+// magnitude <= 4 * 127, which fp16 represents exactly, so the sums, the
+// saturation at +-127 (HMNMX2) and the comparisons are exact in fp16 arithmetic.
+// The Q16 scaling (mag * alpha_fx + 32768) >> 16 becomes ONE fused multiply-add
+// with the magic constant 1536 (= 1.5 * 2^10, where fp16 has unit spacing):
+// fma(mag, c, 1536) - 1536 = round-to-nearest-even(mag * c), and the loader only
+// selects this kernel after checking, for all 128 magnitudes, that it equals the
+// reference's integer formula for the fp16 constant c it picked (P.alpha_h).
+// Messages are stored as fp16 integers; a zero magnitude may carry a sign bit
+// (-0), which is harmless: gamma is never 0 (decoder.cpp:115-120), so no sum
+// can evaluate to -0 and a stored q is never -0 (its sign bit is the reference's
+// `v < 0`).
 #pragma once
 
 #include "common.cuh"
@@ -42,7 +56,29 @@ __device__ __forceinline__ void two_smallest6_h2(const __half2 (&a)[6], __half2&
   m2 = __hmin2(med, __hmin2(__hmin2(h0, h1), h2));
 }
 
+template <bool kI8>
+__device__ __forceinline__ __half2 h2_clamp_t(__half2 x) {
+  if constexpr (kI8) {
+    const __half2 c = __half2half2(__ushort_as_half(0x57f0));  // 127
+    return __hmax2(__hmin2(x, c), __hneg2(c));
+  } else {
+    return h2_clamp(x);
+  }
+}
+
+// alpha * m: one fp16 multiply (half mode) or the exact Q16 rounding (int8 mode)
+template <bool kI8>
+__device__ __forceinline__ __half2 h2_scale(__half2 alpha, __half2 m) {
+  if constexpr (kI8) {
+    const __half2 magic = __half2half2(__ushort_as_half(0x6600));  // 1536
+    return __hsub2(__hfma2(m, alpha, magic), magic);
+  } else {
+    return __hmul2(alpha, m);
+  }
+}
+
 // syn_pair: bit 15 = syndrome bit of the low-half shot, bit 31 = of the high-half shot
+template <bool kI8>
 __device__ __forceinline__ void cn6_h2(const DecodeParams& P, unsigned char* blk, uint32_t syn_pair) {
   const uint2* qp = reinterpret_cast<const uint2*>(blk);
   uint32_t u[6];
@@ -58,7 +94,7 @@ __device__ __forceinline__ void cn6_h2(const DecodeParams& P, unsigned char* blk
   __half2 m1, m2;
   two_smallest6_h2(a, m1, m2);
   const __half2 alpha = __half2half2(__ushort_as_half(P.alpha_h));
-  const uint32_t s1 = h22u(__hmul2(alpha, m1)), s2 = h22u(__hmul2(alpha, m2));
+  const uint32_t s1 = h22u(h2_scale<kI8>(alpha, m1)), s2 = h22u(h2_scale<kI8>(alpha, m2));
   const uint32_t sx = u[0] ^ u[1] ^ u[2] ^ u[3] ^ u[4] ^ u[5] ^ syn_pair;
   uint32_t o[6];
 #pragma unroll
@@ -72,18 +108,20 @@ __device__ __forceinline__ void cn6_h2(const DecodeParams& P, unsigned char* blk
 }
 
 // returns the sign bits of the two posteriors (bit 15 / bit 31)
+template <bool kI8>
 __device__ __forceinline__ uint32_t vn3_h2(unsigned char* base, const uint32_t (&eo)[3],
                                            __half2 gamma2) {
   const __half2 r0 = *reinterpret_cast<const __half2*>(base + eo[0] + kH2ROff);
   const __half2 r1 = *reinterpret_cast<const __half2*>(base + eo[1] + kH2ROff);
   const __half2 r2 = *reinterpret_cast<const __half2*>(base + eo[2] + kH2ROff);
   const __half2 total = __hadd2(__hadd2(__hadd2(gamma2, r0), r1), r2);
-  *reinterpret_cast<__half2*>(base + eo[0]) = h2_clamp(__hsub2(total, r0));
-  *reinterpret_cast<__half2*>(base + eo[1]) = h2_clamp(__hsub2(total, r1));
-  *reinterpret_cast<__half2*>(base + eo[2]) = h2_clamp(__hsub2(total, r2));
+  *reinterpret_cast<__half2*>(base + eo[0]) = h2_clamp_t<kI8>(__hsub2(total, r0));
+  *reinterpret_cast<__half2*>(base + eo[1]) = h2_clamp_t<kI8>(__hsub2(total, r1));
+  *reinterpret_cast<__half2*>(base + eo[2]) = h2_clamp_t<kI8>(__hsub2(total, r2));
   return h22u(total) & 0x80008000u;
 }
 
+template <bool kI8>
 __device__ __forceinline__ uint32_t vn3_first_h2(const DecodeParams& P, unsigned char* base,
                                                  const uint32_t (&eo)[3], const uint32_t* par_a,
                                                  const uint32_t* par_b, __half2 gamma2) {
@@ -98,12 +136,23 @@ __device__ __forceinline__ uint32_t vn3_first_h2(const DecodeParams& P, unsigned
   const __half2 total = __hadd2(__hadd2(__hadd2(gamma2, r[0]), r[1]), r[2]);
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    *reinterpret_cast<__half2*>(base + eo[i]) = h2_clamp(__hsub2(total, r[i]));
+    *reinterpret_cast<__half2*>(base + eo[i]) = h2_clamp_t<kI8>(__hsub2(total, r[i]));
   }
   return h22u(total) & 0x80008000u;
 }
 
-template <int CPT, int VPT, bool kFast, int MAXT, int MINB>
+// prior of one variable as a stored message: clamped fp16 (half mode) or the exact
+// fp16 image of the quantised int prior (int8 mode)
+template <bool kI8>
+__device__ __forceinline__ __half h2_prior(float g) {
+  if constexpr (kI8) {
+    return __float2half_rn(g);  // |g| <= 127, an integer: exact
+  } else {
+    return prior_as_msg<ArithF16>(g);
+  }
+}
+
+template <int CPT, int VPT, bool kFast, int MAXT, int MINB, bool kI8 = false>
 __global__ void __launch_bounds__(MAXT, MINB)
 decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_constant__ ShotIO io) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -132,6 +181,7 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
   float gam[kFast ? 1 : VPT];
   {
     const float* __restrict__ gamma = static_cast<const float*>(P.gamma);
+    const int32_t* __restrict__ gamma_i = static_cast<const int32_t*>(P.gamma);  // int8 mode
     const uint32_t dummy = P.seg_mmax * kH2Stride;
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
@@ -143,7 +193,13 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
         const uint32_t e = ok ? P.var_edges[n * kDV + i] - seg.e0 : 0u;
         eo[k][i] = ok ? (e / kDC) * kH2Stride + (e % kDC) * 4u : dummy + i * 4u;
       }
-      if constexpr (!kFast) gam[k] = ok ? gamma[n] : 1.0f;
+      if constexpr (!kFast) {
+        if constexpr (kI8) {
+          gam[k] = ok ? static_cast<float>(gamma_i[n]) : 1.0f;
+        } else {
+          gam[k] = ok ? gamma[n] : 1.0f;
+        }
+      }
     }
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
@@ -208,7 +264,7 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
     if constexpr (!kFast) {
 #pragma unroll
       for (int k = 0; k < VPT; ++k) {
-        const __half2 init = __half2half2(prior_as_msg<ArithF16>(gam[k]));
+        const __half2 init = __half2half2(h2_prior<kI8>(gam[k]));
 #pragma unroll
         for (int i = 0; i < kDV; ++i) *reinterpret_cast<__half2*>(msgs + eo[k][i]) = init;
       }
@@ -244,20 +300,20 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
         const __half2 g2 = __half2half2(__ushort_as_half(P.gamma_hb));
 #pragma unroll
         for (int k = 0; k < VPT; ++k) {
-          const uint32_t sg = vn3_first_h2(P, msgs, eo[k], par_a, par_b, g2);
+          const uint32_t sg = vn3_first_h2<kI8>(P, msgs, eo[k], par_a, par_b, g2);
           eb_a |= ((sg >> 15) & 1u) << k;
           eb_b |= (sg >> 31) << k;
         }
         __syncthreads();
       } else {
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) cn6_h2(P, msgs + co[k], synpair[k]);
+        for (int k = 0; k < CPT; ++k) cn6_h2<kI8>(P, msgs + co[k], synpair[k]);
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < VPT; ++k) {
           const __half2 g2 = kFast ? __half2half2(__ushort_as_half(P.gamma_hb))
-                                   : __half2half2(prior_as_msg<ArithF16>(gam[k]));
-          const uint32_t sg = vn3_h2(msgs, eo[k], g2);
+                                   : __half2half2(h2_prior<kI8>(gam[k]));
+          const uint32_t sg = vn3_h2<kI8>(msgs, eo[k], g2);
           eb_a |= ((sg >> 15) & 1u) << k;
           eb_b |= (sg >> 31) << k;
         }

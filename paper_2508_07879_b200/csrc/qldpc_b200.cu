@@ -158,6 +158,7 @@ struct qb_decoder {
   int64_t opt_idle_ms = 200;
   bool regular63 = false;  // every check degree 6, every variable degree 3
   uint32_t max_dc = 0, max_dv = 0;  // largest check / variable degree of the graph
+  bool i8_pair_ok = false;  // int8 mode: the Q16 scaling has an exact fp16 form (kernel_lean_h2.cuh)
   bool fast_ok = false;    // uniform prior (and, for fp32, provably clamp-free)
   int64_t opt_fast = 1;
   LaunchPlan lat, bat;
@@ -377,6 +378,18 @@ KernelFn lean_kernel(int arith, int variant, bool fast) {
   }
 }
 
+// int8 mode on the packed fp16 kernel (kernel_lean_h2.cuh): the shapes the loader may pick
+template <bool kFast>
+KernelFn lean_h2_i8_kernel_tf(int variant) {
+  switch (variant) {
+    case 1: return decode_lean_h2_kernel<1, 2, kFast, 1024, 1, true>;
+    case 3: return decode_lean_h2_kernel<2, 4, kFast, 256, 3, true>;
+    case 6: return decode_lean_h2_kernel<2, 4, kFast, 512, 2, true>;
+    case 8: return decode_lean_h2_kernel<3, 5, kFast, 160, 4, true>;
+    default: return nullptr;
+  }
+}
+
 template <bool kFast>
 KernelFn lean_h2_kernel_tf(int variant) {
   switch (variant) {
@@ -584,14 +597,21 @@ void make_plans(qb_decoder* h) {
     // work item = (shot, segment): lean item kernel; first variant whose CTA fits
     // (measured on [[784,24,24]]: the packed fp16 kernel prefers the spill-free
     // 96-register build at four CTAs per SM)
-    const bool pair = h->arith == QB_ARITH_HALF && h->opt_batch_pair != 0;
+    const bool i8 = h->arith == QB_ARITH_INT8;
+    const bool pair_wanted = (h->arith == QB_ARITH_HALF || (i8 && h->i8_pair_ok)) && h->opt_batch_pair != 0;
     const int order_f32[] = {4, 3, 5, 2, 6, 1}, order_h2[] = {8, 3, 5, 2, 6, 1};
-    const int* order_auto = pair ? order_h2 : order_f32;
+    const int* order_auto = pair_wanted ? order_h2 : order_f32;
     for (int idx = 0; idx < 6 && !bat_done; ++idx) {
       const int variant = h->opt_batch_npt ? static_cast<int>(h->opt_batch_npt) : order_auto[idx];
       const LeanVariant& lv = kLeanVariants[variant - 1];
       const uint32_t T = regular_group_threads(P, lv.cpt, lv.vpt);
       if (T <= static_cast<uint32_t>(lv.maxt)) {
+        KernelFn i8_pair = nullptr;
+        if (i8 && pair_wanted) {
+          i8_pair = fast ? lean_h2_i8_kernel_tf<true>(variant) : lean_h2_i8_kernel_tf<false>(variant);
+          if (!i8_pair && !h->opt_batch_npt) continue;  // shape not built for int8 pairs: next one
+        }
+        const bool pair = pair_wanted && (!i8 || i8_pair != nullptr);
         LaunchPlan pl{};
         pl.regular = true;
         pl.items = true;
@@ -599,6 +619,7 @@ void make_plans(qb_decoder* h) {
         pl.npt = variant;
         pl.pair = pair;
         pl.kernel = !pl.pair ? lean_kernel(h->arith, variant, fast)
+                    : i8     ? i8_pair
                     : fast   ? lean_h2_kernel_tf<true>(variant)
                              : lean_h2_kernel_tf<false>(variant);
         pl.name = pl.pair ? "decode_lean_h2_kernel" : "decode_lean_kernel";
@@ -1212,6 +1233,28 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
         P.it1_neg = g0 < 0 ? 1u : 0u;
         P.it1_i = static_cast<int32_t>(
             (static_cast<int64_t>(g0 < 0 ? -g0 : g0) * alpha_fx + 32768) >> 16);
+        if (arith == QB_ARITH_INT8) {
+          // int8 on the packed fp16 kernel: find an fp16 constant c with
+          // round-to-nearest-even(mag * c) == (mag * alpha_fx + 32768) >> 16 for every
+          // magnitude 0..127 (mag * c is exact in double; ties included in the check)
+          const __half c0 = __float2half_rn(static_cast<float>(alpha_fx) / 65536.0f);
+          for (int d : {0, -1, 1, -2, 2}) {
+            const unsigned short bits = static_cast<unsigned short>(__half_as_ushort(c0) + d);
+            const double c = static_cast<double>(__half2float(__ushort_as_half(bits)));
+            bool ok = c > 0.0 && c <= 1.0;
+            for (int mag = 0; mag <= 127 && ok; ++mag) {
+              const int64_t want = (static_cast<int64_t>(mag) * alpha_fx + 32768) >> 16;
+              ok = static_cast<int64_t>(std::nearbyint(mag * c)) == want;
+            }
+            if (ok) {
+              h->i8_pair_ok = true;
+              P.alpha_h = bits;
+              P.gamma_hb = __half_as_ushort(__float2half_rn(static_cast<float>(g0)));
+              P.it1_h = __half_as_ushort(__float2half_rn(static_cast<float>(P.it1_i)));
+              break;
+            }
+          }
+        }
       }
     }
     {

@@ -411,3 +411,38 @@ def test_half_mode_every_kernel_gives_identical_results(name, shots, p):
             dec.set_option(OPT_KERNEL, 1)
             got = dec.decode_batch_segments(syn)
             assert all(np.array_equal(a, b) for a, b in zip(got, want)), "generic"
+
+
+@pytest.mark.parametrize("name,shots,p", [("bb72", 257, 0.03), ("bb144", 1001, 0.02),
+                                          ("bb784", 601, 0.01), ("bb784", 300, 0.04)])
+def test_int8_on_the_packed_fp16_kernel_is_bit_exact(oracle, name, shots, p):
+    """int8 batches run two shots per thread on packed fp16 instructions (int8
+    quantities are exact fp16 integers, Q16 scaling as one fused multiply-add,
+    kernel_lean_h2.cuh).  Must equal the integer oracle (decoder.cpp:260-283) bit
+    for bit - uniform and per-variable priors incl. saturating and negative ones,
+    several alphas / scales, odd shot counts - and the one-shot-per-thread kernel."""
+    code = codes.make_code(name)
+    rng = np.random.default_rng(23)
+    _, _, syn = error_syndromes(code, rng, shots, p)
+    g = code.combined_graph
+    priors = (rng.uniform(0.2, 20.0, g.num_vars) * rng.choice([-1.0, 1.0], g.num_vars, p=[0.05, 0.95]))
+    cfgs = [DecoderConfig(max_iterations=30, arithmetic="int8"),
+            DecoderConfig(max_iterations=7, early_termination=False, arithmetic="int8"),
+            DecoderConfig(max_iterations=30, arithmetic="int8", priors=priors.tolist()),
+            DecoderConfig(max_iterations=20, arithmetic="int8", alpha=0.625, quant_scale=20.0),
+            DecoderConfig(max_iterations=20, arithmetic="int8", alpha=1.0, quant_scale=100.0),
+            DecoderConfig(max_iterations=20, arithmetic="int8", alpha=0.3, quant_scale=3.0,
+                          priors=(-priors).tolist())]
+    paired = 0
+    for cfg in cfgs:
+        oe, ores, oc, oi = oracle.decode_many(g, cfg, syn, code.segments)
+        with Decoder(code, cfg) as dec:
+            paired += dec.get_option(OPT_HALF_PAIRS)
+            got = dec.decode_batch_segments(syn)
+            assert np.array_equal(got[0], oe) and np.array_equal(got[1], ores), "bits"
+            assert np.array_equal(got[2], oc) and np.array_equal(got[3], oi), "flags"
+            dec.set_option(OPT_HALF_PAIRS, 0)
+            assert dec.get_option(OPT_HALF_PAIRS) == 0
+            got = dec.decode_batch_segments(syn)
+            assert np.array_equal(got[0], oe) and np.array_equal(got[3], oi), "unpaired"
+    assert paired >= 4, "the packed kernel was not selected"
