@@ -53,6 +53,7 @@ def parse_args():
     ap.add_argument("--skip-latency", action="store_true")
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-variants", action="store_true")
     ap.add_argument("--ref-shots", type=int, default=1 << 14,
                     help="--impl reference: shots per step (bounded sample)")
     return ap.parse_args()
@@ -311,6 +312,21 @@ def run_ours(args):
                 "bytes_per_shot": hbm_bytes_per_shot, "traffic": None},
     }
 
+    # DRAM traffic of the dominant kernel: from the committed `ncu --set full` capture of this
+    # very command (profiles/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum per
+    # launch), not a live measurement; null when the capture is for another shot count.
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f)
+        if (tr.get("shots_per_launch") == shots and tr.get("arithmetic") == args.arithmetic
+                and tr.get("workload") == workload_name(args)):
+            roofline["traffic"] = tr["dram_bytes_per_launch"]
+            roofline["traffic_source"] = tr.get("source")
+            roofline["hbm"]["traffic"] = tr["dram_bytes_per_launch"]
+            roofline["hbm"]["algorithmic_bytes_per_launch"] = shots * hbm_bytes_per_shot
+    except (OSError, ValueError, KeyError):
+        pass
+
     line = {
         "metric": METRIC, "value": value, "unit": "decodes/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -338,6 +354,8 @@ def run_ours(args):
     # ---- single-shot latency (N=1 only)
     if world == 1 and not args.skip_latency:
         line["latency_us"] = measure_latency(args, code, lib, d_syn)
+    if world == 1 and not args.skip_variants:
+        line["variants"] = measure_variants(args, code, d_syn, d_est, d_conv, d_its, stream)
     if world == 1 and not args.skip_cpu_baseline:
         try:
             _, _, base = reference_throughput(args, 4096, 40, 2)
@@ -349,6 +367,77 @@ def run_ours(args):
     dec.close()
     if dist is not None:
         dist.destroy_process_group()
+
+
+def _time_batches(dec, shots, bufs, stream, reps=3):
+    import torch
+    d_syn, d_est, d_conv, d_its = bufs
+    f = lambda: dec.decode_batch_device(shots, d_syn.data_ptr(), d_est.data_ptr(), None,
+                                        d_conv.data_ptr(), d_its.data_ptr(), stream)
+    for _ in range(3):
+        f()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        f()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def measure_variants(args, code, d_syn, d_est, d_conv, d_its, stream):
+    """Device-resident throughput of the other arithmetic modes / protocols on the SAME
+    syndromes (bb784, p as the main line), and of BASELINE config 5: the phenomenological
+    extension diag([Hz | I], [Hx | I]) with LLR priors, int8 messages (degree-padded
+    kernel).  Reported beside the headline, never in place of it."""
+    import torch
+    from paper_2508_07879_b200 import Decoder, DecoderConfig, codes, gf2
+    g = code.combined_graph
+    shots = min(args.shots, 1 << 19)
+    edges = g.num_edges
+    out = {"shots_per_launch": shots, "note": "CUDA events around 3 launches after 3 warm-ups; "
+           "float / int8 / int16 are bit-exact with the reference, half has no reference mode"}
+    for arith in ("float", "int8", "half", "int16"):
+        for label, iters, early in (("cap50_early", 50, True), ("fixed10", 10, False)):
+            if arith == args.arithmetic and label == "cap50_early" and args.max_iterations == 50:
+                continue  # the headline itself
+            cfg = DecoderConfig(max_iterations=iters, early_termination=early, arithmetic=arith)
+            with Decoder(code, cfg) as dec:
+                ms = _time_batches(dec, shots, (d_syn, d_est, d_conv, d_its), stream)
+                eu = float(d_its[:shots].to(torch.int64).sum().item()) * (edges // 2)
+                out[f"{arith}_{label}"] = {"decodes_per_s": shots / ms * 1e3,
+                                           "edge_updates_per_s": eu / ms * 1e3,
+                                           "two_shots_per_thread": bool(dec.get_option(10))}
+    # ---- config 5: extended graph, per-variable priors, int8 (and float for comparison)
+    pq = 0.005
+    h, segs = codes.extended_graph(code)
+    ge = codes.build_tanner_graph(h)
+    n, mz, mx = code.n, code.hz.rows, code.hx.rows
+    llr = float(np.log((1 - pq) / pq))
+    probs = np.full(ge.num_vars, pq)
+    sw, ew = gf2.num_words(ge.num_checks), gf2.num_words(ge.num_vars)
+    shots5 = min(shots, 1 << 18)
+    dev = d_syn.device
+    e_syn = torch.zeros((shots5, sw), dtype=torch.int64, device=dev)
+    e_est = torch.zeros((shots5, ew), dtype=torch.int64, device=dev)
+    for arith in ("int8", "float"):
+        for label, iters, early in (("cap50_early", 50, True), ("fixed10", 10, False)):
+            cfg = DecoderConfig(max_iterations=iters, early_termination=early, arithmetic=arith,
+                                priors=[llr] * ge.num_vars)
+            with Decoder(ge, cfg, segments=segs) as dec:
+                dec.generate_syndromes(args.seed, 0.0, shots5, e_syn.data_ptr(), None, probs=probs,
+                                       css_interleave=False, stream=stream)
+                ms = _time_batches(dec, shots5, (e_syn, e_est, d_conv, d_its), stream)
+                its = d_its[:shots5].to(torch.int64)
+                eu = float(its.sum().item()) * (ge.num_edges // 2)
+                out[f"config5_ext_{arith}_{label}"] = {
+                    "decodes_per_s": shots5 / ms * 1e3, "edge_updates_per_s": eu / ms * 1e3,
+                    "kernel": "decode_ell_kernel" if dec.get_option(107) else "decode_generic_kernel",
+                    "p_data": pq, "p_meas": pq, "shots_per_launch": shots5,
+                    "convergence_rate": float((d_conv[:shots5].min(dim=1).values == 1).double().mean().item()),
+                    "mean_iterations": float(its.max(dim=1).values.double().mean().item())}
+    return out
 
 
 def measure_e2e(args, dec, lib, d_syn, shots, sw, ew, nseg, world):

@@ -49,7 +49,7 @@ __host__ __device__ inline uint32_t lean_stride(int arith) {
 __host__ __device__ inline uint32_t lean_pw(uint32_t seg_mmax) { return (seg_mmax >> 5) + 1; }
 __host__ __device__ inline size_t lean_smem_bytes(uint32_t seg_mmax, int arith) {
   const size_t msg = (static_cast<size_t>(seg_mmax + 1) * lean_stride(arith) + 15) & ~size_t(15);
-  return msg + 4 * (2 * static_cast<size_t>(lean_pw(seg_mmax)) + 8);
+  return msg + 4 * (4 * static_cast<size_t>(lean_pw(seg_mmax)) + 8);
 }
 
 // ---- check update on one message block ---------------------------------------
@@ -346,6 +346,7 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
   uint32_t* const bits = reinterpret_cast<uint32_t*>(smem_raw + msg_bytes);
   uint32_t* const unsat_ctr = bits + 2 * pw;  // [2]
   uint32_t* const ticket = bits + 2 * pw + 2;  // [2]
+  uint32_t* const syn_copy = bits + 2 * pw + 8;  // [2][pw] the syndrome itself, never toggled
 
   // ---- per-thread tables: byte offsets of the q side of every edge / check block
   uint32_t eo[VPT][kDV], co[CPT], cl[CPT], valid = 0;
@@ -385,6 +386,7 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
 
   while (shot < io.nshots) {
     uint32_t* const par = bits + ipar * pw;
+    uint32_t* const syn0 = syn_copy + ipar * pw;
     volatile uint32_t* const unsat = unsat_ctr + ipar;
     // ---------------- prologue ----------------
     if (warp == 0) {
@@ -397,7 +399,10 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
       } else if (Ms - lane * 32u < 32u) {
         loc &= (1u << (Ms - lane * 32u)) - 1u;
       }
-      if (lane < pw) par[lane] = loc;
+      if (lane < pw) {
+        par[lane] = loc;
+        syn0[lane] = loc;
+      }
       const uint32_t cnt = __reduce_add_sync(0xffffffffu, __popc(loc));
       if (lane == 0) {
         *unsat = cnt;
@@ -431,7 +436,7 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
 
     uint32_t synbits = 0;
 #pragma unroll
-    for (int k = 0; k < CPT; ++k) synbits |= ((par[cl[k] >> 5] >> (cl[k] & 31u)) & 1u) << k;
+    for (int k = 0; k < CPT; ++k) synbits |= ((syn0[cl[k] >> 5] >> (cl[k] & 31u)) & 1u) << k;
     const uint32_t next = ticket[ipar];
     if (warp == 0 && lane < gspan && next != kNoShot) {  // prefetch the next shot's syndrome
       raw_next = io.syn[static_cast<uint64_t>(next) * P.syn_w32 + gw0 + lane];
@@ -445,8 +450,9 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
       uint32_t eb = 0;
       if (kFast && iter == 1u) {
 #pragma unroll
-        for (int k = 0; k < VPT; ++k) eb |= vn3_first(P, A{}, msgs, eo[k], par) << k;
-        __syncthreads();  // every thread has read its syndrome bits before any toggle
+        // syndrome bits come from the untouched copy, so toggles of the live bitmap by
+        // faster threads need no barrier here
+        for (int k = 0; k < VPT; ++k) eb |= vn3_first(P, A{}, msgs, eo[k], syn0) << k;
       } else {
 #pragma unroll
         for (int k = 0; k < CPT; ++k) cn6_block(P, A{}, msgs + co[k], (synbits >> k) & 1u);

@@ -38,7 +38,7 @@ constexpr uint32_t kH2Stride = 56, kH2ROff = 24;  // [6 x half2 q | 6 x half2 r 
 
 __host__ __device__ inline size_t lean_h2_smem_bytes(uint32_t seg_mmax) {
   const size_t msg = (static_cast<size_t>(seg_mmax + 1) * kH2Stride + 15) & ~size_t(15);
-  return msg + 4 * (4 * static_cast<size_t>(lean_pw(seg_mmax)) + 16);
+  return msg + 4 * (8 * static_cast<size_t>(lean_pw(seg_mmax)) + 16);
 }
 
 __device__ __forceinline__ __half2 u2h2(uint32_t u) {
@@ -176,6 +176,7 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
   // [item parity][shot lane][pw] bitmaps, then [item parity][shot lane] counters, tickets
   uint32_t* const unsat_ctr = bits + 4 * pw;  // [2][2]
   uint32_t* const ticket = bits + 4 * pw + 4;  // [2]
+  uint32_t* const syn_copy = bits + 4 * pw + 16;  // [item parity][shot lane][pw], never toggled
 
   uint32_t eo[VPT][kDV], co[CPT], cl[CPT], valid = 0;
   float gam[kFast ? 1 : VPT];
@@ -224,11 +225,13 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
     const bool has_b = shot_b < io.nshots;
     uint32_t* const par_a = bits + (ipar * 2) * pw;
     uint32_t* const par_b = bits + (ipar * 2 + 1) * pw;
+    uint32_t* const syn_a = syn_copy + (ipar * 2) * pw;
+    uint32_t* const syn_b = syn_copy + (ipar * 2 + 1) * pw;
     volatile uint32_t* const unsat_a = unsat_ctr + ipar * 2;
     volatile uint32_t* const unsat_b = unsat_ctr + ipar * 2 + 1;
     // ---------------- prologue ----------------
     if (warp == 0) {
-      auto localise = [&](uint32_t raw, uint32_t* par, volatile uint32_t* ctr) {
+      auto localise = [&](uint32_t raw, uint32_t* par, uint32_t* syn0, volatile uint32_t* ctr) {
         uint32_t nb = __shfl_down_sync(0xffffffffu, raw, 1);
         if (lane + 1 >= gspan) nb = 0;
         uint32_t loc = cshift ? __funnelshift_r(raw, nb, cshift) : raw;
@@ -237,12 +240,15 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
         } else if (Ms - lane * 32u < 32u) {
           loc &= (1u << (Ms - lane * 32u)) - 1u;
         }
-        if (lane < pw) par[lane] = loc;
+        if (lane < pw) {
+          par[lane] = loc;
+          syn0[lane] = loc;
+        }
         const uint32_t cnt = __reduce_add_sync(0xffffffffu, __popc(loc));
         if (lane == 0) *ctr = cnt;
       };
-      localise(raw_a, par_a, unsat_a);
-      localise(raw_b, par_b, unsat_b);
+      localise(raw_a, par_a, syn_a, unsat_a);
+      localise(raw_b, par_b, syn_b, unsat_b);
       if (lane == 0) {
         const uint64_t t = static_cast<uint64_t>(atomicAdd(&io.sched[2 + s], 1u)) + peers;
         ticket[ipar] = t < npairs ? static_cast<uint32_t>(t) : kNoShot;
@@ -275,8 +281,8 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
     uint32_t synpair[CPT];
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
-      const uint32_t ba = (par_a[cl[k] >> 5] >> (cl[k] & 31u)) & 1u;
-      const uint32_t bb = (par_b[cl[k] >> 5] >> (cl[k] & 31u)) & 1u;
+      const uint32_t ba = (syn_a[cl[k] >> 5] >> (cl[k] & 31u)) & 1u;
+      const uint32_t bb = (syn_b[cl[k] >> 5] >> (cl[k] & 31u)) & 1u;
       synpair[k] = (ba << 15) | (bb << 31);
     }
     const uint32_t next = ticket[ipar];
@@ -300,11 +306,11 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
         const __half2 g2 = __half2half2(__ushort_as_half(P.gamma_hb));
 #pragma unroll
         for (int k = 0; k < VPT; ++k) {
-          const uint32_t sg = vn3_first_h2<kI8>(P, msgs, eo[k], par_a, par_b, g2);
+          // syndrome bits from the untouched copies: no barrier before the toggles
+          const uint32_t sg = vn3_first_h2<kI8>(P, msgs, eo[k], syn_a, syn_b, g2);
           eb_a |= ((sg >> 15) & 1u) << k;
           eb_b |= (sg >> 31) << k;
         }
-        __syncthreads();
       } else {
 #pragma unroll
         for (int k = 0; k < CPT; ++k) cn6_h2<kI8>(P, msgs + co[k], synpair[k]);

@@ -76,5 +76,30 @@ def main(path, units=None):
     print(f"shared-memory wavefronts: {wf:.0f} total, {ex:.0f} excessive (bank conflicts)")
 
 
+def traffic_json(path, out, shots, arithmetic, workload):
+    """profiles/traffic.json: DRAM bytes of ONE launch of the dominant kernel (bench.py reads it
+    for roofline.traffic)."""
+    import json
+    raw = list(csv.reader(io.StringIO(run(["-i", path, "--page", "raw", "--csv"]))))
+    hdr, units, vals = raw[0], raw[1], raw[-1]
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = {}
+    for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        i = hdr.index(name)
+        tot[name] = float(vals[i].replace(",", "")) * scale[units[i]]
+    with open(out, "w") as f:
+        json.dump({"kernel": vals[hdr.index("Kernel Name")], "shots_per_launch": int(shots),
+                   "arithmetic": arithmetic, "workload": workload,
+                   "dram_bytes_read": tot["dram__bytes_read.sum"],
+                   "dram_bytes_write": tot["dram__bytes_write.sum"],
+                   "dram_bytes_per_launch": sum(tot.values()),
+                   "source": "ncu --set full --clock-control none, one launch of `python bench.py "
+                             "--steps 2 --warmup 1` (tools/prof_bench.sh)"}, f, indent=1)
+        f.write("\n")
+
+
 if __name__ == "__main__":
-    main(sys.argv[1], float(sys.argv[2]) if len(sys.argv) > 2 else None)
+    if len(sys.argv) > 2 and sys.argv[2] == "--traffic-json":
+        traffic_json(sys.argv[1], *sys.argv[3:7])
+    else:
+        main(sys.argv[1], float(sys.argv[2]) if len(sys.argv) > 2 else None)
