@@ -277,7 +277,11 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
   // at most 32 packed words per segment (the loader checks): one lane per word
   const uint32_t gw0 = seg.c0 >> 5, gspan = Ms ? ((seg.c1 - 1) >> 5) - gw0 + 1 : 0u;
   const uint32_t cshift = seg.c0 & 31u;
-  const uint32_t vw0 = seg.v0 >> 5, vspan = seg.v1 > seg.v0 ? ((seg.v1 - 1) >> 5) - vw0 + 1 : 0u;
+  // the last segment also owns the padding bits of the packed rows (they are written as 0)
+  const uint32_t v1z = s + 1u == nseg ? P.est_w32 * 32u : seg.v1;
+  const uint32_t c1z = s + 1u == nseg ? P.syn_w32 * 32u : seg.c1;
+  const uint32_t vw0 = seg.v0 >> 5, vspan = v1z > seg.v0 ? ((v1z - 1) >> 5) - vw0 + 1 : 0u;
+  const uint32_t gspan_out = c1z > seg.c0 ? ((c1z - 1) >> 5) - gw0 + 1 : 0u;
 
   unsigned char* const msgs = smem_raw;
   const size_t msg_bytes = (static_cast<size_t>(P.seg_mmax + 2) * kStride + 15) & ~size_t(15);
@@ -365,7 +369,7 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
     if (warp == nwarps - 1) {  // zero this segment's bits of the shot's estimate
       uint32_t* est_g = io.est + shot * P.est_w32 + vw0;
       for (uint32_t w = lane; w < vspan; w += 32u) {
-        const uint32_t mask = range_mask(vw0 + w, seg.v0, seg.v1);
+        const uint32_t mask = range_mask(vw0 + w, seg.v0, v1z);
         if (mask == 0xffffffffu) {
           est_g[w] = 0u;
         } else {
@@ -436,9 +440,9 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
       uint32_t lo = __shfl_up_sync(0xffffffffu, hi, 1);
       if (lane == 0) lo = 0;
       const uint32_t out = cshift ? __funnelshift_l(lo, hi, cshift) : hi;
-      if (lane < gspan) {
+      if (lane < gspan_out) {
         uint32_t* dst = io.resid + shot * P.syn_w32 + gw0 + lane;
-        const uint32_t mask = range_mask(gw0 + lane, seg.c0, seg.c1);
+        const uint32_t mask = range_mask(gw0 + lane, seg.c0, c1z);
         if (mask == 0xffffffffu) {
           *dst = out;
         } else {

@@ -47,9 +47,17 @@ __host__ __device__ inline uint32_t lean_stride(int arith) {
   return arith == 0 ? 56u : arith == 1 ? 24u : 28u;
 }
 __host__ __device__ inline uint32_t lean_pw(uint32_t seg_mmax) { return (seg_mmax >> 5) + 1; }
-__host__ __device__ inline size_t lean_smem_bytes(uint32_t seg_mmax, int arith) {
+// Syndromes reach the batch kernel in TILES of up to kMaxTile shots: one TMA bulk copy
+// (cp.async.bulk, completing on an mbarrier) and one queue ticket per tile, two tiles in
+// flight per CTA.
+constexpr uint32_t kMaxTile = 16;
+__host__ __device__ inline size_t lean_bits_words(uint32_t seg_mmax) {
+  return (4 * static_cast<size_t>(lean_pw(seg_mmax)) + 8 + 3) & ~size_t(3);  // keeps 16-byte alignment
+}
+__host__ __device__ inline size_t lean_smem_bytes(uint32_t seg_mmax, int arith, uint32_t syn_w32) {
   const size_t msg = (static_cast<size_t>(seg_mmax + 1) * lean_stride(arith) + 15) & ~size_t(15);
-  return msg + 4 * (4 * static_cast<size_t>(lean_pw(seg_mmax)) + 8);
+  // messages | bitmaps, counters, tickets | 2 syndrome tiles | 2 mbarriers | tile info [2][2]
+  return msg + 4 * lean_bits_words(seg_mmax) + 2 * kMaxTile * syn_w32 * 4 + 16 + 16 + 16;
 }
 
 // ---- check update on one message block ---------------------------------------
@@ -321,6 +329,37 @@ __device__ __forceinline__ uint32_t vn3_first(const DecodeParams& P, ArithI16, u
 
 // ---- the kernel ---------------------------------------------------------------
 
+// Warp 0 of a batch CTA: describe syndrome tile `t` (K shots) in info = {first shot, shots}
+// and start its copy into `buf`: one TMA bulk copy completing on `bar`, or - for a ragged
+// tile (odd number of 8-byte-multiple rows) or a caller buffer that is not 16-byte aligned -
+// plain loads.  Out of line on purpose: it runs once per tile, and the item loop around it
+// is short of registers and instruction-cache room.
+__device__ __noinline__ void lean_issue_tile(const uint32_t* syn, uint64_t nshots, uint32_t syn_w32,
+                                             uint32_t K, uint64_t t, uint32_t* buf, uint64_t* bar,
+                                             uint32_t* info, uint32_t lane) {
+  const uint64_t first = t * K;
+  const uint32_t cnt =
+      first < nshots ? static_cast<uint32_t>(min(static_cast<uint64_t>(K), nshots - first)) : 0u;
+  if (lane == 0) {
+    info[0] = cnt ? static_cast<uint32_t>(first) : kNoShot;
+    info[1] = cnt;
+  }
+  if (cnt == 0u) return;
+  const uint32_t* src = syn + first * syn_w32;
+  const uint32_t bytes = cnt * syn_w32 * 4u;
+  if (((bytes | static_cast<uint32_t>(reinterpret_cast<uintptr_t>(src))) & 15u) == 0u) {
+    if (lane == 0) {
+      fence_proxy_async_smem();  // earlier generic-proxy reads of this buffer are done
+      mbar_expect_tx(bar, bytes);
+      tma_load_1d(buf, src, bytes, bar);
+    }
+  } else {
+    for (uint32_t w = lane; w < cnt * syn_w32; w += 32u) buf[w] = src[w];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar);
+  }
+}
+
 template <class A, int CPT, int VPT, bool kFast, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB)
 decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant__ ShotIO io) {
@@ -339,7 +378,11 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
   const uint32_t pw = lean_pw(P.seg_mmax);
   const uint32_t pws = (Ms + 31u) >> 5;
   const uint32_t gw0 = seg.c0 >> 5, gspan = ((seg.c1 - 1) >> 5) - gw0 + 1, cshift = seg.c0 & 31u;
-  const uint32_t vw0 = seg.v0 >> 5, vspan = ((seg.v1 - 1) >> 5) - vw0 + 1;
+  // the last segment also owns the padding bits of the packed rows (they are written as 0)
+  const uint32_t v1z = s + 1u == nseg ? P.est_w32 * 32u : seg.v1;
+  const uint32_t c1z = s + 1u == nseg ? P.syn_w32 * 32u : seg.c1;
+  const uint32_t vw0 = seg.v0 >> 5, vspan = ((v1z - 1) >> 5) - vw0 + 1;
+  const uint32_t gspan_out = ((c1z - 1) >> 5) - gw0 + 1;
 
   unsigned char* const msgs = smem_raw;
   const size_t msg_bytes = (static_cast<size_t>(P.seg_mmax + 1) * kStride + 15) & ~size_t(15);
@@ -347,6 +390,13 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
   uint32_t* const unsat_ctr = bits + 2 * pw;  // [2]
   uint32_t* const ticket = bits + 2 * pw + 2;  // [2]
   uint32_t* const syn_copy = bits + 2 * pw + 8;  // [2][pw] the syndrome itself, never toggled
+  uint32_t* const tilebuf = bits + lean_bits_words(P.seg_mmax);  // [2][kMaxTile][syn_w32]
+  uint64_t* const mbar = reinterpret_cast<uint64_t*>(tilebuf + 2 * kMaxTile * P.syn_w32);  // [2]
+  uint32_t* const tinfo = reinterpret_cast<uint32_t*>(mbar + 2);  // [2]{first shot, shots}
+  // warp 0's tile cursor lives in shared memory (it is touched once per item, and registers
+  // are what this kernel is short of): buffer in use, item within it, mbarrier phase bits
+  uint32_t* const tstate = tinfo + 4;  // {tb, ti, tphase}
+  const uint32_t K = io.tile, tile_words = kMaxTile * P.syn_w32;
 
   // ---- per-thread tables: byte offsets of the q side of every edge / check block
   uint32_t eo[VPT][kDV], co[CPT], cl[CPT], valid = 0;
@@ -376,11 +426,19 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
   }
   for (uint32_t b = tid; b < kStride; b += T) msgs[P.seg_mmax * kStride + b] = 0;  // dummy block
 
-  uint64_t shot = peer;
-  uint32_t raw_next = 0;
-  if (warp == 0 && lane < gspan && shot < io.nshots) {
-    raw_next = io.syn[shot * P.syn_w32 + gw0 + lane];
+  auto issue_tile = [&](uint64_t t, uint32_t b) {
+    lean_issue_tile(io.syn, io.nshots, P.syn_w32, K, t, tilebuf + b * tile_words, &mbar[b],
+                    tinfo + 2 * b, lane);
+  };
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1u);
+    mbar_init(&mbar[1], 1u);
+    mbar_fence_init();
+    tstate[0] = tstate[1] = tstate[2] = 0u;
   }
+  __syncthreads();
+  if (warp == 0) issue_tile(peer, 0u);
+  uint64_t shot = static_cast<uint64_t>(peer) * K;
   uint32_t ipar = 0;
   __syncthreads();
 
@@ -390,7 +448,24 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
     volatile uint32_t* const unsat = unsat_ctr + ipar;
     // ---------------- prologue ----------------
     if (warp == 0) {
+      uint32_t tb = tstate[0], ti = tstate[1];
+      if (ti == 0u) {
+        // first item of a tile: its bytes must have landed; the other buffer is free (its
+        // tile is finished), so draw the next tile's ticket and start that copy now - the
+        // atomic's round trip and the copy hide behind the K items of this tile
+        const uint32_t tphase = tstate[2];
+        mbar_wait(&mbar[tb], (tphase >> tb) & 1u);
+        __syncwarp();
+        if (lane == 0) tstate[2] = tphase ^ (1u << tb);
+        uint32_t t = 0;
+        if (lane == 0) t = atomicAdd(&io.sched[2 + s], 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        issue_tile(static_cast<uint64_t>(t) + peers, tb ^ 1u);
+        __syncwarp();
+      }
       // packed syndrome words -> segment-local bitmap, and its population count
+      const uint32_t raw_next =
+          lane < gspan ? tilebuf[tb * tile_words + ti * P.syn_w32 + gw0 + lane] : 0u;
       uint32_t nb = __shfl_down_sync(0xffffffffu, raw_next, 1);
       if (lane + 1 >= gspan) nb = 0;
       uint32_t loc = cshift ? __funnelshift_r(raw_next, nb, cshift) : raw_next;
@@ -406,14 +481,17 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
       const uint32_t cnt = __reduce_add_sync(0xffffffffu, __popc(loc));
       if (lane == 0) {
         *unsat = cnt;
-        const uint64_t t = static_cast<uint64_t>(atomicAdd(&io.sched[2 + s], 1u)) + peers;
-        ticket[ipar] = t < io.nshots ? static_cast<uint32_t>(t) : kNoShot;
+        // next item: the following row of this tile, else the first row of the next tile
+        const bool more = ti + 1u < tinfo[2 * tb + 1];
+        ticket[ipar] = more ? static_cast<uint32_t>(shot) + 1u : tinfo[2 * (tb ^ 1u)];
+        tstate[0] = more ? tb : tb ^ 1u;
+        tstate[1] = more ? ti + 1u : 0u;
       }
     }
     if (warp == nwarps - 1) {  // zero this segment's bits of the shot's estimate
       uint32_t* est_g = io.est + shot * P.est_w32 + vw0;
       for (uint32_t w = lane; w < vspan; w += 32u) {
-        const uint32_t mask = range_mask(vw0 + w, seg.v0, seg.v1);
+        const uint32_t mask = range_mask(vw0 + w, seg.v0, v1z);
         if (mask == 0xffffffffu) {
           est_g[w] = 0u;
         } else {
@@ -438,9 +516,6 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
 #pragma unroll
     for (int k = 0; k < CPT; ++k) synbits |= ((syn0[cl[k] >> 5] >> (cl[k] & 31u)) & 1u) << k;
     const uint32_t next = ticket[ipar];
-    if (warp == 0 && lane < gspan && next != kNoShot) {  // prefetch the next shot's syndrome
-      raw_next = io.syn[static_cast<uint64_t>(next) * P.syn_w32 + gw0 + lane];
-    }
 
     // ---------------- iterations ----------------
     uint32_t iter = 0;
@@ -494,9 +569,9 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
       uint32_t lo = __shfl_up_sync(0xffffffffu, hi, 1);
       if (lane == 0) lo = 0;
       const uint32_t out = cshift ? __funnelshift_l(lo, hi, cshift) : hi;
-      if (lane < gspan) {
+      if (lane < gspan_out) {
         uint32_t* dst = io.resid + shot * P.syn_w32 + gw0 + lane;
-        const uint32_t mask = range_mask(gw0 + lane, seg.c0, seg.c1);
+        const uint32_t mask = range_mask(gw0 + lane, seg.c0, c1z);
         if (mask == 0xffffffffu) {
           *dst = out;
         } else {

@@ -167,7 +167,11 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
   const uint32_t pw = lean_pw(P.seg_mmax);
   const uint32_t pws = (Ms + 31u) >> 5;
   const uint32_t gw0 = seg.c0 >> 5, gspan = ((seg.c1 - 1) >> 5) - gw0 + 1, cshift = seg.c0 & 31u;
-  const uint32_t vw0 = seg.v0 >> 5, vspan = ((seg.v1 - 1) >> 5) - vw0 + 1;
+  // the last segment also owns the padding bits of the packed rows (they are written as 0)
+  const uint32_t v1z = s + 1u == nseg ? P.est_w32 * 32u : seg.v1;
+  const uint32_t c1z = s + 1u == nseg ? P.syn_w32 * 32u : seg.c1;
+  const uint32_t vw0 = seg.v0 >> 5, vspan = ((v1z - 1) >> 5) - vw0 + 1;
+  const uint32_t gspan_out = ((c1z - 1) >> 5) - gw0 + 1;
   const uint64_t npairs = (io.nshots + 1) / 2;
 
   unsigned char* const msgs = smem_raw;
@@ -258,7 +262,7 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
       for (int which = 0; which < (has_b ? 2 : 1); ++which) {
         uint32_t* est_g = io.est + (shot_a + which) * P.est_w32 + vw0;
         for (uint32_t w = lane; w < vspan; w += 32u) {
-          const uint32_t mask = range_mask(vw0 + w, seg.v0, seg.v1);
+          const uint32_t mask = range_mask(vw0 + w, seg.v0, v1z);
           if (mask == 0xffffffffu) {
             est_g[w] = 0u;
           } else {
@@ -383,9 +387,9 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
         uint32_t lo = __shfl_up_sync(0xffffffffu, hi, 1);
         if (lane == 0) lo = 0;
         const uint32_t out = cshift ? __funnelshift_l(lo, hi, cshift) : hi;
-        if (lane < gspan) {
+        if (lane < gspan_out) {
           uint32_t* dst = io.resid + shot * P.syn_w32 + gw0 + lane;
-          const uint32_t mask = range_mask(gw0 + lane, seg.c0, seg.c1);
+          const uint32_t mask = range_mask(gw0 + lane, seg.c0, c1z);
           if (mask == 0xffffffffu) {
             *dst = out;
           } else {

@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -679,13 +680,30 @@ void ensure_batch(qb_decoder* h, uint64_t shots, bool want_resid) {
   h->batch_cap = cap;
 }
 
-unsigned batch_grid(qb_decoder* h, uint64_t shots) {
+uint64_t resident_ctas(qb_decoder* h) {
   int per_sm = h->bat.ctas_per_sm;
   if (h->opt_batch_ctas > 0) per_sm = std::min<int>(per_sm, static_cast<int>(h->opt_batch_ctas));
-  const uint64_t resident = static_cast<uint64_t>(per_sm) * h->sm_count;
+  return static_cast<uint64_t>(per_sm) * h->sm_count;
+}
+
+// Shots per syndrome tile of the lean batch kernel (one TMA bulk copy + one queue ticket
+// each): as large as leaves every resident CTA at least four tiles; 1 for small batches.
+uint32_t batch_tile(qb_decoder* h, uint64_t shots) {
+  if (!(h->bat.lean && !h->bat.pair && !h->bat.ell)) return 1;
+  const uint64_t per_seg = std::max<uint64_t>(1, resident_ctas(h) / h->P.nseg);
+  if (const char* e = std::getenv("QB_TILE")) return static_cast<uint32_t>(std::atoi(e));
+  for (uint32_t k = kMaxTile; k > 1; k >>= 1) {
+    if ((shots + k - 1) / k >= 4 * per_seg) return k;
+  }
+  return 1;
+}
+
+unsigned batch_grid(qb_decoder* h, uint64_t shots) {
+  const uint64_t resident = resident_ctas(h);
   if (h->bat.items) {  // equal numbers of CTAs per segment
     const uint64_t nseg = h->P.nseg;
-    const uint64_t items = h->bat.pair ? (shots + 1) / 2 : shots;
+    const uint64_t tile = batch_tile(h, shots);
+    const uint64_t items = h->bat.pair ? (shots + 1) / 2 : (shots + tile - 1) / tile;
     const uint64_t per_seg = std::max<uint64_t>(1, std::min<uint64_t>(resident / nseg, items));
     return static_cast<unsigned>(per_seg * nseg);
   }
@@ -705,6 +723,7 @@ void run_batch_device(qb_decoder* h, uint64_t shots, const uint32_t* d_syn, uint
   io.conv = d_conv;
   io.iters = d_iters;
   io.sched = h->d_sched + sched_slot * kSchedWords;  // concurrent launches need their own tickets
+  io.tile = batch_tile(h, shots);
   launch_plan(h, h->bat, io, batch_grid(h, shots), stream);
 }
 
@@ -1175,7 +1194,7 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
       P.seg_mmax = std::max(P.seg_mmax, P.segs[k].c1 - P.segs[k].c0);
       P.seg_nmax = std::max(P.seg_nmax, P.segs[k].v1 - P.segs[k].v0);
     }
-    h->smem_lean = lean_smem_bytes(P.seg_mmax, arith == QB_ARITH_HALF ? 3 : arith);
+    h->smem_lean = lean_smem_bytes(P.seg_mmax, arith == QB_ARITH_HALF ? 3 : arith, P.syn_w32);
     if (h->smem_bytes > static_cast<size_t>(h->max_smem_optin)) {
       fail(QB_INVALID_ARGUMENT, "graph needs " + std::to_string(h->smem_bytes) +
                                     " bytes of shared memory per shot; the device offers " +

@@ -446,3 +446,64 @@ def test_int8_on_the_packed_fp16_kernel_is_bit_exact(oracle, name, shots, p):
             got = dec.decode_batch_segments(syn)
             assert np.array_equal(got[0], oe) and np.array_equal(got[3], oi), "unpaired"
     assert paired >= 4, "the packed kernel was not selected"
+
+
+@pytest.mark.parametrize("mode", ["float", "int16"])
+def test_tma_tiles_ragged_tail_and_unaligned_buffers(oracle, mode):
+    """The lean batch kernel streams syndromes in tiles of up to 16 shots (one TMA bulk copy
+    per tile).  20001 shots leave a ragged last tile (odd row count -> plain loads), and a
+    buffer that starts on an odd 104-byte row is only 8-byte aligned (every tile -> plain
+    loads): both must give the same results as the aligned bulk copies and the oracle."""
+    import torch
+    code = codes.make_code("bb784")
+    g = code.combined_graph
+    shots = 20001
+    rng = np.random.default_rng(99)
+    _, _, syn = error_syndromes(code, rng, shots, 0.01)
+    cfg = DecoderConfig(max_iterations=20, arithmetic=mode)
+    sw, ew = gf2.num_words(g.num_checks), gf2.num_words(g.num_vars)
+    host = torch.from_numpy(syn.view(np.int64).copy())
+    d_all = torch.zeros((shots + 1, sw), dtype=torch.int64, device="cuda")
+    d_all[1:] = host.cuda()
+    d_aligned = d_all[1:].clone()
+    assert d_aligned.data_ptr() % 16 == 0 and d_all[1:].data_ptr() % 16 == 8
+    outs = []
+    stream = torch.cuda.current_stream().cuda_stream
+    with Decoder(code, cfg) as dec:
+        for d_syn in (d_aligned, d_all[1:]):
+            d_est = torch.full((shots, ew), -1, dtype=torch.int64, device="cuda")
+            d_res = torch.full((shots, sw), -1, dtype=torch.int64, device="cuda")
+            d_conv = torch.zeros((shots, 2), dtype=torch.uint8, device="cuda")
+            d_its = torch.zeros((shots, 2), dtype=torch.int32, device="cuda")
+            dec.decode_batch_device(shots, d_syn.data_ptr(), d_est.data_ptr(), d_res.data_ptr(),
+                                    d_conv.data_ptr(), d_its.data_ptr(), stream)
+            torch.cuda.synchronize()
+            outs.append((d_est.cpu().numpy().view(np.uint64), d_res.cpu().numpy().view(np.uint64),
+                         d_conv.cpu().numpy(), d_its.cpu().numpy().astype(np.uint32)))
+    assert all(np.array_equal(a, b) for a, b in zip(outs[0], outs[1])), "aligned vs unaligned"
+    for sl in (slice(0, 200), slice(shots - 200, shots)):
+        oe, ores, oc, oi = oracle.decode_many(g, cfg, syn[sl], code.segments)
+        assert np.array_equal(outs[0][0][sl], oe) and np.array_equal(outs[0][1][sl], ores)
+        assert np.array_equal(outs[0][2][sl], oc) and np.array_equal(outs[0][3][sl], oi)
+    # every shot: residual == H e_hat xor s, converged <=> zero residual (size-independent)
+    est = gf2.unpack_bits(outs[0][0], g.num_vars)
+    res = gf2.unpack_bits(outs[0][1], g.num_checks)
+    assert np.array_equal(res, code.combined.mat_vec(est) ^ gf2.unpack_bits(syn, g.num_checks))
+    mz = code.hz.rows
+    assert np.array_equal(outs[0][2][:, 0] == 1, ~res[:, :mz].any(axis=1))
+    assert np.array_equal(outs[0][2][:, 1] == 1, ~res[:, mz:].any(axis=1))
+    # the other batch kernels on pre-filled (-1) output buffers: padding bits of the packed
+    # rows must come back as zeros from every one of them
+    n2 = 2001
+    with Decoder(code, cfg) as dec:
+        for opt, val in ((OPT_BATCH_SHAPE, 1), (OPT_KERNEL, 1)):
+            dec.set_option(opt, val)
+            d_est = torch.full((n2, ew), -1, dtype=torch.int64, device="cuda")
+            d_res = torch.full((n2, sw), -1, dtype=torch.int64, device="cuda")
+            d_conv = torch.zeros((n2, 2), dtype=torch.uint8, device="cuda")
+            d_its = torch.zeros((n2, 2), dtype=torch.int32, device="cuda")
+            dec.decode_batch_device(n2, d_aligned.data_ptr(), d_est.data_ptr(), d_res.data_ptr(),
+                                    d_conv.data_ptr(), d_its.data_ptr(), stream)
+            torch.cuda.synchronize()
+            assert np.array_equal(d_est.cpu().numpy().view(np.uint64), outs[0][0][:n2]), (opt, val)
+            assert np.array_equal(d_res.cpu().numpy().view(np.uint64), outs[0][1][:n2]), (opt, val)
