@@ -487,8 +487,10 @@ def measure_latency(args, code, lib, d_syn):
         cfg = DecoderConfig(max_iterations=iters, early_termination=early,
                             arithmetic=args.arithmetic)
         with Decoder(code, cfg) as dec:
-            for io_mode, io_name in ((2, "doorbell"), (0, "mapped"), (1, "memcpy")):
+            for io_mode, io_name in ((2, "doorbell"), (0, "mapped"), (1, "memcpy"),
+                                     (1, "memcpy_nograph")):
                 dec.set_option(1, io_mode)
+                dec.set_option(12, 0 if io_name == "memcpy_nograph" else 1)
                 wall, kern, digest = dec.latency_run(pool, 300, args.latency_shots)
                 wall = np.sort(wall.astype(np.float64) * 1e-3)
                 kern = np.sort(kern.astype(np.float64) * 1e-3)
@@ -497,12 +499,22 @@ def measure_latency(args, code, lib, d_syn):
                     "mean": float(np.mean(wall)), "min": float(wall[0]), "max": float(wall[-1]),
                     "kernel_p50": nearest_rank(kern, 50), "kernel_p99": nearest_rank(kern, 99),
                     "shots": args.latency_shots, "digest": "%016x" % digest}
+                if io_mode == 1:  # the same protocol timed by CUDA events on the stream
+                    dec.set_option(11, 1)
+                    _, ev, _ = dec.latency_run(pool, 300, args.latency_shots)
+                    dec.set_option(11, 0)
+                    ev = np.sort(ev.astype(np.float64) * 1e-3)
+                    out[f"{label}_{io_name}"].update(
+                        {"cuda_event_p50": nearest_rank(ev, 50), "cuda_event_p99": nearest_rank(ev, 99),
+                         "cuda_event_mean": float(np.mean(ev))})
     out["note"] = ("wall = host steady_clock around the whole qb_decode (copy-in, launch, "
                    "completion, copy-out) inside qb_latency_run; kernel = in-kernel %globaltimer "
                    "span; doorbell = persistent cluster polling mapped host memory (no launch per "
                    "shot), mapped = one cluster launch per shot with the syndrome in the kernel "
                    "parameters and results to mapped pinned memory + completion flag, memcpy = "
-                   "cudaMemcpyAsync H2D / kernel / D2H + stream sync (paper protocol)")
+                   "cudaMemcpyAsync H2D / kernel / D2H + stream sync (paper protocol) as ONE CUDA-graph "
+                   "launch per decode (memcpy_nograph: three separate stream operations); cuda_event = "
+                   "cudaEventRecord before the H2D copy and after the D2H copy of that protocol")
     return out
 
 

@@ -122,6 +122,16 @@ typedef enum {
    * Q16 scaling for all 128 magnitudes); 0 = one shot per thread.  Results are
    * identical either way. */
   QB_OPT_HALF_PAIRS = 10,
+  /* 1 = bracket every single-shot decode of the memcpy protocol (QB_OPT_LATENCY_IO
+   * = 1) with CUDA events on its stream: H2D copy + kernel + D2H copy as the device
+   * sees them (the reference paper's timing).  qb_latency_run then
+   * reports that span in kernel_ns[] instead of the in-kernel %globaltimer span;
+   * QB_OPT_INFO_LAST_EVENT_NS returns the most recent one. */
+  QB_OPT_LATENCY_EVENTS = 11,
+  /* Memcpy protocol (QB_OPT_LATENCY_IO = 1): 1 (default) = H2D copy, cluster kernel
+   * and D2H copy are ONE CUDA-graph launch per decode (captured on first use);
+   * 0 = three separate stream operations. */
+  QB_OPT_LATENCY_GRAPH = 12,
   /* Read-only (qb_get_option): the launch plans actually in use. */
   QB_OPT_INFO_BATCH_CTAS_PER_SM = 100,
   QB_OPT_INFO_BATCH_BLOCK = 101,
@@ -132,7 +142,8 @@ typedef enum {
   QB_OPT_INFO_LATENCY_LEAN = 106,
   /* 100 * DC + DV of the degree-padded batch kernel in use (irregular graphs whose
    * degrees fit an instantiated bound), 0 when another kernel serves batches. */
-  QB_OPT_INFO_BATCH_ELL = 107
+  QB_OPT_INFO_BATCH_ELL = 107,
+  QB_OPT_INFO_LAST_EVENT_NS = 108
 } qb_option;
 
 /* Builds a decoder: validates like Decoder::Decoder (decoder.cpp:373-404,

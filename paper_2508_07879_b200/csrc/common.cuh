@@ -178,6 +178,15 @@ struct ArithI16 {
   static constexpr bool kInt = true;
 };
 
+// Integer modes with messages held in 32-bit words (degree-padded kernel): same arithmetic
+// as int8 / int16 - the saturation bound is DecodeParams::kmax - without the sub-word
+// packing and sign-extension instructions, which dominate the ALU-bound integer kernels.
+struct ArithI32 {
+  using Msg = int32_t;
+  using Gam = int32_t;
+  static constexpr bool kInt = true;
+};
+
 // Q16 scaling of a non-negative magnitude (decoder.cpp:226-229).  mag <= 32767
 // and alpha_fx <= 65536, so the product fits 32 unsigned bits.
 __device__ __forceinline__ int32_t scale_q16(uint32_t mag, uint32_t alpha_fx) {

@@ -81,6 +81,11 @@ template <> struct EllSentinel<ArithI16> {
   static __device__ __forceinline__ int16_t deg1(const DecodeParams& P) { return static_cast<int16_t>(P.kmax); }
 };
 
+template <> struct EllSentinel<ArithI32> {
+  static __device__ __forceinline__ int32_t pad(const DecodeParams& P) { return P.kmax; }
+  static __device__ __forceinline__ int32_t deg1(const DecodeParams& P) { return P.kmax; }
+};
+
 // ---- check update over one padded block ------------------------------------------
 
 template <int DC>
@@ -177,6 +182,11 @@ __device__ __forceinline__ void cn_ell(const DecodeParams& P, ArithI16, unsigned
                                        uint32_t syn_bit) {
   cn_ell_int<ArithI16, DC>(P, blk, syn_bit);
 }
+template <int DC>
+__device__ __forceinline__ void cn_ell(const DecodeParams& P, ArithI32, unsigned char* blk,
+                                       uint32_t syn_bit) {
+  cn_ell_int<ArithI32, DC>(P, blk, syn_bit);
+}
 
 // ---- variable update over DV padded slots; returns 1 iff the variable decides 1 ----
 // `keep0`: the variable has degree 1, so its only real message stays gamma.
@@ -249,6 +259,11 @@ template <int DC, int DV>
 __device__ __forceinline__ uint32_t vn_ell(const DecodeParams& P, ArithI16, unsigned char* base,
                                            const uint32_t (&eo)[DV], int32_t gamma, bool) {
   return vn_ell_int<ArithI16, DC, DV>(P, base, eo, gamma);
+}
+template <int DC, int DV>
+__device__ __forceinline__ uint32_t vn_ell(const DecodeParams& P, ArithI32, unsigned char* base,
+                                           const uint32_t (&eo)[DV], int32_t gamma, bool) {
+  return vn_ell_int<ArithI32, DC, DV>(P, base, eo, gamma);
 }
 
 // ---- the kernel -------------------------------------------------------------------

@@ -157,6 +157,15 @@ struct qb_decoder {
   uint32_t rec_stride = 0;
   bool db_running = false;
   int64_t opt_idle_ms = 200;
+  // optional CUDA-event timing of the memcpy protocol (H2D + kernel + D2H on the stream)
+  int64_t opt_latency_events = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  uint64_t last_event_ns = 0;
+  // memcpy protocol as ONE CUDA-graph launch (H2D copy -> cluster kernel -> D2H copy); two
+  // instantiated graphs with different record tags alternate, so a stale record is detected
+  int64_t opt_latency_graph = 1;
+  cudaGraphExec_t lat_graph[2] = {nullptr, nullptr};
+  uint32_t lat_graph_flip = 0;
   bool regular63 = false;  // every check degree 6, every variable degree 3
   uint32_t max_dc = 0, max_dv = 0;  // largest check / variable degree of the graph
   bool i8_pair_ok = false;  // int8 mode: the Q16 scaling has an exact fp16 form (kernel_lean_h2.cuh)
@@ -171,6 +180,13 @@ struct qb_decoder {
 };
 
 namespace {
+
+void drop_latency_graphs(qb_decoder* h) {
+  for (auto& g : h->lat_graph) {
+    if (g) cudaGraphExecDestroy(g);
+    g = nullptr;
+  }
+}
 
 void free_batch(qb_decoder* h) {
   cudaFree(h->b_syn);
@@ -195,6 +211,9 @@ void destroy(qb_decoder* h) {
   }
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (void* p : h->dev_allocs) cudaFree(p);
+  drop_latency_graphs(h);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
   cudaFree(h->d_sched);
   cudaFree(h->d_in_dev);
   cudaFree(h->d_out_dev);
@@ -453,14 +472,16 @@ KernelFn ell_kernel_t(int idx) {
   }
 }
 
+// int8 and int16 share one build: 32-bit message words, saturation bound from DecodeParams
 KernelFn ell_kernel(int arith, int idx) {
   switch (arith) {
     case QB_ARITH_FLOAT: return ell_kernel_t<ArithF32>(idx);
-    case QB_ARITH_INT8: return ell_kernel_t<ArithI8>(idx);
-    case QB_ARITH_INT16: return ell_kernel_t<ArithI16>(idx);
+    case QB_ARITH_INT8:
+    case QB_ARITH_INT16: return ell_kernel_t<ArithI32>(idx);
     default: return ell_kernel_t<ArithF16>(idx);
   }
 }
+uint32_t ell_msg_bytes(int arith) { return arith == QB_ARITH_HALF ? 2u : 4u; }
 
 uint32_t round_up32(uint32_t x) { return (x + 31u) & ~31u; }
 
@@ -479,7 +500,7 @@ uint32_t regular_group_threads(const DecodeParams& P, uint32_t cpt, uint32_t vpt
 void finish_plan(qb_decoder* h, LaunchPlan& pl) {
   pl.block = pl.cluster ? pl.group_threads : pl.ngroups * pl.group_threads;
   if (pl.items) pl.block = pl.group_threads;
-  pl.smem = pl.ell    ? ell_smem_bytes(h->P.seg_mmax, static_cast<uint32_t>(msg_bytes_of(h->arith)),
+  pl.smem = pl.ell    ? ell_smem_bytes(h->P.seg_mmax, ell_msg_bytes(h->arith),
                                        static_cast<uint32_t>(pl.ell / 100))
             : pl.pair ? lean_h2_smem_bytes(h->P.seg_mmax)
             : pl.lean ? h->smem_lean
@@ -513,6 +534,7 @@ LaunchPlan generic_plan(qb_decoder* h) {
 
 void make_plans(qb_decoder* h) {
   const DecodeParams& P = h->P;
+  drop_latency_graphs(h);  // they bake in the kernel and its launch shape
   const bool use_regular = h->regular63 && h->opt_kernel != 1;
   if (h->opt_kernel == 2 && !h->regular63) {
     fail(QB_INVALID_ARGUMENT, "regular kernel needs a (6,3)-regular graph with at most 8 segments");
@@ -526,7 +548,7 @@ void make_plans(qb_decoder* h) {
         if (h->max_dc > static_cast<uint32_t>(ev.dc) || h->max_dv > static_cast<uint32_t>(ev.dv)) continue;
         const uint32_t T = regular_group_threads(P, ev.cpt, ev.vpt);
         if (T > static_cast<uint32_t>(ev.maxt)) continue;
-        const size_t smem = ell_smem_bytes(P.seg_mmax, static_cast<uint32_t>(msg_bytes_of(h->arith)),
+        const size_t smem = ell_smem_bytes(P.seg_mmax, ell_msg_bytes(h->arith),
                                            static_cast<uint32_t>(ev.dc));
         if (smem > static_cast<size_t>(h->max_smem_optin)) continue;
         LaunchPlan pl{};
@@ -912,13 +934,54 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
       ctl.mode = 1;  // the paper's protocol: H2D copy, kernel, D2H copy, synchronize
       std::memcpy(h->h_in, syndrome, P.syn_w32 * 4);
       io.syn = h->d_in_dev;
-      CUDA_TRY(cudaMemcpyAsync(h->d_in_dev, h->h_in, P.syn_w32 * 4, cudaMemcpyHostToDevice,
-                               h->stream));
-      launch_lean_latency(h, io, ctl, syn);
-      CUDA_TRY(cudaMemcpyAsync(h->h_rec, h->d_rec_dev,
-                               static_cast<size_t>(h->rec_stride) * P.nseg * 4,
-                               cudaMemcpyDeviceToHost, h->stream));
+      const bool timed = h->opt_latency_events != 0;
+      if (timed && !h->ev0) {
+        CUDA_TRY(cudaEventCreate(&h->ev0));
+        CUDA_TRY(cudaEventCreate(&h->ev1));
+      }
+      auto enqueue = [&] {
+        CUDA_TRY(cudaMemcpyAsync(h->d_in_dev, h->h_in, P.syn_w32 * 4, cudaMemcpyHostToDevice,
+                                 h->stream));
+        launch_lean_latency(h, io, ctl, syn);
+        CUDA_TRY(cudaMemcpyAsync(h->h_rec, h->d_rec_dev,
+                                 static_cast<size_t>(h->rec_stride) * P.nseg * 4,
+                                 cudaMemcpyDeviceToHost, h->stream));
+      };
+      if (h->opt_latency_graph != 0 && !debug) {
+        const uint32_t g = h->lat_graph_flip ^= 1u;
+        seq = 0x7ffffff0u + g;  // the record tag baked into graph g
+        if (!h->lat_graph[g]) {
+          ctl.first_seq = seq;
+          io.seq = seq;
+          cudaGraph_t graph = nullptr;
+          CUDA_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+          try {
+            enqueue();
+          } catch (...) {
+            cudaStreamEndCapture(h->stream, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+          }
+          CUDA_TRY(cudaStreamEndCapture(h->stream, &graph));
+          const cudaError_t ie = cudaGraphInstantiate(&h->lat_graph[g], graph, 0);
+          cudaGraphDestroy(graph);
+          CUDA_TRY(ie);
+          --h->launches;  // the capture enqueued nothing
+        }
+        if (timed) CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
+        CUDA_TRY(cudaGraphLaunch(h->lat_graph[g], h->stream));
+        ++h->launches;
+      } else {
+        if (timed) CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
+        enqueue();
+      }
+      if (timed) CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
       CUDA_TRY(cudaStreamSynchronize(h->stream));
+      if (timed) {
+        float ms = 0.0f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+        h->last_event_ns = static_cast<uint64_t>(static_cast<double>(ms) * 1e6);
+      }
       if (!records_ready(h, seq)) fail(QB_RUNTIME_ERROR, "decode kernel produced no record");
     }
     unpack_records(h, estimate, residual, converged, iterations);
@@ -1357,6 +1420,14 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
         if (value < 0 || value > 2) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_SHAPE: 0, 1 or 2");
         h->opt_batch_shape = value;
         break;
+      case QB_OPT_LATENCY_GRAPH:
+        if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_LATENCY_GRAPH: 0 or 1");
+        h->opt_latency_graph = value;
+        return;
+      case QB_OPT_LATENCY_EVENTS:
+        if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_LATENCY_EVENTS: 0 or 1");
+        h->opt_latency_events = value;
+        return;  // no effect on the launch plans
       case QB_OPT_HALF_PAIRS:
         if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_HALF_PAIRS: 0 or 1");
         h->opt_batch_pair = value;
@@ -1422,6 +1493,9 @@ int64_t qb_get_option(const qb_decoder* h, int option) {
     case QB_OPT_HALF_PAIRS: return h->bat.pair ? 1 : 0;
     case QB_OPT_INFO_LATENCY_LEAN: return h->lat_lean_kernel ? 1 : 0;
     case QB_OPT_INFO_BATCH_ELL: return h->bat.ell;
+    case QB_OPT_LATENCY_EVENTS: return h->opt_latency_events;
+    case QB_OPT_LATENCY_GRAPH: return h->opt_latency_graph;
+    case QB_OPT_INFO_LAST_EVENT_NS: return static_cast<int64_t>(h->last_event_ns);
     case QB_OPT_BATCH_CTAS_PER_SM: return h->opt_batch_ctas;
     default: return -1;
   }
@@ -1470,7 +1544,10 @@ qb_status qb_latency_run(qb_decoder* h, const uint64_t* pool, uint64_t pool_size
         wall_ns[k] = static_cast<uint64_t>(
             std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count());
       }
-      if (kernel_ns) kernel_ns[k] = h->last_kernel_ns;
+      if (kernel_ns) {
+        kernel_ns[k] = h->opt_latency_events && h->opt_latency_io == 1 ? h->last_event_ns
+                                                                       : h->last_kernel_ns;
+      }
       unsigned char c = 1;
       uint64_t it = 0;
       for (uint32_t s = 0; s < P.nseg; ++s) {

@@ -2,7 +2,9 @@
 import argparse, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
-from paper_2508_07879_b200 import Decoder, DecoderConfig, codes, gf2
+from paper_2508_07879_b200 import Decoder, DecoderConfig, codes, gf2, _lib
+if os.environ.get("QB_LIB"):  # A/B runs of differently built libraries (dev only)
+    _lib.LIB_PATH = os.path.abspath(os.environ["QB_LIB"])
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--code", default="bb784")
