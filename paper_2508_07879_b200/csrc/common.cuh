@@ -14,6 +14,7 @@ namespace qb {
 
 constexpr int kMaxSegments = 8;
 constexpr int kWarp = 32;
+constexpr uint32_t kNoAbsorb = 0xffu;
 constexpr uint32_t kPadEdges = 8;  // message slots of the dummy check (regular kernel)
 
 struct SegmentDev {
@@ -63,6 +64,11 @@ struct DecodeParams {
   const uint32_t* edge_var;    // [E]
   const uint32_t* edge_check;  // [E]
   const void* gamma;           // [N] float (float/half modes) or int32 (int modes)
+  // degree-padded kernel (kernel_ell.cuh): variables a thread updates, and the degree-1
+  // variables ABSORBED by their check (updated by the check's thread)
+  const uint32_t* ell_vars;    // [N]: segment s lists its ell_nvars[s] own variables from index segs[s].v0
+  const uint32_t* ell_abs;     // [M]: slot of the absorbed variable in check m's block, or kNoAbsorb
+  uint32_t ell_nvars[kMaxSegments];
   SegmentDev segs[kMaxSegments];
 };
 

@@ -19,6 +19,13 @@
 //    degree-1 variable keeps q = gamma (decoder.cpp:324-329): its single store is
 //    predicated off in the floating-point modes, where (gamma + r) - r need not
 //    equal gamma;
+//  * a degree-1 variable whose check has no other one is ABSORBED by that check: its
+//    message q = gamma never changes (it sits in the check's block for the life of the
+//    CTA), and its posterior gamma + r and hard decision are evaluated by the check's
+//    thread right after it has produced r - the variable costs no slot on the
+//    variable side at all.  On the phenomenological graphs [H | I] this removes a third
+//    of the variables (one measurement-error variable per check) from the variable
+//    stage and a third of the per-thread offset registers;
 //  * thread <-> node assignment, byte offsets of every slot and the priors live
 //    in registers for the life of the persistent CTA, exactly as in the (6,3)
 //    lean kernel (kernel_lean.cuh), whose item loop, counter-based stop test and
@@ -188,6 +195,18 @@ __device__ __forceinline__ void cn_ell(const DecodeParams& P, ArithI32, unsigned
   cn_ell_int<ArithI32, DC>(P, blk, syn_bit);
 }
 
+// ---- hard decision of an absorbed degree-1 variable: gamma + r < 0 in the mode's arithmetic
+__device__ __forceinline__ uint32_t absorbed_decision(ArithF32, float q, float r) {
+  return (static_cast<double>(q) + static_cast<double>(r)) < 0.0 ? 1u : 0u;  // decoder.cpp:319-323
+}
+__device__ __forceinline__ uint32_t absorbed_decision(ArithF16, __half q, __half r) {
+  return h_neg(__hadd(q, r)) ? 1u : 0u;
+}
+template <class A>
+__device__ __forceinline__ uint32_t absorbed_decision(A, int32_t q, int32_t r) {
+  return static_cast<uint32_t>(q + r) >> 31;
+}
+
 // ---- variable update over DV padded slots; returns 1 iff the variable decides 1 ----
 // `keep0`: the variable has degree 1, so its only real message stays gamma.
 
@@ -311,13 +330,17 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
 
   // ---- per-thread tables
   uint32_t eo[VPT][DV], co[CPT], cl[CPT], valid = 0, keep0 = 0;
+  uint32_t absorb = 0;  // byte k: slot of the variable absorbed by this thread's k-th check, or kNoAbsorb
+  static_assert(CPT <= 4, "absorbed slots are packed one byte per check");
   Gam gam[VPT];
+  const uint32_t nv = P.ell_nvars[s];  // variables updated on the variable side
   {
     const Gam* __restrict__ gamma = static_cast<const Gam*>(P.gamma);
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
-      const uint32_t n = seg.v0 + tid + k * T;
-      const bool ok = n < seg.v1;
+      const uint32_t idx = tid + k * T;
+      const bool ok = idx < nv;
+      const uint32_t n = ok ? P.ell_vars[seg.v0 + idx] : 0u;
       const uint32_t b = ok ? P.var_off[n] : 0u;
       const uint32_t deg = ok ? P.var_off[n + 1] - b : 0u;
       valid |= (ok ? 1u : 0u) << k;
@@ -340,14 +363,22 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
       const bool ok = m < Ms;
       cl[k] = ok ? m : Ms;  // dummy check: bit Ms of the bitmap, always 0
       co[k] = (ok ? m : P.seg_mmax) * kStride;
+      uint32_t aslot = kNoAbsorb;
       if (ok) {  // sentinels of the padded slots: written once, never overwritten
-        const uint32_t deg = P.check_off[seg.c0 + m + 1] - P.check_off[seg.c0 + m];
+        const uint32_t e0 = P.check_off[seg.c0 + m];
+        const uint32_t deg = P.check_off[seg.c0 + m + 1] - e0;
         const Msg sent = deg == 1u ? EllSentinel<A>::deg1(P) : EllSentinel<A>::pad(P);
 #pragma unroll
         for (int j = 0; j < DC; ++j) {
           if (static_cast<uint32_t>(j) >= deg) *reinterpret_cast<Msg*>(msgs + co[k] + j * kMsg) = sent;
         }
+        aslot = P.ell_abs[seg.c0 + m];
+        if (aslot != kNoAbsorb) {  // the absorbed variable's message: its prior, for ever
+          *reinterpret_cast<Msg*>(msgs + co[k] + aslot * kMsg) =
+              prior_as_msg<A>(gamma[P.edge_var[e0 + aslot]]);
+        }
       }
+      absorb |= aslot << (8 * k);
     }
   }
 
@@ -399,7 +430,7 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
 #pragma unroll
       for (int i = 0; i < DV; ++i) *reinterpret_cast<Msg*>(msgs + eo[k][i]) = init;
     }
-    uint32_t eprev = 0;
+    uint32_t eprev = 0, aprev = 0;  // decisions of this thread's variables / absorbed variables
     __syncthreads();
 
     uint32_t synbits = 0;
@@ -416,8 +447,24 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
     for (;;) {
       ++iter;
       uint32_t eb = 0;
+      int32_t adelta = 0;
 #pragma unroll
-      for (int k = 0; k < CPT; ++k) cn_ell<DC>(P, A{}, msgs + co[k], (synbits >> k) & 1u);
+      for (int k = 0; k < CPT; ++k) {
+        cn_ell<DC>(P, A{}, msgs + co[k], (synbits >> k) & 1u);
+        const uint32_t aslot = (absorb >> (8 * k)) & 0xffu;
+        if (aslot != kNoAbsorb) {  // posterior of the absorbed variable from the r just produced
+          const unsigned char* slot = msgs + co[k] + aslot * kMsg;
+          const uint32_t e = absorbed_decision(A{}, *reinterpret_cast<const Msg*>(slot),
+                                               *reinterpret_cast<const Msg*>(slot + DC * kMsg));
+          if (e != ((aprev >> k) & 1u)) {  // it flips the parity of its one check
+            aprev ^= 1u << k;
+            const uint32_t bit = 1u << (cl[k] & 31u);
+            const uint32_t old = atomicXor(&par[cl[k] >> 5], bit);
+            adelta += (old & bit) ? -1 : 1;
+          }
+        }
+      }
+      if (adelta) atomicAdd(const_cast<uint32_t*>(unsat), static_cast<uint32_t>(adelta));
       __syncthreads();
 #pragma unroll
       for (int k = 0; k < VPT; ++k) {
@@ -466,12 +513,20 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
         }
       }
     }
-    if (eprev) {
+    if (eprev | aprev) {
       uint32_t* est_g = io.est + shot * P.est_w32;
 #pragma unroll
       for (int k = 0; k < VPT; ++k) {
         if ((eprev >> k) & 1u) {
-          const uint32_t n = seg.v0 + tid + k * T;
+          const uint32_t n = P.ell_vars[seg.v0 + tid + k * T];
+          atomicOr(&est_g[n >> 5], 1u << (n & 31u));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        if ((aprev >> k) & 1u) {
+          const uint32_t n =
+              P.edge_var[P.check_off[seg.c0 + cl[k]] + ((absorb >> (8 * k)) & 0xffu)];
           atomicOr(&est_g[n >> 5], 1u << (n & 31u));
         }
       }

@@ -456,7 +456,8 @@ struct EllVariant {
 };
 constexpr EllVariant kEllVariants[] = {
     {4, 2, 1, 2, 1024},   // e.g. the toy 3x6 fixture, repetition / surface-like checks
-    {7, 3, 3, 8, 192},    // [H | I] extension of a (6,3)-regular code (phenomenological noise)
+    {7, 3, 3, 5, 192},    // [H | I] extension of a (6,3)-regular code (phenomenological noise):
+                          // the identity columns are absorbed by their checks
     {8, 4, 2, 4, 512},
     {12, 6, 1, 2, 1024},
 };
@@ -466,7 +467,7 @@ template <class A>
 KernelFn ell_kernel_t(int idx) {
   switch (idx) {
     case 0: return decode_ell_kernel<A, 4, 2, 1, 2, 1024, 1>;
-    case 1: return decode_ell_kernel<A, 7, 3, 3, 8, 192, 4>;
+    case 1: return decode_ell_kernel<A, 7, 3, 3, 5, 192, 5>;
     case 2: return decode_ell_kernel<A, 8, 4, 2, 4, 512, 2>;
     default: return decode_ell_kernel<A, 12, 6, 1, 2, 1024, 1>;
   }
@@ -546,7 +547,13 @@ void make_plans(qb_decoder* h) {
       for (int idx = 0; idx < kNumEllVariants; ++idx) {
         const EllVariant& ev = kEllVariants[idx];
         if (h->max_dc > static_cast<uint32_t>(ev.dc) || h->max_dv > static_cast<uint32_t>(ev.dv)) continue;
-        const uint32_t T = regular_group_threads(P, ev.cpt, ev.vpt);
+        uint32_t want = 32;  // threads so that T * cpt covers the checks, T * vpt the own variables
+        for (uint32_t k = 0; k < P.nseg; ++k) {
+          const uint32_t ms = P.segs[k].c1 - P.segs[k].c0;
+          want = std::max(want, std::max((ms + ev.cpt - 1) / ev.cpt,
+                                         (P.ell_nvars[k] + ev.vpt - 1) / ev.vpt));
+        }
+        const uint32_t T = round_up32(want);
         if (T > static_cast<uint32_t>(ev.maxt)) continue;
         const size_t smem = ell_smem_bytes(P.seg_mmax, ell_msg_bytes(h->arith),
                                            static_cast<uint32_t>(ev.dc));
@@ -1354,6 +1361,32 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
       for (uint32_t n = 0; n < N; ++n) {
         h->max_dv = std::max(h->max_dv, graph->var_offsets[n + 1] - graph->var_offsets[n]);
       }
+    }
+    {
+      // degree-padded kernel: every check absorbs its first degree-1 variable (that variable
+      // is then updated by the check's thread); the others are listed per segment
+      std::vector<uint32_t> abs_slot(M, kNoAbsorb), vars(N, 0);
+      std::vector<uint8_t> absorbed(N, 0);
+      for (uint32_t m = 0; m < M; ++m) {
+        const uint32_t e0 = graph->check_offsets[m], e1 = graph->check_offsets[m + 1];
+        for (uint32_t e = e0; e < e1 && e - e0 < kNoAbsorb; ++e) {
+          const uint32_t v = graph->edge_var[e];
+          if (graph->var_offsets[v + 1] - graph->var_offsets[v] == 1) {
+            abs_slot[m] = e - e0;
+            absorbed[v] = 1;
+            break;
+          }
+        }
+      }
+      for (uint32_t k = 0; k < P.nseg; ++k) {
+        uint32_t cnt = 0;
+        for (uint32_t v = P.segs[k].v0; v < P.segs[k].v1; ++v) {
+          if (!absorbed[v]) vars[P.segs[k].v0 + cnt++] = v;
+        }
+        P.ell_nvars[k] = cnt;
+      }
+      P.ell_vars = keep(dev_upload(vars));
+      P.ell_abs = keep(dev_upload(abs_slot));
     }
     make_plans(h);
 
