@@ -408,6 +408,7 @@ def measure_variants(args, code, d_syn, d_est, d_conv, d_its, stream):
                 eu = float(d_its[:shots].to(torch.int64).sum().item()) * (edges // 2)
                 out[f"{arith}_{label}"] = {"decodes_per_s": shots / ms * 1e3,
                                            "edge_updates_per_s": eu / ms * 1e3,
+                                           "smem_bytes_per_s": eu / ms * 1e3 * BYTES_PER_EDGE_UPDATE[arith],
                                            "two_shots_per_thread": bool(dec.get_option(10))}
     # ---- config 5: extended graph, per-variable priors, int8 (and float for comparison)
     pq = 0.005
@@ -507,6 +508,22 @@ def measure_latency(args, code, lib, d_syn):
                     out[f"{label}_{io_name}"].update(
                         {"cuda_event_p50": nearest_rank(ev, 50), "cuda_event_p99": nearest_rank(ev, 99),
                          "cuda_event_mean": float(np.mean(ev))})
+    # config 3 also names the reduced-precision path: same protocol, doorbell and launch-per-shot
+    for arith in ("half", "int8"):
+        if arith == args.arithmetic:
+            continue
+        cfg = DecoderConfig(max_iterations=10, early_termination=False, arithmetic=arith)
+        with Decoder(code, cfg) as dec:
+            for io_mode, io_name in ((2, "doorbell"), (0, "mapped")):
+                dec.set_option(1, io_mode)
+                wall, kern, digest = dec.latency_run(pool, 300, args.latency_shots)
+                wall = np.sort(wall.astype(np.float64) * 1e-3)
+                kern = np.sort(kern.astype(np.float64) * 1e-3)
+                out[f"{arith}_fixed10_{io_name}"] = {
+                    "p50": nearest_rank(wall, 50), "p99": nearest_rank(wall, 99),
+                    "mean": float(np.mean(wall)), "kernel_p50": nearest_rank(kern, 50),
+                    "kernel_p99": nearest_rank(kern, 99), "shots": args.latency_shots,
+                    "digest": "%016x" % digest}
     out["note"] = ("wall = host steady_clock around the whole qb_decode (copy-in, launch, "
                    "completion, copy-out) inside qb_latency_run; kernel = in-kernel %globaltimer "
                    "span; doorbell = persistent cluster polling mapped host memory (no launch per "

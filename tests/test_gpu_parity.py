@@ -507,3 +507,31 @@ def test_tma_tiles_ragged_tail_and_unaligned_buffers(oracle, mode):
             torch.cuda.synchronize()
             assert np.array_equal(d_est.cpu().numpy().view(np.uint64), outs[0][0][:n2]), (opt, val)
             assert np.array_equal(d_res.cpu().numpy().view(np.uint64), outs[0][1][:n2]), (opt, val)
+
+
+def test_memcpy_protocol_graph_and_event_timing(oracle):
+    """Single shots through the paper's protocol (H2D copy, kernel, D2H copy): as one
+    CUDA-graph launch (default) and as three stream operations, results identical to the
+    oracle; with QB_OPT_LATENCY_EVENTS the CUDA-event span of the protocol is reported."""
+    OPT_LATENCY_EVENTS, OPT_LATENCY_GRAPH, INFO_LAST_EVENT_NS = 11, 12, 108
+    code = codes.make_code("bb784")
+    g = code.combined_graph
+    rng = np.random.default_rng(4)
+    _, _, syn = error_syndromes(code, rng, 40, 0.02)
+    cfg = DecoderConfig(max_iterations=10, early_termination=False)
+    with Decoder(code, cfg) as dec:
+        dec.set_option(OPT_LATENCY_IO, 1)
+        for graph in (1, 0, 1):
+            dec.set_option(OPT_LATENCY_GRAPH, graph)
+            assert dec.get_option(OPT_LATENCY_GRAPH) == graph
+            launches = dec.launch_count()
+            assert_matches_oracle(oracle, g, cfg, syn, code.segments, dec=dec)
+            assert dec.launch_count() - launches == len(syn)
+        dec.set_option(OPT_LATENCY_EVENTS, 1)
+        wall, ev, _ = dec.latency_run(syn.view(np.uint64), 5, 50)
+        assert dec.get_option(INFO_LAST_EVENT_NS) > 0
+        # device span of copy + kernel + copy: above the kernel alone, below the host wall clock
+        assert 2_000 < np.median(ev) <= np.median(wall) < 1_000_000
+        dec.set_option(OPT_LATENCY_EVENTS, 0)
+        _, kern, _ = dec.latency_run(syn.view(np.uint64), 5, 50)
+        assert np.median(kern) < np.median(ev)
