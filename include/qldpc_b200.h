@@ -132,6 +132,10 @@ typedef enum {
    * and D2H copy are ONE CUDA-graph launch per decode (captured on first use);
    * 0 = three separate stream operations. */
   QB_OPT_LATENCY_GRAPH = 12,
+  /* Lean batch kernel: shots per syndrome tile (one TMA bulk copy and one queue
+   * ticket per tile), 1 .. 16; 0 = auto (16 for large batches, smaller when that
+   * would leave resident CTAs without work). */
+  QB_OPT_BATCH_TILE = 13,
   /* Read-only (qb_get_option): the launch plans actually in use. */
   QB_OPT_INFO_BATCH_CTAS_PER_SM = 100,
   QB_OPT_INFO_BATCH_BLOCK = 101,

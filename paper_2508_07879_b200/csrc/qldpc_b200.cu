@@ -13,7 +13,6 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
-#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -25,6 +24,7 @@
 #include "kernel_lean.cuh"
 #include "kernel_lean_h2.cuh"
 #include "kernel_ell.cuh"
+#include "kernel_ell_h2.cuh"
 #include "kernel_noise.cuh"
 #include "kernel_bw.cuh"
 #include "kernel_classify.cuh"
@@ -163,6 +163,7 @@ struct qb_decoder {
   uint64_t last_event_ns = 0;
   // memcpy protocol as ONE CUDA-graph launch (H2D copy -> cluster kernel -> D2H copy); two
   // instantiated graphs with different record tags alternate, so a stale record is detected
+  int64_t opt_batch_tile = 0;  // shots per TMA syndrome tile, 0 = auto
   int64_t opt_latency_graph = 1;
   cudaGraphExec_t lat_graph[2] = {nullptr, nullptr};
   uint32_t lat_graph_flip = 0;
@@ -484,6 +485,19 @@ KernelFn ell_kernel(int arith, int idx) {
 }
 uint32_t ell_msg_bytes(int arith) { return arith == QB_ARITH_HALF ? 2u : 4u; }
 
+// two shots per thread on packed fp16 instructions (kernel_ell_h2.cuh): half mode, and int8
+// mode when the loader has verified the fp16 form of the Q16 scaling
+constexpr int kEllH2MaxT[] = {1024, 160, 512, 1024};
+template <bool kI8>
+KernelFn ell_h2_kernel_t(int idx) {
+  switch (idx) {
+    case 0: return decode_ell_h2_kernel<4, 2, 1, 2, 1024, 1, kI8>;
+    case 1: return decode_ell_h2_kernel<7, 3, 3, 5, 160, 4, kI8>;
+    case 2: return decode_ell_h2_kernel<8, 4, 2, 4, 512, 1, kI8>;
+    default: return decode_ell_h2_kernel<12, 6, 1, 2, 1024, 1, kI8>;
+  }
+}
+
 uint32_t round_up32(uint32_t x) { return (x + 31u) & ~31u; }
 
 // Threads per segment group so that T*cpt covers the checks and T*vpt the
@@ -501,7 +515,8 @@ uint32_t regular_group_threads(const DecodeParams& P, uint32_t cpt, uint32_t vpt
 void finish_plan(qb_decoder* h, LaunchPlan& pl) {
   pl.block = pl.cluster ? pl.group_threads : pl.ngroups * pl.group_threads;
   if (pl.items) pl.block = pl.group_threads;
-  pl.smem = pl.ell    ? ell_smem_bytes(h->P.seg_mmax, ell_msg_bytes(h->arith),
+  pl.smem = pl.ell && pl.pair ? ell_h2_smem_bytes(h->P.seg_mmax, static_cast<uint32_t>(pl.ell / 100))
+            : pl.ell  ? ell_smem_bytes(h->P.seg_mmax, ell_msg_bytes(h->arith),
                                        static_cast<uint32_t>(pl.ell / 100))
             : pl.pair ? lean_h2_smem_bytes(h->P.seg_mmax)
             : pl.lean ? h->smem_lean
@@ -554,16 +569,22 @@ void make_plans(qb_decoder* h) {
                                          (P.ell_nvars[k] + ev.vpt - 1) / ev.vpt));
         }
         const uint32_t T = round_up32(want);
+        const bool pair = (h->arith == QB_ARITH_HALF || (h->arith == QB_ARITH_INT8 && h->i8_pair_ok)) &&
+                          h->opt_batch_pair != 0 && T <= static_cast<uint32_t>(kEllH2MaxT[idx]);
         if (T > static_cast<uint32_t>(ev.maxt)) continue;
-        const size_t smem = ell_smem_bytes(P.seg_mmax, ell_msg_bytes(h->arith),
-                                           static_cast<uint32_t>(ev.dc));
+        const size_t smem = pair ? ell_h2_smem_bytes(P.seg_mmax, static_cast<uint32_t>(ev.dc))
+                                 : ell_smem_bytes(P.seg_mmax, ell_msg_bytes(h->arith),
+                                                  static_cast<uint32_t>(ev.dc));
         if (smem > static_cast<size_t>(h->max_smem_optin)) continue;
         LaunchPlan pl{};
         pl.items = true;
         pl.lean = true;
+        pl.pair = pair;
         pl.ell = 100 * ev.dc + ev.dv;
-        pl.kernel = ell_kernel(h->arith, idx);
-        pl.name = "decode_ell_kernel";
+        pl.kernel = !pair                       ? ell_kernel(h->arith, idx)
+                    : h->arith == QB_ARITH_INT8 ? ell_h2_kernel_t<true>(idx)
+                                                : ell_h2_kernel_t<false>(idx);
+        pl.name = pair ? "decode_ell_h2_kernel" : "decode_ell_kernel";
         pl.ngroups = 1;
         pl.group_threads = T;
         finish_plan(h, pl);
@@ -720,7 +741,7 @@ uint64_t resident_ctas(qb_decoder* h) {
 uint32_t batch_tile(qb_decoder* h, uint64_t shots) {
   if (!(h->bat.lean && !h->bat.pair && !h->bat.ell)) return 1;
   const uint64_t per_seg = std::max<uint64_t>(1, resident_ctas(h) / h->P.nseg);
-  if (const char* e = std::getenv("QB_TILE")) return static_cast<uint32_t>(std::atoi(e));
+  if (h->opt_batch_tile > 0) return static_cast<uint32_t>(h->opt_batch_tile);
   for (uint32_t k = kMaxTile; k > 1; k >>= 1) {
     if ((shots + k - 1) / k >= 4 * per_seg) return k;
   }
@@ -1453,6 +1474,12 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
         if (value < 0 || value > 2) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_SHAPE: 0, 1 or 2");
         h->opt_batch_shape = value;
         break;
+      case QB_OPT_BATCH_TILE:
+        if (value < 0 || value > static_cast<int64_t>(kMaxTile)) {
+          fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_TILE: 0 .. 16");
+        }
+        h->opt_batch_tile = value;
+        return;
       case QB_OPT_LATENCY_GRAPH:
         if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_LATENCY_GRAPH: 0 or 1");
         h->opt_latency_graph = value;
@@ -1528,6 +1555,7 @@ int64_t qb_get_option(const qb_decoder* h, int option) {
     case QB_OPT_INFO_BATCH_ELL: return h->bat.ell;
     case QB_OPT_LATENCY_EVENTS: return h->opt_latency_events;
     case QB_OPT_LATENCY_GRAPH: return h->opt_latency_graph;
+    case QB_OPT_BATCH_TILE: return h->opt_batch_tile;
     case QB_OPT_INFO_LAST_EVENT_NS: return static_cast<int64_t>(h->last_event_ns);
     case QB_OPT_BATCH_CTAS_PER_SM: return h->opt_batch_ctas;
     default: return -1;

@@ -184,3 +184,37 @@ def test_soundness_at_scale():
     assert np.array_equal(conv[:, 0] == 1, ~bits_all[:, :mz].any(axis=1))
     assert np.array_equal(conv[:, 1] == 1, ~bits_all[:, mz:].any(axis=1))
     assert conv.mean() > 0.5
+
+
+@pytest.mark.parametrize("mode", ["int8", "half"])
+def test_packed_pairs_on_irregular_graphs(oracle, mode):
+    """decode_ell_h2_kernel (two shots per thread on packed fp16 instructions): equal to the
+    one-shot-per-thread degree-padded kernel and to the generic CSR kernel on the same
+    handle; in int8 mode also to the integer oracle (decoder.cpp:260-283).  Odd shot counts
+    exercise the half-empty last pair; the graphs have degree-0 / degree-1 nodes."""
+    OPT_HALF_PAIRS = 10
+    rng = np.random.default_rng(77)
+    graphs = [codes.build_tanner_graph(_degree_zero_graph())]
+    for _ in range(5):
+        graphs.append(codes.build_tanner_graph(
+            random_ldpc_matrix(rng, 20 + int(rng.integers(0, 60)), 40 + int(rng.integers(0, 80)))))
+    paired = 0
+    for gi, g in enumerate(graphs):
+        priors = rng.uniform(0.2, 12.0, g.num_vars) * rng.choice([-1.0, 1.0], g.num_vars, p=[0.1, 0.9])
+        for early in (True, False):
+            cfg = DecoderConfig(max_iterations=11, early_termination=early, arithmetic=mode,
+                                priors=priors.tolist(), alpha=0.8 if gi % 2 else 0.625)
+            syn = random_syndromes(rng, 333, g.num_checks, 0.2)
+            with Decoder(g, cfg) as dec:
+                if not dec.get_option(OPT_INFO_ELL):
+                    continue
+                paired += dec.get_option(OPT_HALF_PAIRS)
+                a = _batch(dec, syn)
+                dec.set_option(OPT_HALF_PAIRS, 0)
+                assert dec.get_option(OPT_HALF_PAIRS) == 0 and dec.get_option(OPT_INFO_ELL)
+                assert _same(a, _batch(dec, syn)), "pairs vs one shot per thread"
+                dec.set_option(OPT_KERNEL, 1)
+                assert _same(a, _batch(dec, syn)), "pairs vs generic"
+            if mode == "int8":
+                assert _same(a, oracle.decode_many(g, cfg, syn, None)), "pairs vs oracle"
+    assert paired >= 6, "the packed kernel was not selected"

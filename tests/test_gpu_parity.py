@@ -481,6 +481,18 @@ def test_tma_tiles_ragged_tail_and_unaligned_buffers(oracle, mode):
             outs.append((d_est.cpu().numpy().view(np.uint64), d_res.cpu().numpy().view(np.uint64),
                          d_conv.cpu().numpy(), d_its.cpu().numpy().astype(np.uint32)))
     assert all(np.array_equal(a, b) for a, b in zip(outs[0], outs[1])), "aligned vs unaligned"
+    # every tile size gives the same bits (QB_OPT_BATCH_TILE = 13)
+    with Decoder(code, cfg) as dec:
+        for tile in (1, 2, 5, 16):
+            dec.set_option(13, tile)
+            d_est = torch.full((shots, ew), -1, dtype=torch.int64, device="cuda")
+            d_conv = torch.zeros((shots, 2), dtype=torch.uint8, device="cuda")
+            d_its = torch.zeros((shots, 2), dtype=torch.int32, device="cuda")
+            dec.decode_batch_device(shots, d_aligned.data_ptr(), d_est.data_ptr(), None,
+                                    d_conv.data_ptr(), d_its.data_ptr(), stream)
+            torch.cuda.synchronize()
+            assert np.array_equal(d_est.cpu().numpy().view(np.uint64), outs[0][0]), tile
+            assert np.array_equal(d_its.cpu().numpy().astype(np.uint32), outs[0][3]), tile
     for sl in (slice(0, 200), slice(shots - 200, shots)):
         oe, ores, oc, oi = oracle.decode_many(g, cfg, syn[sl], code.segments)
         assert np.array_equal(outs[0][0][sl], oe) and np.array_equal(outs[0][1][sl], ores)
