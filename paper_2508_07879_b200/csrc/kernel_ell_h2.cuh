@@ -37,7 +37,7 @@ __device__ __forceinline__ void cn_ell_h2(const DecodeParams& P, unsigned char* 
 #pragma unroll
   for (int j = 0; j < DC; ++j) {
     u[j] = qp[j];
-    a[j] = u2h2(u[j] & 0x7fff7fffu);
+    a[j] = __habs2(u2h2(u[j]));  // folds into the consumers as |x|
   }
   __half2 m1 = __hmin2(a[0], a[1]), m2 = __hmax2(a[0], a[1]);
 #pragma unroll
@@ -46,15 +46,17 @@ __device__ __forceinline__ void cn_ell_h2(const DecodeParams& P, unsigned char* 
     m1 = __hmin2(m1, a[j]);
   }
   const __half2 alpha = __half2half2(__ushort_as_half(P.alpha_h));
-  const uint32_t s1 = h22u(h2_scale<kI8>(alpha, m1)), s2 = h22u(h2_scale<kI8>(alpha, m2));
+  // both scaled minima carry the sign common to all edges; edge j flips by its own incoming sign
   uint32_t sx = syn_pair;
 #pragma unroll
   for (int j = 0; j < DC; ++j) sx ^= u[j];
+  sx &= 0x80008000u;
+  const uint32_t s1 = h22u(h2_scale<kI8>(alpha, m1)) ^ sx, s2 = h22u(h2_scale<kI8>(alpha, m2)) ^ sx;
   uint32_t* rp = reinterpret_cast<uint32_t*>(blk + DC * 4);
 #pragma unroll
   for (int j = 0; j < DC; ++j) {
     const uint32_t eq = __heq2_mask(a[j], m1);  // 0xffff in each lane whose magnitude is the minimum
-    rp[j] = ((s2 & eq) | (s1 & ~eq)) | ((sx ^ u[j]) & 0x80008000u);
+    rp[j] = ((s2 & eq) | (s1 & ~eq)) ^ (u[j] & 0x80008000u);
   }
 }
 

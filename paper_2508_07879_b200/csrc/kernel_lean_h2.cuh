@@ -90,17 +90,20 @@ __device__ __forceinline__ void cn6_h2(const DecodeParams& P, unsigned char* blk
   }
   __half2 a[6];
 #pragma unroll
-  for (int j = 0; j < 6; ++j) a[j] = u2h2(u[j] & 0x7fff7fffu);
+  for (int j = 0; j < 6; ++j) a[j] = __habs2(u2h2(u[j]));  // folds into the consumers as |x|
   __half2 m1, m2;
   two_smallest6_h2(a, m1, m2);
   const __half2 alpha = __half2half2(__ushort_as_half(P.alpha_h));
-  const uint32_t s1 = h22u(h2_scale<kI8>(alpha, m1)), s2 = h22u(h2_scale<kI8>(alpha, m2));
-  const uint32_t sx = u[0] ^ u[1] ^ u[2] ^ u[3] ^ u[4] ^ u[5] ^ syn_pair;
+  // both scaled minima carry the sign common to all edges (syndrome and the parity of every
+  // incoming sign); edge j then only flips by its own incoming sign
+  const uint32_t sx =
+      (u[0] ^ u[1] ^ u[2] ^ u[3] ^ u[4] ^ u[5] ^ syn_pair) & 0x80008000u;
+  const uint32_t s1 = h22u(h2_scale<kI8>(alpha, m1)) ^ sx, s2 = h22u(h2_scale<kI8>(alpha, m2)) ^ sx;
   uint32_t o[6];
 #pragma unroll
   for (int j = 0; j < 6; ++j) {
     const uint32_t eq = __heq2_mask(a[j], m1);  // 0xffff in each lane whose magnitude is the minimum
-    o[j] = ((s2 & eq) | (s1 & ~eq)) | ((sx ^ u[j]) & 0x80008000u);
+    o[j] = ((s2 & eq) | (s1 & ~eq)) ^ (u[j] & 0x80008000u);
   }
   uint2* rp = reinterpret_cast<uint2*>(blk + kH2ROff);
 #pragma unroll
