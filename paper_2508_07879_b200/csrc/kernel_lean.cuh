@@ -79,19 +79,21 @@ __device__ __forceinline__ void cn6_block(const DecodeParams& P, ArithF32, unsig
   const float m1 = fminf(fminf(l0, l1), l2);
   const float med = fmaxf(fminf(l0, l1), fminf(fmaxf(l0, l1), l2));
   const float m2 = fminf(med, fminf(fminf(h0, h1), h2));
-  // float(alpha * |min|): fp64 product, one rounding (decoder.cpp:302-307)
-  const uint32_t s1 = __float_as_uint(static_cast<float>(P.alpha * static_cast<double>(m1)));
-  const uint32_t s2 = __float_as_uint(static_cast<float>(P.alpha * static_cast<double>(m2)));
+  // float(alpha * |min|): fp64 product, one rounding (decoder.cpp:302-307).  Both carry the
+  // sign common to all edges (syndrome, parity of every incoming sign); edge j then only
+  // flips by its own incoming sign.
   uint32_t sx = syn_bit << 31;
 #pragma unroll
   for (int j = 0; j < 6; ++j) sx ^= __float_as_uint(v[j]);
+  sx &= 0x80000000u;
+  const uint32_t s1 = __float_as_uint(static_cast<float>(P.alpha * static_cast<double>(m1))) ^ sx;
+  const uint32_t s2 = __float_as_uint(static_cast<float>(P.alpha * static_cast<double>(m2))) ^ sx;
   float2* rp = reinterpret_cast<float2*>(blk + Lay<ArithF32>::kROff);
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
-    const uint32_t ox = (fabsf(v[2 * j]) == m1 ? s2 : s1) |
-                        ((sx ^ __float_as_uint(v[2 * j])) & 0x80000000u);
-    const uint32_t oy = (fabsf(v[2 * j + 1]) == m1 ? s2 : s1) |
-                        ((sx ^ __float_as_uint(v[2 * j + 1])) & 0x80000000u);
+    const uint32_t ox = (fabsf(v[2 * j]) == m1 ? s2 : s1) ^ (__float_as_uint(v[2 * j]) & 0x80000000u);
+    const uint32_t oy =
+        (fabsf(v[2 * j + 1]) == m1 ? s2 : s1) ^ (__float_as_uint(v[2 * j + 1]) & 0x80000000u);
     rp[j] = make_float2(__uint_as_float(ox), __uint_as_float(oy));
   }
 }
