@@ -296,14 +296,16 @@ decode_ell_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_consta
       if (ad_a) atomicAdd(const_cast<uint32_t*>(unsat_a), static_cast<uint32_t>(ad_a));
       if (ad_b) atomicAdd(const_cast<uint32_t*>(unsat_b), static_cast<uint32_t>(ad_b));
       __syncthreads();
-      uint32_t eb_a = 0, eb_b = 0;
+      // posterior sign bits (bits 15 / 31) shift into one accumulator: after VPT variables
+      // shot a's decisions sit in bits [16-VPT, 15], shot b's in [32-VPT, 31]
+      static_assert(VPT <= 8, "decision accumulator");
+      uint32_t acc = 0;
 #pragma unroll
       for (int k = 0; k < VPT; ++k) {
-        const uint32_t sg =
-            vn_ell_h2<DC, DV, kI8>(msgs, eo[k], __half2half2(gam[k]), (keep0 >> k) & 1u);
-        eb_a |= ((sg >> 15) & 1u) << k;
-        eb_b |= (sg >> 31) << k;
+        acc = (acc >> 1) |
+              vn_ell_h2<DC, DV, kI8>(msgs, eo[k], __half2half2(gam[k]), (keep0 >> k) & 1u);
       }
+      uint32_t eb_a = (acc >> (16 - VPT)) & ((1u << VPT) - 1u), eb_b = acc >> (32 - VPT);
       eb_a &= valid;
       eb_b &= valid;
       auto toggle = [&](uint32_t changed, uint32_t* par, volatile uint32_t* ctr) {

@@ -308,15 +308,16 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
     uint32_t fin_a = 0, fin_b = 0;  // decisions of each shot at the moment it stopped
     for (;;) {
       ++iter;
-      uint32_t eb_a = 0, eb_b = 0;
+      // posterior sign bits of the pair (bits 15 / 31) are shifted into one accumulator:
+      // after VPT variables, shot a's decisions sit in bits [16-VPT, 15], shot b's in [32-VPT, 31]
+      static_assert(VPT <= 8, "decision accumulator");
+      uint32_t acc = 0;
       if (kFast && iter == 1u) {
         const __half2 g2 = __half2half2(__ushort_as_half(P.gamma_hb));
 #pragma unroll
         for (int k = 0; k < VPT; ++k) {
           // syndrome bits from the untouched copies: no barrier before the toggles
-          const uint32_t sg = vn3_first_h2<kI8>(P, msgs, eo[k], syn_a, syn_b, g2);
-          eb_a |= ((sg >> 15) & 1u) << k;
-          eb_b |= (sg >> 31) << k;
+          acc = (acc >> 1) | vn3_first_h2<kI8>(P, msgs, eo[k], syn_a, syn_b, g2);
         }
       } else {
 #pragma unroll
@@ -326,11 +327,10 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
         for (int k = 0; k < VPT; ++k) {
           const __half2 g2 = kFast ? __half2half2(__ushort_as_half(P.gamma_hb))
                                    : __half2half2(h2_prior<kI8>(gam[k]));
-          const uint32_t sg = vn3_h2<kI8>(msgs, eo[k], g2);
-          eb_a |= ((sg >> 15) & 1u) << k;
-          eb_b |= (sg >> 31) << k;
+          acc = (acc >> 1) | vn3_h2<kI8>(msgs, eo[k], g2);
         }
       }
+      uint32_t eb_a = (acc >> (16 - VPT)) & ((1u << VPT) - 1u), eb_b = acc >> (32 - VPT);
       eb_a &= valid;
       eb_b &= valid;
       auto toggle = [&](uint32_t changed, uint32_t* par, volatile uint32_t* ctr) {
