@@ -78,6 +78,14 @@ __device__ __forceinline__ __half2 h2_scale(__half2 alpha, __half2 m) {
 }
 
 // syn_pair: bit 15 = syndrome bit of the low-half shot, bit 31 = of the high-half shot
+// The packed kernels are bound by the ALU pipe (min/max, compares, bit logic), while the
+// FMA pipe idles.  So the check update computes each edge's "minimum of the OTHER five
+// magnitudes" directly (nine two/three-input minima: no second-minimum network, no
+// compare-and-select) and applies scale and sign with multiplications: edge j's output is
+// e_j * (+-alpha), the sign being the syndrome, the parity of all incoming signs and
+// edge j's own sign.  e_j is m1 or m2 of the scalar formulation and a product's magnitude
+// does not depend on the sign of its factors, so the bits are those of
+// "select alpha*m1 / alpha*m2, then set the sign".
 template <bool kI8>
 __device__ __forceinline__ void cn6_h2(const DecodeParams& P, unsigned char* blk, uint32_t syn_pair) {
   const uint2* qp = reinterpret_cast<const uint2*>(blk);
@@ -91,19 +99,29 @@ __device__ __forceinline__ void cn6_h2(const DecodeParams& P, unsigned char* blk
   __half2 a[6];
 #pragma unroll
   for (int j = 0; j < 6; ++j) a[j] = __habs2(u2h2(u[j]));  // folds into the consumers as |x|
-  __half2 m1, m2;
-  two_smallest6_h2(a, m1, m2);
-  const __half2 alpha = __half2half2(__ushort_as_half(P.alpha_h));
-  // both scaled minima carry the sign common to all edges (syndrome and the parity of every
-  // incoming sign); edge j then only flips by its own incoming sign
-  const uint32_t sx =
-      (u[0] ^ u[1] ^ u[2] ^ u[3] ^ u[4] ^ u[5] ^ syn_pair) & 0x80008000u;
-  const uint32_t s1 = h22u(h2_scale<kI8>(alpha, m1)) ^ sx, s2 = h22u(h2_scale<kI8>(alpha, m2)) ^ sx;
+  const __half2 pa = __hmin2(a[0], a[1]), pb = __hmin2(a[2], a[3]), pc = __hmin2(a[4], a[5]);
+  __half2 e[6];
+  e[0] = __hmin2(__hmin2(a[1], pb), pc);
+  e[1] = __hmin2(__hmin2(a[0], pb), pc);
+  e[2] = __hmin2(__hmin2(a[3], pa), pc);
+  e[3] = __hmin2(__hmin2(a[2], pa), pc);
+  e[4] = __hmin2(__hmin2(a[5], pa), pb);
+  e[5] = __hmin2(__hmin2(a[4], pa), pb);
+  const uint32_t sx = (u[0] ^ u[1] ^ u[2] ^ u[3] ^ u[4] ^ u[5] ^ syn_pair) & 0x80008000u;
   uint32_t o[6];
+  if constexpr (kI8) {
+    const __half2 c2 = __half2half2(__ushort_as_half(P.alpha_h));
+    const __half2 magic = __half2half2(__ushort_as_half(0x6600));  // 1536
+    const uint32_t one = sx ^ 0x3c003c00u;                         // +-1 with the common sign
 #pragma unroll
-  for (int j = 0; j < 6; ++j) {
-    const uint32_t eq = __heq2_mask(a[j], m1);  // 0xffff in each lane whose magnitude is the minimum
-    o[j] = ((s2 & eq) | (s1 & ~eq)) ^ (u[j] & 0x80008000u);
+    for (int j = 0; j < 6; ++j) {
+      const __half2 t = __hsub2(__hfma2(e[j], c2, magic), magic);  // exact Q16 scaling
+      o[j] = h22u(__hmul2(t, u2h2(one ^ (u[j] & 0x80008000u))));
+    }
+  } else {
+    const uint32_t al = sx ^ (static_cast<uint32_t>(P.alpha_h) * 0x00010001u);  // +-alpha
+#pragma unroll
+    for (int j = 0; j < 6; ++j) o[j] = h22u(__hmul2(e[j], u2h2(al ^ (u[j] & 0x80008000u))));
   }
   uint2* rp = reinterpret_cast<uint2*>(blk + kH2ROff);
 #pragma unroll
