@@ -28,9 +28,11 @@ __host__ __device__ inline size_t ell_h2_smem_bytes(uint32_t seg_mmax, uint32_t 
   return msg + 4 * (8 * static_cast<size_t>(ell_pw(seg_mmax)) + 16);
 }
 
-// check update over one padded block of half2 slots
+// check update over one padded block of half2 slots: per-edge minimum of the OTHER
+// magnitudes from prefix / suffix minima, scale and sign by multiplication (see cn6_h2)
 template <int DC, bool kI8>
 __device__ __forceinline__ void cn_ell_h2(const DecodeParams& P, unsigned char* blk, uint32_t syn_pair) {
+  static_assert(DC >= 3, "prefix / suffix minima");
   const uint32_t* qp = reinterpret_cast<const uint32_t*>(blk);
   uint32_t u[DC];
   __half2 a[DC];
@@ -39,24 +41,30 @@ __device__ __forceinline__ void cn_ell_h2(const DecodeParams& P, unsigned char* 
     u[j] = qp[j];
     a[j] = __habs2(u2h2(u[j]));  // folds into the consumers as |x|
   }
-  __half2 m1 = __hmin2(a[0], a[1]), m2 = __hmax2(a[0], a[1]);
+  __half2 pre[DC], suf[DC];  // pre[j] = min(a[0..j]), suf[j] = min(a[j..DC-1])
+  pre[0] = a[0];
 #pragma unroll
-  for (int j = 2; j < DC; ++j) {
-    m2 = __hmin2(m2, __hmax2(m1, a[j]));
-    m1 = __hmin2(m1, a[j]);
-  }
-  const __half2 alpha = __half2half2(__ushort_as_half(P.alpha_h));
-  // both scaled minima carry the sign common to all edges; edge j flips by its own incoming sign
+  for (int j = 1; j < DC - 1; ++j) pre[j] = __hmin2(pre[j - 1], a[j]);
+  suf[DC - 1] = a[DC - 1];
+#pragma unroll
+  for (int j = DC - 2; j > 0; --j) suf[j] = __hmin2(suf[j + 1], a[j]);
   uint32_t sx = syn_pair;
 #pragma unroll
   for (int j = 0; j < DC; ++j) sx ^= u[j];
   sx &= 0x80008000u;
-  const uint32_t s1 = h22u(h2_scale<kI8>(alpha, m1)) ^ sx, s2 = h22u(h2_scale<kI8>(alpha, m2)) ^ sx;
   uint32_t* rp = reinterpret_cast<uint32_t*>(blk + DC * 4);
+  const __half2 c2 = __half2half2(__ushort_as_half(P.alpha_h));
+  const __half2 magic = __half2half2(__ushort_as_half(0x6600));  // 1536
+  const uint32_t sgn = sx ^ (kI8 ? 0x3c003c00u : static_cast<uint32_t>(P.alpha_h) * 0x00010001u);
 #pragma unroll
   for (int j = 0; j < DC; ++j) {
-    const uint32_t eq = __heq2_mask(a[j], m1);  // 0xffff in each lane whose magnitude is the minimum
-    rp[j] = ((s2 & eq) | (s1 & ~eq)) ^ (u[j] & 0x80008000u);
+    const __half2 e = j == 0 ? suf[1] : j == DC - 1 ? pre[DC - 2] : __hmin2(pre[j - 1], suf[j + 1]);
+    const __half2 f = u2h2(sgn ^ (u[j] & 0x80008000u));  // +-1 (int8) or +-alpha (half)
+    if constexpr (kI8) {
+      rp[j] = h22u(__hmul2(__hsub2(__hfma2(e, c2, magic), magic), f));  // exact Q16 scaling, sign
+    } else {
+      rp[j] = h22u(__hmul2(e, f));
+    }
   }
 }
 
