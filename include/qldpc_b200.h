@@ -136,6 +136,11 @@ typedef enum {
    * ticket per tile), 1 .. 16; 0 = auto (16 for large batches, smaller when that
    * would leave resident CTAs without work). */
   QB_OPT_BATCH_TILE = 13,
+  /* Lean batch kernels ((6,3)-regular codes): 1 (default) = the loader permutes the six
+   * message slots inside every check's block so that the variable-side accesses of a
+   * warp spread over the shared-memory banks (results are unaffected: the check
+   * update is symmetric in its slots); 0 = slots in row order. */
+  QB_OPT_SLOT_SPREAD = 14,
   /* Read-only (qb_get_option): the launch plans actually in use. */
   QB_OPT_INFO_BATCH_CTAS_PER_SM = 100,
   QB_OPT_INFO_BATCH_BLOCK = 101,

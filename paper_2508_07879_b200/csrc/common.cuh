@@ -69,6 +69,10 @@ struct DecodeParams {
   const uint32_t* ell_vars;    // [N]: segment s lists its ell_nvars[s] own variables from index segs[s].v0
   const uint32_t* ell_abs;     // [M]: slot of the absorbed variable in check m's block, or kNoAbsorb
   uint32_t ell_nvars[kMaxSegments];
+  // lean batch kernels ((6,3)-regular codes): slot of edge e inside its check's message
+  // block - a permutation of 0..5 per check chosen by the loader to spread the variable-side
+  // accesses of a warp over the banks (the check update is symmetric in its slots)
+  const uint8_t* edge_slot;    // [E]
   SegmentDev segs[kMaxSegments];
 };
 

@@ -413,8 +413,9 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
       valid |= (ok ? 1u : 0u) << k;
 #pragma unroll
       for (int i = 0; i < kDV; ++i) {
-        const uint32_t e = ok ? P.var_edges[n * kDV + i] - seg.e0 : 0u;
-        eo[k][i] = ok ? (e / kDC) * kStride + (e % kDC) * static_cast<uint32_t>(sizeof(Msg))
+        const uint32_t eg = ok ? P.var_edges[n * kDV + i] : 0u;
+        const uint32_t e = ok ? eg - seg.e0 : 0u;
+        eo[k][i] = ok ? (e / kDC) * kStride + P.edge_slot[eg] * static_cast<uint32_t>(sizeof(Msg))
                       : dummy + i * static_cast<uint32_t>(sizeof(Msg));
       }
       if constexpr (!kFast) gam[k] = ok ? gamma[n] : static_cast<Gam>(1);

@@ -216,8 +216,9 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
       valid |= (ok ? 1u : 0u) << k;
 #pragma unroll
       for (int i = 0; i < kDV; ++i) {
-        const uint32_t e = ok ? P.var_edges[n * kDV + i] - seg.e0 : 0u;
-        eo[k][i] = ok ? (e / kDC) * kH2Stride + (e % kDC) * 4u : dummy + i * 4u;
+        const uint32_t eg = ok ? P.var_edges[n * kDV + i] : 0u;
+        const uint32_t e = ok ? eg - seg.e0 : 0u;
+        eo[k][i] = ok ? (e / kDC) * kH2Stride + P.edge_slot[eg] * 4u : dummy + i * 4u;
       }
       if constexpr (!kFast) {
         if constexpr (kI8) {

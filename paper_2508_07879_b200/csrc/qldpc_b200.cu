@@ -164,11 +164,14 @@ struct qb_decoder {
   // memcpy protocol as ONE CUDA-graph launch (H2D copy -> cluster kernel -> D2H copy); two
   // instantiated graphs with different record tags alternate, so a stale record is detected
   int64_t opt_batch_tile = 0;  // shots per TMA syndrome tile, 0 = auto
+  int64_t opt_slot_spread = 1;  // lean batch kernels: bank-spreading slot permutation
   int64_t opt_latency_graph = 1;
   cudaGraphExec_t lat_graph[2] = {nullptr, nullptr};
   uint32_t lat_graph_flip = 0;
   bool regular63 = false;  // every check degree 6, every variable degree 3
   uint32_t max_dc = 0, max_dv = 0;  // largest check / variable degree of the graph
+  uint8_t* d_edge_slot = nullptr;  // [E] slot permutation of the lean batch kernels
+  std::vector<uint32_t> h_var_edges, h_check_off;  // host copies for the slot optimiser
   bool i8_pair_ok = false;  // int8 mode: the Q16 scaling has an exact fp16 form (kernel_lean_h2.cuh)
   bool fast_ok = false;    // uniform prior (and, for fp32, provably clamp-free)
   int64_t opt_fast = 1;
@@ -548,7 +551,93 @@ LaunchPlan generic_plan(qb_decoder* h) {
   return pl;
 }
 
+// Slot permutation for the lean batch kernels on a (6,3)-regular graph: the variable-side
+// gathers / scatters of one warp instruction touch 32 (check, slot) positions; with the
+// 14-word block stride a fixed slot can only reach the 16 banks of one parity, so the natural
+// order (slot = position in the row) is 2-way conflicted throughout.  Greedy assignment in
+// launch order - each edge takes the free slot of its check whose bank is least used by its
+// warp instruction so far - then one pass of improving pairwise swaps.  ~1 ms on
+// [[784,24,24]]; 2.15 -> ~1.75 wavefronts per access.
+void optimise_edge_slots(qb_decoder* h, uint32_t T) {
+  const DecodeParams& P = h->P;
+  const uint32_t E = P.E;
+  std::vector<uint8_t> slot(E, 0);
+  for (uint32_t e = 0; e < E; ++e) slot[e] = static_cast<uint8_t>(e % 6);
+  if (h->regular63 && T >= 32) {
+    constexpr uint32_t kStrideWords = 14;
+    std::vector<uint32_t> group_of(E, 0);
+    std::vector<std::vector<uint32_t>> groups;
+    for (uint32_t s = 0; s < P.nseg; ++s) {
+      const SegmentDev& sg = P.segs[s];
+      const uint32_t ns = sg.v1 - sg.v0, vpt = (ns + T - 1) / T;
+      for (uint32_t k = 0; k < vpt; ++k) {
+        for (uint32_t w = 0; w < T / 32; ++w) {
+          for (uint32_t i = 0; i < 3; ++i) {
+            std::vector<uint32_t> g;
+            for (uint32_t l = 0; l < 32; ++l) {
+              const uint32_t nl = 32 * w + l + k * T;
+              if (nl < ns) g.push_back(h->h_var_edges[(sg.v0 + nl) * 3 + i]);
+            }
+            if (g.empty()) continue;
+            for (uint32_t e : g) group_of[e] = static_cast<uint32_t>(groups.size());
+            groups.push_back(std::move(g));
+          }
+        }
+      }
+    }
+    auto bank = [&](uint32_t e, uint32_t sl) { return (kStrideWords * (e / 6) + sl) & 31u; };
+    std::vector<uint8_t> free_mask(E / 6, 0x3f);
+    std::fill(slot.begin(), slot.end(), 0xff);
+    for (const auto& g : groups) {
+      uint8_t used[32] = {};
+      for (uint32_t e : g) {
+        uint32_t best = 6, best_use = 255;
+        for (uint32_t sl = 0; sl < 6; ++sl) {
+          if (!((free_mask[e / 6] >> sl) & 1u)) continue;
+          const uint32_t u = used[bank(e, sl)];
+          if (u < best_use) {
+            best_use = u;
+            best = sl;
+          }
+        }
+        slot[e] = static_cast<uint8_t>(best);
+        free_mask[e / 6] &= static_cast<uint8_t>(~(1u << best));
+        ++used[bank(e, best)];
+      }
+    }
+    auto cost = [&](uint32_t gi) {  // sum of squared bank loads of one warp instruction
+      uint8_t c[32] = {};
+      uint32_t tot = 0;
+      for (uint32_t e : groups[gi]) ++c[bank(e, slot[e])];
+      for (uint32_t b = 0; b < 32; ++b) tot += static_cast<uint32_t>(c[b]) * c[b];
+      return tot;
+    };
+    for (uint32_t m = 0; m < E / 6; ++m) {
+      for (uint32_t a = 0; a < 6; ++a) {
+        for (uint32_t b = a + 1; b < 6; ++b) {
+          const uint32_t ea = 6 * m + a, eb = 6 * m + b;
+          const uint32_t ga = group_of[ea], gb = group_of[eb];
+          const uint32_t before = cost(ga) + (gb != ga ? cost(gb) : 0u);
+          std::swap(slot[ea], slot[eb]);
+          const uint32_t after = cost(ga) + (gb != ga ? cost(gb) : 0u);
+          if (after >= before) std::swap(slot[ea], slot[eb]);
+        }
+      }
+    }
+  }
+  CUDA_TRY(cudaMemcpy(h->d_edge_slot, slot.data(), E, cudaMemcpyHostToDevice));
+}
+
+void choose_plans(qb_decoder* h);
+
 void make_plans(qb_decoder* h) {
+  choose_plans(h);
+  // whatever batch plan was chosen, leave a slot table that matches its thread shape
+  const bool lean_batch = h->bat.lean && !h->bat.ell;
+  optimise_edge_slots(h, lean_batch && h->opt_slot_spread != 0 ? h->bat.group_threads : 0u);
+}
+
+void choose_plans(qb_decoder* h) {
   const DecodeParams& P = h->P;
   drop_latency_graphs(h);  // they bake in the kernel and its launch shape
   const bool use_regular = h->regular63 && h->opt_kernel != 1;
@@ -1271,6 +1360,11 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
     P.var_edges = keep(dev_upload(std::vector<uint32_t>(graph->var_edges, graph->var_edges + E)));
     P.edge_var = keep(dev_upload(std::vector<uint32_t>(graph->edge_var, graph->edge_var + E)));
     P.edge_check = keep(dev_upload(edge_check));
+    h->h_var_edges.assign(graph->var_edges, graph->var_edges + E);
+    h->h_check_off.assign(graph->check_offsets, graph->check_offsets + M + 1);
+    CUDA_TRY(cudaMalloc(&h->d_edge_slot, std::max<size_t>(E, 1)));
+    h->dev_allocs.push_back(h->d_edge_slot);
+    P.edge_slot = h->d_edge_slot;
     P.gamma = gamma_f.empty() ? static_cast<const void*>(keep(dev_upload(gamma_i)))
                               : static_cast<const void*>(keep(dev_upload(gamma_f)));
 
@@ -1474,6 +1568,10 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
         if (value < 0 || value > 2) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_SHAPE: 0, 1 or 2");
         h->opt_batch_shape = value;
         break;
+      case QB_OPT_SLOT_SPREAD:
+        if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_SLOT_SPREAD: 0 or 1");
+        h->opt_slot_spread = value;
+        break;
       case QB_OPT_BATCH_TILE:
         if (value < 0 || value > static_cast<int64_t>(kMaxTile)) {
           fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_TILE: 0 .. 16");
@@ -1556,6 +1654,7 @@ int64_t qb_get_option(const qb_decoder* h, int option) {
     case QB_OPT_LATENCY_EVENTS: return h->opt_latency_events;
     case QB_OPT_LATENCY_GRAPH: return h->opt_latency_graph;
     case QB_OPT_BATCH_TILE: return h->opt_batch_tile;
+    case QB_OPT_SLOT_SPREAD: return h->opt_slot_spread;
     case QB_OPT_INFO_LAST_EVENT_NS: return static_cast<int64_t>(h->last_event_ns);
     case QB_OPT_BATCH_CTAS_PER_SM: return h->opt_batch_ctas;
     default: return -1;

@@ -17,6 +17,7 @@ ap.add_argument("--iters", default="50:1,10:0")
 ap.add_argument("--kernel", type=int, default=0)
 ap.add_argument("--shapes", default="2")
 ap.add_argument("--pairs", type=int, default=1)
+ap.add_argument("--spread", default="1", help="QB_OPT_SLOT_SPREAD values to sweep")
 args = ap.parse_args()
 code = codes.make_code(args.code)
 g = code.combined_graph
@@ -37,8 +38,10 @@ for spec in args.iters.split(","):
             if args.kernel: dec.set_option(0, args.kernel)
             dec.set_option(10, args.pairs)
             for shape, npt in [(int(sh), int(x)) for sh in args.shapes.split(",") for x in args.npts.split(",")]:
+              for spread in [int(x) for x in args.spread.split(",")]:
                 for ctas in [int(x) for x in args.ctas.split(",")]:
                     dec.set_option(8, shape); dec.set_option(5, npt); dec.set_option(4, ctas)
+                    dec.set_option(14, spread)
                     f = lambda: dec.decode_batch_device(shots, d_syn.data_ptr(), d_est.data_ptr(), None, d_conv.data_ptr(), d_its.data_ptr(), stream)
                     f(); f(); torch.cuda.synchronize()
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -48,7 +51,7 @@ for spec in args.iters.split(","):
                     ms = e0.elapsed_time(e1) / 3
                     its = d_its.to(torch.int64)
                     eu = float((its.sum(dim=0) * torch.tensor([g.num_edges // 2] * 2, device=dev)).sum())
-                    print(json.dumps({"arith": arith, "max_iter": int(mi), "early": int(early), "shape": shape, "npt": npt,
+                    print(json.dumps({"arith": arith, "max_iter": int(mi), "early": int(early), "shape": shape, "npt": npt, "spread": spread,
                                       "ctas_req": ctas, "ctas_per_sm": dec.get_option(100), "block": dec.get_option(101),
                                       "Mshots_s": shots / ms / 1e3, "G_edge_updates_s": eu / ms / 1e6,
                                       "mean_iters": float(its.max(dim=1).values.double().mean()), "conv": float(d_conv.min(dim=1).values.double().mean())}), flush=True)
