@@ -13,8 +13,19 @@
 // of qubit v - n) uses draw 2(v - n) + 1.  Because SplitMix64 is counter-based,
 // every bit of every shot is generated independently: one warp per shot, 32
 // variables per step, errors packed with __ballot_sync straight into the
-// Gf2Vector word layout; the syndrome is then one XOR-gather per check.
+// Gf2Vector word layout.
+//
+// Two things keep it cheap without changing a bit of the stream:
+//  * `unit < p` with unit = k * 2^-53 (k = draw >> 11, an integer below 2^53) is the
+//    INTEGER comparison k < ceil(p * 2^53): p * 2^53 is exact in fp64, and for an
+//    integer k, k < x <=> k < ceil(x).  The host precomputes the threshold(s); no
+//    64-bit integer -> fp64 conversion and no fp64 compare per draw;
+//  * the syndrome H e is accumulated SPARSELY: only a flipped variable (1 in 1/p)
+//    XORs its column - its few checks - into the warp's syndrome words in shared
+//    memory, instead of every check gathering all of its variables.
 #pragma once
+
+#include <cmath>
 
 #include "common.cuh"
 
@@ -24,13 +35,20 @@ struct NoiseParams {
   uint64_t seed;
   uint64_t first_trial;
   uint64_t nshots;
-  double p;            // uniform flip probability (used when probs == nullptr)
-  const double* probs; // optional per-variable probabilities [N]
+  uint64_t thr;            // ceil(p * 2^53): flip iff (draw >> 11) < thr (when thrs == nullptr)
+  const uint64_t* thrs;    // optional per-variable thresholds [N]
   uint32_t mode;       // 0: variable v uses draw v; 1: CSS independent-xz interleave
   uint32_t n_qubits;   // mode 1: variables [0,n) are X errors, [n,2n) Z errors
   uint32_t* syn;       // [nshots][syn_w32] out
   uint32_t* err;       // [nshots][est_w32] out, may be nullptr
 };
+
+// ceil(p * 2^53) for p in [0, 1] (host)
+inline uint64_t noise_threshold(double p) {
+  if (!(p > 0.0)) return 0;
+  if (p >= 1.0) return 1ull << 53;
+  return static_cast<uint64_t>(std::ceil(std::ldexp(p, 53)));
+}
 
 constexpr uint64_t kPhi = 0x9E3779B97F4A7C15ull;
 
@@ -42,44 +60,45 @@ __host__ __device__ __forceinline__ uint64_t splitmix_mix(uint64_t z) {
 
 constexpr int kNoiseWarps = 8;
 
+// kCss: CSS independent-xz interleave (NoiseParams::mode 1); kPerVar: per-variable thresholds
+template <bool kCss, bool kPerVar>
 __global__ void __launch_bounds__(kNoiseWarps * 32)
 noise_syndrome_kernel(const __grid_constant__ DecodeParams P, const __grid_constant__ NoiseParams np) {
-  extern __shared__ uint32_t noise_smem[];  // [kNoiseWarps][est_w32]
+  extern __shared__ uint32_t noise_smem[];  // [kNoiseWarps][syn_w32 + est_w32]
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  uint32_t* ebits = noise_smem + warp * P.est_w32;
+  uint32_t* sbits = noise_smem + warp * (P.syn_w32 + P.est_w32);
+  uint32_t* ebits = sbits + P.syn_w32;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kNoiseWarps;
+  const uint32_t N = P.N, nq = np.n_qubits, steps = P.est_w32;
+  const uint64_t thr = np.thr;
   for (uint64_t shot = static_cast<uint64_t>(blockIdx.x) * kNoiseWarps + warp; shot < np.nshots;
        shot += stride) {
     const uint64_t trial = np.first_trial + shot;
     const uint64_t state0 = splitmix_mix(np.seed + kPhi * trial + kPhi);
-    for (uint32_t vb = 0; vb < P.est_w32 * 32u; vb += 32u) {
-      const uint32_t v = vb + lane;
-      bool bit = false;
-      if (v < P.N) {
-        uint64_t j = v;
-        if (np.mode == 1u) j = v < np.n_qubits ? 2ull * v : 2ull * (v - np.n_qubits) + 1ull;
-        const uint64_t z = splitmix_mix(state0 + (j + 1ull) * kPhi);
-        const double unit = static_cast<double>(z >> 11) * 0x1.0p-53;
-        bit = unit < (np.probs ? np.probs[v] : np.p);
-      }
+    for (uint32_t w = lane; w < P.syn_w32; w += 32u) sbits[w] = 0u;
+    __syncwarp();
+#pragma unroll 2
+    for (uint32_t step = 0; step < steps; ++step) {
+      const uint32_t v = step * 32u + lane;
+      uint32_t j = v;  // draw index of variable v
+      if constexpr (kCss) j = v < nq ? 2u * v : 2u * (v - nq) + 1u;
+      const uint64_t z = splitmix_mix(state0 + static_cast<uint64_t>(j + 1u) * kPhi);
+      uint64_t t = thr;
+      if constexpr (kPerVar) t = v < N ? np.thrs[v] : 0ull;
+      const bool bit = v < N && (z >> 11) < t;
       const uint32_t word = __ballot_sync(0xffffffffu, bit);
-      if (lane == 0) {
-        ebits[vb >> 5] = word;
-        if (np.err) np.err[shot * P.est_w32 + (vb >> 5)] = word;
+      if (lane == 0) ebits[step] = word;
+      if (bit) {  // XOR this variable's column of H into the syndrome
+        for (uint32_t i = P.var_off[v]; i < P.var_off[v + 1]; ++i) {
+          const uint32_t m = P.edge_check[P.var_edges[i]];
+          atomicXor(&sbits[m >> 5], 1u << (m & 31u));
+        }
       }
     }
     __syncwarp();
-    for (uint32_t mb = 0; mb < P.syn_w32 * 32u; mb += 32u) {
-      const uint32_t m = mb + lane;
-      uint32_t parity = 0;
-      if (m < P.M) {
-        for (uint32_t e = P.check_off[m]; e < P.check_off[m + 1]; ++e) {
-          const uint32_t v = P.edge_var[e];
-          parity ^= (ebits[v >> 5] >> (v & 31u)) & 1u;
-        }
-      }
-      const uint32_t word = __ballot_sync(0xffffffffu, parity != 0u);
-      if (lane == 0) np.syn[shot * P.syn_w32 + (mb >> 5)] = word;
+    for (uint32_t w = lane; w < P.syn_w32; w += 32u) np.syn[shot * P.syn_w32 + w] = sbits[w];
+    if (np.err) {
+      for (uint32_t w = lane; w < P.est_w32; w += 32u) np.err[shot * P.est_w32 + w] = ebits[w];
     }
     __syncwarp();
   }

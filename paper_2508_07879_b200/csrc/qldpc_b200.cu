@@ -135,7 +135,7 @@ struct qb_decoder {
   uint8_t* b_conv = nullptr;
   // debug dumps
   void *d_qdump = nullptr, *d_rdump = nullptr;
-  double* d_probs = nullptr;  // per-variable flip probabilities of the noise generator
+  uint64_t* d_probs = nullptr;  // per-variable flip thresholds of the noise generator
   // campaign state
   uint32_t *d_tests_x = nullptr, *d_tests_z = nullptr;
   uint32_t n_tests_x = 0, n_tests_z = 0;
@@ -1771,14 +1771,20 @@ qb_status qb_generate_syndromes(qb_decoder* h, uint64_t seed, double p, const do
     np.seed = seed;
     np.first_trial = first_trial;
     np.nshots = shots;
-    np.p = p;
     if (probs) {
-      for (uint32_t v = 0; v < P.N; ++v) check_p(probs[v]);
-      if (!h->d_probs) CUDA_TRY(cudaMalloc(&h->d_probs, sizeof(double) * P.N));
-      CUDA_TRY(cudaMemcpyAsync(h->d_probs, probs, sizeof(double) * P.N, cudaMemcpyHostToDevice, st));
-      np.probs = h->d_probs;
+      std::vector<uint64_t> thr(P.N);
+      for (uint32_t v = 0; v < P.N; ++v) {
+        check_p(probs[v]);
+        thr[v] = noise_threshold(probs[v]);
+      }
+      if (!h->d_probs) CUDA_TRY(cudaMalloc(&h->d_probs, sizeof(uint64_t) * P.N));
+      // synchronous: `thr` is a local
+      CUDA_TRY(cudaStreamSynchronize(st));
+      CUDA_TRY(cudaMemcpy(h->d_probs, thr.data(), sizeof(uint64_t) * P.N, cudaMemcpyHostToDevice));
+      np.thrs = h->d_probs;
     } else {
       check_p(p);
+      np.thr = noise_threshold(p);
     }
     np.mode = css_interleave ? 1u : 0u;
     if (css_interleave) {
@@ -1793,8 +1799,10 @@ qb_status qb_generate_syndromes(qb_decoder* h, uint64_t seed, double p, const do
     const uint64_t blocks_needed = (shots + kNoiseWarps - 1) / kNoiseWarps;
     const unsigned grid = static_cast<unsigned>(
         std::min<uint64_t>(blocks_needed, static_cast<uint64_t>(h->sm_count) * 8));
-    const size_t smem = static_cast<size_t>(kNoiseWarps) * P.est_w32 * 4;
-    noise_syndrome_kernel<<<grid, kNoiseWarps * 32, smem, st>>>(P, np);
+    const size_t smem = static_cast<size_t>(kNoiseWarps) * (P.syn_w32 + P.est_w32) * 4;
+    auto* kern = np.mode ? (np.thrs ? noise_syndrome_kernel<true, true> : noise_syndrome_kernel<true, false>)
+                         : (np.thrs ? noise_syndrome_kernel<false, true> : noise_syndrome_kernel<false, false>);
+    kern<<<grid, kNoiseWarps * 32, smem, st>>>(P, np);
     CUDA_TRY(cudaGetLastError());
     ++h->launches;
   });
