@@ -49,7 +49,7 @@ def parse_args():
     ap.add_argument("--no-early-stop", action="store_true")
     ap.add_argument("--arithmetic", default="float")
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--latency-shots", type=int, default=4000)
+    ap.add_argument("--latency-shots", type=int, default=10000)
     ap.add_argument("--skip-latency", action="store_true")
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
