@@ -18,6 +18,7 @@ ap.add_argument("--kernel", type=int, default=0)
 ap.add_argument("--shapes", default="2")
 ap.add_argument("--pairs", type=int, default=1)
 ap.add_argument("--spread", default="1", help="QB_OPT_SLOT_SPREAD values to sweep")
+ap.add_argument("--priors", type=int, default=0, help="1: per-variable LLR priors (general path)")
 args = ap.parse_args()
 code = codes.make_code(args.code)
 g = code.combined_graph
@@ -32,7 +33,10 @@ stream = torch.cuda.current_stream().cuda_stream
 for spec in args.iters.split(","):
     mi, early = spec.split(":")
     for arith in args.ariths.split(","):
-        cfg = DecoderConfig(max_iterations=int(mi), early_termination=bool(int(early)), arithmetic=arith)
+        pri = None
+        if args.priors:
+            pri = (np.log((1 - args.p) / args.p) * (1.0 + 0.1 * np.random.default_rng(5).random(g.num_vars))).tolist()
+        cfg = DecoderConfig(max_iterations=int(mi), early_termination=bool(int(early)), arithmetic=arith, priors=pri)
         with Decoder(code, cfg) as dec:
             dec.generate_syndromes(1, args.p, shots, d_syn.data_ptr(), None, stream=stream)
             if args.kernel: dec.set_option(0, args.kernel)
