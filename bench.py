@@ -54,6 +54,7 @@ def parse_args():
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-variants", action="store_true")
+    ap.add_argument("--e2e-chunk", type=int, default=0, help="QB_OPT_BATCH_CHUNK for the e2e leg (0 = auto)")
     ap.add_argument("--ref-shots", type=int, default=1 << 14,
                     help="--impl reference: shots per step (bounded sample)")
     return ap.parse_args()
@@ -465,6 +466,8 @@ def measure_e2e(args, dec, lib, d_syn, shots, sw, ew, nseg):
         return p
 
     n = shots
+    if args.e2e_chunk:
+        dec.set_option(15, args.e2e_chunk)
     h_syn, h_est = pinned(n * sw * 8), pinned(n * ew * 8)
     h_conv, h_its = pinned(n * nseg), pinned(n * nseg * 4)
     # stage the same synthetic batch on the host (outside the timed region)

@@ -141,6 +141,9 @@ typedef enum {
    * warp spread over the shared-memory banks (results are unaffected: the check
    * update is symmetric in its slots); 0 = slots in row order. */
   QB_OPT_SLOT_SPREAD = 14,
+  /* qb_decode_batch (host buffers): shots per pipeline chunk (H2D copy, kernel and D2H
+   * copy of consecutive chunks overlap on three streams); 0 = auto. */
+  QB_OPT_BATCH_CHUNK = 15,
   /* Read-only (qb_get_option): the launch plans actually in use. */
   QB_OPT_INFO_BATCH_CTAS_PER_SM = 100,
   QB_OPT_INFO_BATCH_BLOCK = 101,

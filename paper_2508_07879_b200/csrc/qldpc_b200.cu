@@ -164,6 +164,7 @@ struct qb_decoder {
   // memcpy protocol as ONE CUDA-graph launch (H2D copy -> cluster kernel -> D2H copy); two
   // instantiated graphs with different record tags alternate, so a stale record is detected
   int64_t opt_batch_tile = 0;  // shots per TMA syndrome tile, 0 = auto
+  int64_t opt_batch_chunk = 0;  // qb_decode_batch: shots per pipeline chunk, 0 = auto (2^15)
   int64_t opt_slot_spread = 1;  // lean batch kernels: bank-spreading slot permutation
   int64_t opt_latency_graph = 1;
   cudaGraphExec_t lat_graph[2] = {nullptr, nullptr};
@@ -1580,6 +1581,10 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
         if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_SLOT_SPREAD: 0 or 1");
         h->opt_slot_spread = value;
         break;
+      case QB_OPT_BATCH_CHUNK:
+        if (value < 0) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_CHUNK: >= 0");
+        h->opt_batch_chunk = value;
+        return;
       case QB_OPT_BATCH_TILE:
         if (value < 0 || value > static_cast<int64_t>(kMaxTile)) {
           fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_TILE: 0 .. 16");
@@ -1662,6 +1667,7 @@ int64_t qb_get_option(const qb_decoder* h, int option) {
     case QB_OPT_LATENCY_EVENTS: return h->opt_latency_events;
     case QB_OPT_LATENCY_GRAPH: return h->opt_latency_graph;
     case QB_OPT_BATCH_TILE: return h->opt_batch_tile;
+    case QB_OPT_BATCH_CHUNK: return h->opt_batch_chunk;
     case QB_OPT_SLOT_SPREAD: return h->opt_slot_spread;
     case QB_OPT_INFO_LAST_EVENT_NS: return static_cast<int64_t>(h->last_event_ns);
     case QB_OPT_BATCH_CTAS_PER_SM: return h->opt_batch_ctas;
@@ -1945,8 +1951,9 @@ qb_status qb_decode_batch(qb_decoder* h, uint64_t shots, const uint64_t* syndrom
     // scheduler words, so that with pinned host buffers the H2D copy of chunk i+1,
     // the kernel of chunk i and the D2H copy of chunk i-1 run concurrently (one
     // copy engine per direction).
-    const uint64_t kMaxChunk = 1ull << 17;
-    const uint64_t chunk = std::min<uint64_t>(shots, kMaxChunk);
+    const uint64_t max_chunk = h->opt_batch_chunk > 0 ? static_cast<uint64_t>(h->opt_batch_chunk) & ~1ull
+                                                      : (1ull << 15);  // measured: 103.6 M/s at 2^15, 102.6 at 2^16, 99.3 at 2^17
+    const uint64_t chunk = std::min<uint64_t>(shots, std::max<uint64_t>(max_chunk, 2));
     ensure_batch(h, chunk * kPipeSlots, residuals != nullptr);
     bool used[kPipeSlots] = {};
     uint64_t done = 0;
