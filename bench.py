@@ -55,7 +55,7 @@ def parse_args():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-variants", action="store_true")
     ap.add_argument("--e2e-chunk", type=int, default=0, help="QB_OPT_BATCH_CHUNK for the e2e leg (0 = auto)")
-    ap.add_argument("--ref-shots", type=int, default=1 << 14,
+    ap.add_argument("--ref-shots", type=int, default=1 << 18,
                     help="--impl reference: shots per step (bounded sample)")
     return ap.parse_args()
 
@@ -373,7 +373,7 @@ def run_ours(args):
         line["variants"] = measure_variants(args, code, d_syn, d_est, d_conv, d_its, stream)
     if world == 1 and not args.skip_cpu_baseline:
         try:
-            _, _, base = reference_throughput(args, 4096, 40, 2)
+            _, _, base = reference_throughput(args, 1 << 16, 40, 2)  # ~10-15 s of CPU work
             line["cpu_baseline"] = base
         except Exception as exc:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "unit": "decodes/s", "cores": 0,
