@@ -326,6 +326,7 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
   const uint32_t zero_off = (P.seg_mmax + 1) * kStride;  // r half stays zero for ever
 
   // both dummy blocks start out as zeros (before any sentinel / q store)
+  const uint64_t t_entry = io.kernel_ns ? globaltimer_ns() : 0ull;  // single-shot use only
   for (uint32_t b = tid; b < 2 * kStride; b += T) msgs[scratch_off + b] = 0;
 
   // ---- per-thread tables
@@ -544,6 +545,8 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
     const unsigned int done = atomicAdd(&io.sched[1], 1u);
     if (done == gridDim.x - 1) {
       for (uint32_t k = 0; k < 2 + kMaxSegments; ++k) io.sched[k] = 0;
+      // single shot: the CTA that finishes last reports its own entry-to-exit span
+      if (io.kernel_ns) *io.kernel_ns = globaltimer_ns() - t_entry;
       __threadfence();
     }
   }

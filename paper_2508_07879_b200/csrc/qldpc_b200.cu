@@ -177,6 +177,7 @@ struct qb_decoder {
   bool fast_ok = false;    // uniform prior (and, for fp32, provably clamp-free)
   int64_t opt_fast = 1;
   LaunchPlan lat, bat;
+  LaunchPlan lat_ell;  // single shots on irregular graphs: degree-padded kernel (kernel == nullptr: none)
 
   uint64_t launches = 0;
   std::string err;
@@ -482,6 +483,24 @@ KernelFn ell_kernel_t(int idx) {
   }
 }
 
+// Single shots on irregular graphs: the same kernel with one check and two variables per
+// thread (more threads per segment, shorter phases); one CTA per segment, one shot.
+constexpr EllVariant kEllLatVariants[] = {
+    {4, 2, 1, 2, 1024},
+    {7, 3, 1, 2, 448},
+    {8, 4, 1, 2, 1024},
+    {12, 6, 1, 2, 1024},
+};
+template <class A>
+KernelFn ell_lat_kernel_t(int idx) {
+  switch (idx) {
+    case 0: return decode_ell_kernel<A, 4, 2, 1, 2, 1024, 1>;
+    case 1: return decode_ell_kernel<A, 7, 3, 1, 2, 448, 1>;
+    case 2: return decode_ell_kernel<A, 8, 4, 1, 2, 1024, 1>;
+    default: return decode_ell_kernel<A, 12, 6, 1, 2, 1024, 1>;
+  }
+}
+
 // int8 and int16 share one build: 32-bit message words, saturation bound from DecodeParams
 KernelFn ell_kernel(int arith, int idx) {
   switch (arith) {
@@ -489,6 +508,14 @@ KernelFn ell_kernel(int arith, int idx) {
     case QB_ARITH_INT8:
     case QB_ARITH_INT16: return ell_kernel_t<ArithI32>(idx);
     default: return ell_kernel_t<ArithF16>(idx);
+  }
+}
+KernelFn ell_lat_kernel(int arith, int idx) {
+  switch (arith) {
+    case QB_ARITH_FLOAT: return ell_lat_kernel_t<ArithF32>(idx);
+    case QB_ARITH_INT8:
+    case QB_ARITH_INT16: return ell_lat_kernel_t<ArithI32>(idx);
+    default: return ell_lat_kernel_t<ArithF16>(idx);
   }
 }
 uint32_t ell_msg_bytes(int arith) { return arith == QB_ARITH_HALF ? 2u : 4u; }
@@ -649,6 +676,7 @@ void choose_plans(qb_decoder* h) {
   if (h->opt_kernel == 2 && !h->regular63) {
     fail(QB_INVALID_ARGUMENT, "regular kernel needs a (6,3)-regular graph with at most 8 segments");
   }
+  h->lat_ell = LaunchPlan{};
   if (!use_regular) {
     h->lat = h->bat = generic_plan(h);
     // batch: degree-padded item kernel when the degrees fit an instantiated bound
@@ -683,6 +711,29 @@ void choose_plans(qb_decoder* h) {
         pl.group_threads = T;
         finish_plan(h, pl);
         h->bat = pl;
+        break;
+      }
+      for (int idx = 0; idx < kNumEllVariants; ++idx) {  // single shots: one check per thread
+        const EllVariant& ev = kEllLatVariants[idx];
+        if (h->max_dc > static_cast<uint32_t>(ev.dc) || h->max_dv > static_cast<uint32_t>(ev.dv)) continue;
+        uint32_t want = 32;
+        for (uint32_t k = 0; k < P.nseg; ++k) {
+          const uint32_t ms = P.segs[k].c1 - P.segs[k].c0;
+          want = std::max(want, std::max((ms + ev.cpt - 1) / ev.cpt,
+                                         (P.ell_nvars[k] + ev.vpt - 1) / ev.vpt));
+        }
+        const uint32_t T = round_up32(want);
+        if (T > static_cast<uint32_t>(ev.maxt)) continue;
+        LaunchPlan pl{};
+        pl.items = true;
+        pl.lean = true;
+        pl.ell = 100 * ev.dc + ev.dv;
+        pl.kernel = ell_lat_kernel(h->arith, idx);
+        pl.name = "decode_ell_kernel";
+        pl.ngroups = 1;
+        pl.group_threads = T;
+        finish_plan(h, pl);
+        h->lat_ell = pl;
         break;
       }
     }
@@ -1114,9 +1165,13 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
     return;
   }
 
-  // ---- graphs the lean kernel does not cover: generic / regular kernels
+  // ---- graphs the lean kernel does not cover: degree-padded / generic / regular kernels
+  // The degree-padded kernel merges the segments' bit vectors with device atomics, so its
+  // single shots always take the copy protocol (device buffers, H2D / kernel / D2H).
+  const bool ell_shot = h->lat_ell.kernel != nullptr && !debug;
+  const bool use_mapped = mapped && !ell_shot;
   volatile uint32_t* h_flag = reinterpret_cast<volatile uint32_t*>(h->h_out + h->off_flag);
-  unsigned char* out = mapped ? h->d_out_map : h->d_out_dev;
+  unsigned char* out = use_mapped ? h->d_out_map : h->d_out_dev;
   io.est = reinterpret_cast<uint32_t*>(out);
   io.resid = reinterpret_cast<uint32_t*>(out + h->off_res);
   io.conv = out + h->off_conv;
@@ -1124,14 +1179,19 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
   io.kernel_ns = reinterpret_cast<uint64_t*>(out + h->off_ns);
   io.flag = reinterpret_cast<volatile uint32_t*>(out + h->off_flag);
   std::memcpy(h->h_in, syndrome, P.syn_w32 * 4);
-  io.syn = mapped ? h->d_in_map : h->d_in_dev;
-  if (mapped) {
+  io.syn = use_mapped ? h->d_in_map : h->d_in_dev;
+  if (use_mapped) {
     launch_plan(h, h->lat, io, h->lat.cluster ? h->P.nseg : 1, h->stream);
     spin_until(h, [&] { return *h_flag == seq; }, false);
   } else {
     CUDA_TRY(cudaMemcpyAsync(h->d_in_dev, h->h_in, P.syn_w32 * 4, cudaMemcpyHostToDevice,
                              h->stream));
-    launch_plan(h, h->lat, io, h->lat.cluster ? h->P.nseg : 1, h->stream);
+    if (ell_shot) {
+      io.tile = 1;
+      launch_plan(h, h->lat_ell, io, h->P.nseg, h->stream);  // one CTA per segment
+    } else {
+      launch_plan(h, h->lat, io, h->lat.cluster ? h->P.nseg : 1, h->stream);
+    }
     CUDA_TRY(cudaMemcpyAsync(h->h_out, h->d_out_dev, h->out_bytes, cudaMemcpyDeviceToHost,
                              h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));

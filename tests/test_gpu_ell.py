@@ -218,3 +218,42 @@ def test_packed_pairs_on_irregular_graphs(oracle, mode):
             if mode == "int8":
                 assert _same(a, oracle.decode_many(g, cfg, syn, None)), "pairs vs oracle"
     assert paired >= 6, "the packed kernel was not selected"
+
+
+@pytest.mark.parametrize("mode", REF_MODES)
+def test_single_shots_through_the_degree_padded_kernel(oracle, mode):
+    """qb_decode on irregular graphs runs the degree-padded kernel with one check per thread
+    and one CTA per segment (copy protocol): every outcome, per segment, equals the oracle's,
+    in both single-shot I/O settings, interleaved with batches on the same handle."""
+    OPT_LATENCY_IO = 1
+    code = codes.make_code("bb144")
+    h, segs = codes.extended_graph(code)
+    g = codes.build_tanner_graph(h)
+    rng = np.random.default_rng(31)
+    probs = np.full(g.num_vars, 0.02)
+    e = (rng.random((60, g.num_vars)) < probs).astype(np.uint8)
+    syn = gf2.pack_bits(h.mat_vec(e))
+    priors = rng.uniform(1.0, 6.0, g.num_vars)
+    for early in (True, False):
+        cfg = DecoderConfig(max_iterations=12, early_termination=early, arithmetic=mode,
+                            priors=priors.tolist())
+        want = oracle.decode_many(g, cfg, syn, segs)
+        with Decoder(g, cfg, segments=segs) as dec:
+            for io_mode in (0, 1):
+                dec.set_option(OPT_LATENCY_IO, io_mode)
+                for k in range(len(syn)):
+                    one = dec.decode_segments(syn[k])
+                    assert all(np.array_equal(a, b[k]) for a, b in zip(one, want)), (io_mode, k)
+                    assert dec.last_kernel_ns() > 0
+                assert _same(_batch(dec, syn), want)
+    # irregular single-segment graphs with degree-0 / degree-1 nodes
+    for g2 in (codes.build_tanner_graph(_degree_zero_graph()),
+               codes.build_tanner_graph(random_ldpc_matrix(rng, 25, 60))):
+        cfg = DecoderConfig(max_iterations=9, arithmetic=mode,
+                            priors=rng.uniform(0.3, 4.0, g2.num_vars).tolist())
+        syn2 = random_syndromes(rng, 40, g2.num_checks, 0.3)
+        want = oracle.decode_many(g2, cfg, syn2, None)
+        with Decoder(g2, cfg) as dec:
+            for k in range(len(syn2)):
+                one = dec.decode_segments(syn2[k])
+                assert all(np.array_equal(a, b[k]) for a, b in zip(one, want)), k
