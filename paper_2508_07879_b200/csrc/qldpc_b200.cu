@@ -168,6 +168,7 @@ struct qb_decoder {
   int64_t opt_slot_spread = 1;  // lean batch kernels: bank-spreading slot permutation
   int64_t opt_latency_graph = 1;
   cudaGraphExec_t lat_graph[2] = {nullptr, nullptr};
+  cudaGraphExec_t ell_graph = nullptr;  // degree-padded single shot: H2D, kernel, D2H
   uint32_t lat_graph_flip = 0;
   bool regular63 = false;  // every check degree 6, every variable degree 3
   uint32_t max_dc = 0, max_dv = 0;  // largest check / variable degree of the graph
@@ -192,6 +193,8 @@ void drop_latency_graphs(qb_decoder* h) {
     if (g) cudaGraphExecDestroy(g);
     g = nullptr;
   }
+  if (h->ell_graph) cudaGraphExecDestroy(h->ell_graph);
+  h->ell_graph = nullptr;
 }
 
 void free_batch(qb_decoder* h) {
@@ -1184,16 +1187,41 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
     launch_plan(h, h->lat, io, h->lat.cluster ? h->P.nseg : 1, h->stream);
     spin_until(h, [&] { return *h_flag == seq; }, false);
   } else {
-    CUDA_TRY(cudaMemcpyAsync(h->d_in_dev, h->h_in, P.syn_w32 * 4, cudaMemcpyHostToDevice,
-                             h->stream));
-    if (ell_shot) {
-      io.tile = 1;
-      launch_plan(h, h->lat_ell, io, h->P.nseg, h->stream);  // one CTA per segment
+    auto enqueue = [&] {
+      CUDA_TRY(cudaMemcpyAsync(h->d_in_dev, h->h_in, P.syn_w32 * 4, cudaMemcpyHostToDevice,
+                               h->stream));
+      if (ell_shot) {
+        io.tile = 1;
+        launch_plan(h, h->lat_ell, io, h->P.nseg, h->stream);  // one CTA per segment
+      } else {
+        launch_plan(h, h->lat, io, h->lat.cluster ? h->P.nseg : 1, h->stream);
+      }
+      CUDA_TRY(cudaMemcpyAsync(h->h_out, h->d_out_dev, h->out_bytes, cudaMemcpyDeviceToHost,
+                               h->stream));
+    };
+    if (ell_shot && h->opt_latency_graph != 0) {
+      // nothing in the three operations depends on the shot: one graph, captured once
+      if (!h->ell_graph) {
+        cudaGraph_t graph = nullptr;
+        CUDA_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+          enqueue();
+        } catch (...) {
+          cudaStreamEndCapture(h->stream, &graph);
+          if (graph) cudaGraphDestroy(graph);
+          throw;
+        }
+        CUDA_TRY(cudaStreamEndCapture(h->stream, &graph));
+        const cudaError_t ie = cudaGraphInstantiate(&h->ell_graph, graph, 0);
+        cudaGraphDestroy(graph);
+        CUDA_TRY(ie);
+        --h->launches;
+      }
+      CUDA_TRY(cudaGraphLaunch(h->ell_graph, h->stream));
+      ++h->launches;
     } else {
-      launch_plan(h, h->lat, io, h->lat.cluster ? h->P.nseg : 1, h->stream);
+      enqueue();
     }
-    CUDA_TRY(cudaMemcpyAsync(h->h_out, h->d_out_dev, h->out_bytes, cudaMemcpyDeviceToHost,
-                             h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
   }
   std::memcpy(estimate, h->h_out, P.est_w32 * 4);
