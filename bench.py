@@ -541,6 +541,26 @@ def measure_latency(args, code, lib, d_syn):
                     "mean": float(np.mean(wall)), "kernel_p50": nearest_rank(kern, 50),
                     "kernel_p99": nearest_rank(kern, 99), "shots": args.latency_shots,
                     "digest": "%016x" % digest}
+    # BASELINE config 5's graph: single shots on the phenomenological extension (degree-padded
+    # kernel, one CTA per segment, H2D / kernel / D2H as one graph launch)
+    from paper_2508_07879_b200 import codes, gf2
+    hx, segs = codes.extended_graph(code)
+    gx = codes.build_tanner_graph(hx)
+    pq = 0.005
+    rng = np.random.default_rng(args.seed)
+    pool5 = gf2.pack_bits(hx.mat_vec((rng.random((256, gx.num_vars)) < pq).astype(np.uint8)))
+    for arith in ("int8", "float"):
+        cfg = DecoderConfig(max_iterations=10, early_termination=False, arithmetic=arith,
+                            priors=[float(np.log((1 - pq) / pq))] * gx.num_vars)
+        with Decoder(gx, cfg, segments=segs) as dec:
+            wall, kern, digest = dec.latency_run(pool5, 300, args.latency_shots)
+            wall = np.sort(wall.astype(np.float64) * 1e-3)
+            kern = np.sort(kern.astype(np.float64) * 1e-3)
+            out[f"config5_ext_{arith}_fixed10"] = {
+                "p50": nearest_rank(wall, 50), "p99": nearest_rank(wall, 99),
+                "mean": float(np.mean(wall)), "kernel_p50": nearest_rank(kern, 50),
+                "kernel_p99": nearest_rank(kern, 99), "shots": args.latency_shots,
+                "kernel": "decode_ell_kernel" if dec.get_option(107) else "decode_generic_kernel"}
     out["note"] = ("wall = host steady_clock around the whole qb_decode (copy-in, launch, "
                    "completion, copy-out) inside qb_latency_run; kernel = in-kernel %globaltimer "
                    "span; doorbell = persistent cluster polling mapped host memory (no launch per "
