@@ -471,6 +471,7 @@ constexpr EllVariant kEllVariants[] = {
     {4, 2, 1, 2, 1024},   // e.g. the toy 3x6 fixture, repetition / surface-like checks
     {7, 3, 3, 5, 192},    // [H | I] extension of a (6,3)-regular code (phenomenological noise):
                           // the identity columns are absorbed by their checks
+    {7, 3, 3, 5, 320},    // ... the same graph as ONE segment (the reference's graph constructor)
     {8, 4, 2, 4, 512},
     {12, 6, 1, 2, 1024},
 };
@@ -481,7 +482,8 @@ KernelFn ell_kernel_t(int idx) {
   switch (idx) {
     case 0: return decode_ell_kernel<A, 4, 2, 1, 2, 1024, 1>;
     case 1: return decode_ell_kernel<A, 7, 3, 3, 5, 192, 5>;
-    case 2: return decode_ell_kernel<A, 8, 4, 2, 4, 512, 2>;
+    case 2: return decode_ell_kernel<A, 7, 3, 3, 5, 320, 3>;
+    case 3: return decode_ell_kernel<A, 8, 4, 2, 4, 512, 2>;
     default: return decode_ell_kernel<A, 12, 6, 1, 2, 1024, 1>;
   }
 }
@@ -494,6 +496,7 @@ constexpr EllVariant kEllLatVariants[] = {
     {8, 4, 1, 2, 1024},
     {12, 6, 1, 2, 1024},
 };
+constexpr int kNumEllLatVariants = sizeof(kEllLatVariants) / sizeof(kEllLatVariants[0]);
 template <class A>
 KernelFn ell_lat_kernel_t(int idx) {
   switch (idx) {
@@ -525,13 +528,14 @@ uint32_t ell_msg_bytes(int arith) { return arith == QB_ARITH_HALF ? 2u : 4u; }
 
 // two shots per thread on packed fp16 instructions (kernel_ell_h2.cuh): half mode, and int8
 // mode when the loader has verified the fp16 form of the Q16 scaling
-constexpr int kEllH2MaxT[] = {1024, 160, 512, 1024};
+constexpr int kEllH2MaxT[] = {1024, 160, 320, 512, 1024};
 template <bool kI8>
 KernelFn ell_h2_kernel_t(int idx) {
   switch (idx) {
     case 0: return decode_ell_h2_kernel<4, 2, 1, 2, 1024, 1, kI8>;
     case 1: return decode_ell_h2_kernel<7, 3, 3, 5, 160, 4, kI8>;
-    case 2: return decode_ell_h2_kernel<8, 4, 2, 4, 512, 1, kI8>;
+    case 2: return decode_ell_h2_kernel<7, 3, 3, 5, 320, 2, kI8>;
+    case 3: return decode_ell_h2_kernel<8, 4, 2, 4, 512, 1, kI8>;
     default: return decode_ell_h2_kernel<12, 6, 1, 2, 1024, 1, kI8>;
   }
 }
@@ -716,7 +720,7 @@ void choose_plans(qb_decoder* h) {
         h->bat = pl;
         break;
       }
-      for (int idx = 0; idx < kNumEllVariants; ++idx) {  // single shots: one check per thread
+      for (int idx = 0; idx < kNumEllLatVariants; ++idx) {  // single shots: one check per thread
         const EllVariant& ev = kEllLatVariants[idx];
         if (h->max_dc > static_cast<uint32_t>(ev.dc) || h->max_dv > static_cast<uint32_t>(ev.dv)) continue;
         uint32_t want = 32;
