@@ -36,9 +36,14 @@ namespace qb {
 
 constexpr uint32_t kH2Stride = 56, kH2ROff = 24;  // [6 x half2 q | 6 x half2 r | pad]
 
-__host__ __device__ inline size_t lean_h2_smem_bytes(uint32_t seg_mmax) {
+__host__ __device__ inline size_t lean_h2_bits_words(uint32_t seg_mmax) {
+  return (8 * static_cast<size_t>(lean_pw(seg_mmax)) + 16 + 3) & ~size_t(3);  // keeps 16-byte alignment
+}
+__host__ __device__ inline size_t lean_h2_smem_bytes(uint32_t seg_mmax, uint32_t syn_w32) {
   const size_t msg = (static_cast<size_t>(seg_mmax + 1) * kH2Stride + 15) & ~size_t(15);
-  return msg + 4 * (8 * static_cast<size_t>(lean_pw(seg_mmax)) + 16);
+  // messages | bitmaps, counters, tickets, syndrome copies | 2 syndrome tiles | 2 mbarriers |
+  // tile info [2][2] | tile cursor
+  return msg + 4 * lean_h2_bits_words(seg_mmax) + 2 * kMaxTile * syn_w32 * 4 + 16 + 16 + 16;
 }
 
 __device__ __forceinline__ __half2 u2h2(uint32_t u) {
@@ -202,6 +207,13 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
   uint32_t* const unsat_ctr = bits + 4 * pw;  // [2][2]
   uint32_t* const ticket = bits + 4 * pw + 4;  // [2]
   uint32_t* const syn_copy = bits + 4 * pw + 16;  // [item parity][shot lane][pw], never toggled
+  // syndromes arrive in TMA tiles of io.tile (even) shots = io.tile / 2 pairs, as in
+  // decode_lean_kernel: one bulk copy and one queue ticket per tile, two tiles in flight
+  uint32_t* const tilebuf = bits + lean_h2_bits_words(P.seg_mmax);  // [2][kMaxTile][syn_w32]
+  uint64_t* const mbar = reinterpret_cast<uint64_t*>(tilebuf + 2 * kMaxTile * P.syn_w32);  // [2]
+  uint32_t* const tinfo = reinterpret_cast<uint32_t*>(mbar + 2);  // [2]{first shot, shots}
+  uint32_t* const tstate = tinfo + 4;                              // {buffer, pair in tile, phases}
+  const uint32_t K = io.tile, tile_words = kMaxTile * P.syn_w32;
 
   uint32_t eo[VPT][kDV], co[CPT], cl[CPT], valid = 0;
   float gam[kFast ? 1 : VPT];
@@ -237,12 +249,19 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
   }
   for (uint32_t b = tid; b < kH2Stride; b += T) msgs[P.seg_mmax * kH2Stride + b] = 0;
 
-  uint64_t pair = peer;
-  uint32_t raw_a = 0, raw_b = 0;
-  if (warp == 0 && lane < gspan && pair < npairs) {
-    raw_a = io.syn[(2 * pair) * P.syn_w32 + gw0 + lane];
-    if (2 * pair + 1 < io.nshots) raw_b = io.syn[(2 * pair + 1) * P.syn_w32 + gw0 + lane];
+  auto issue_tile = [&](uint64_t t, uint32_t b) {
+    lean_issue_tile(io.syn, io.nshots, P.syn_w32, K, t, tilebuf + b * tile_words, &mbar[b],
+                    tinfo + 2 * b, lane);
+  };
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1u);
+    mbar_init(&mbar[1], 1u);
+    mbar_fence_init();
+    tstate[0] = tstate[1] = tstate[2] = 0u;
   }
+  __syncthreads();
+  if (warp == 0) issue_tile(peer, 0u);
+  uint64_t pair = static_cast<uint64_t>(peer) * (K / 2);
   uint32_t ipar = 0;
   __syncthreads();
 
@@ -257,6 +276,21 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
     volatile uint32_t* const unsat_b = unsat_ctr + ipar * 2 + 1;
     // ---------------- prologue ----------------
     if (warp == 0) {
+      const uint32_t tb = tstate[0], ti = tstate[1];
+      if (ti == 0u) {  // first pair of a tile: wait for its bytes, start on the tile after it
+        const uint32_t tphase = tstate[2];
+        mbar_wait(&mbar[tb], (tphase >> tb) & 1u);
+        __syncwarp();
+        if (lane == 0) tstate[2] = tphase ^ (1u << tb);
+        uint32_t t = 0;
+        if (lane == 0) t = atomicAdd(&io.sched[2 + s], 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        issue_tile(static_cast<uint64_t>(t) + peers, tb ^ 1u);
+        __syncwarp();
+      }
+      const uint32_t* rows = tilebuf + tb * tile_words + 2u * ti * P.syn_w32;
+      const uint32_t raw_a = lane < gspan ? rows[gw0 + lane] : 0u;
+      const uint32_t raw_b = lane < gspan && has_b ? rows[P.syn_w32 + gw0 + lane] : 0u;
       auto localise = [&](uint32_t raw, uint32_t* par, uint32_t* syn0, volatile uint32_t* ctr) {
         uint32_t nb = __shfl_down_sync(0xffffffffu, raw, 1);
         if (lane + 1 >= gspan) nb = 0;
@@ -276,8 +310,13 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
       localise(raw_a, par_a, syn_a, unsat_a);
       localise(raw_b, par_b, syn_b, unsat_b);
       if (lane == 0) {
-        const uint64_t t = static_cast<uint64_t>(atomicAdd(&io.sched[2 + s], 1u)) + peers;
-        ticket[ipar] = t < npairs ? static_cast<uint32_t>(t) : kNoShot;
+        // next pair: the following rows of this tile, else the first rows of the next tile
+        const uint32_t tpairs = (tinfo[2 * tb + 1] + 1u) >> 1;
+        const bool more = ti + 1u < tpairs;
+        const uint32_t nf = tinfo[2 * (tb ^ 1u)];
+        ticket[ipar] = more ? static_cast<uint32_t>(pair) + 1u : (nf == kNoShot ? kNoShot : nf >> 1);
+        tstate[0] = more ? tb : tb ^ 1u;
+        tstate[1] = more ? ti + 1u : 0u;
       }
     }
     if (warp == nwarps - 1) {
@@ -312,14 +351,6 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
       synpair[k] = (ba << 15) | (bb << 31);
     }
     const uint32_t next = ticket[ipar];
-    if (warp == 0 && lane < gspan) {
-      raw_a = raw_b = 0;
-      if (next != kNoShot) {
-        const uint64_t na = 2ull * next;
-        raw_a = io.syn[na * P.syn_w32 + gw0 + lane];
-        if (na + 1 < io.nshots) raw_b = io.syn[(na + 1) * P.syn_w32 + gw0 + lane];
-      }
-    }
 
     // ---------------- iterations ----------------
     uint32_t iter = 0, iter_a = 0, iter_b = 0;

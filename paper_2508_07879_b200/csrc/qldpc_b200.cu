@@ -560,7 +560,7 @@ void finish_plan(qb_decoder* h, LaunchPlan& pl) {
   pl.smem = pl.ell && pl.pair ? ell_h2_smem_bytes(h->P.seg_mmax, static_cast<uint32_t>(pl.ell / 100))
             : pl.ell  ? ell_smem_bytes(h->P.seg_mmax, ell_msg_bytes(h->arith),
                                        static_cast<uint32_t>(pl.ell / 100))
-            : pl.pair ? lean_h2_smem_bytes(h->P.seg_mmax)
+            : pl.pair ? lean_h2_smem_bytes(h->P.seg_mmax, h->P.syn_w32)
             : pl.lean ? h->smem_lean
                       : h->smem_bytes;
   CUDA_TRY(cudaFuncSetAttribute(pl.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -895,7 +895,16 @@ uint64_t resident_ctas(qb_decoder* h) {
 // Shots per syndrome tile of the lean batch kernel (one TMA bulk copy + one queue ticket
 // each): as large as leaves every resident CTA at least four tiles; 1 for small batches.
 uint32_t batch_tile(qb_decoder* h, uint64_t shots) {
-  if (!(h->bat.lean && !h->bat.pair && !h->bat.ell)) return 1;
+  if (!(h->bat.lean && !h->bat.ell)) return 1;
+  if (h->bat.pair) {  // two shots per item: tiles hold whole pairs (an even number of shots)
+    const uint64_t per_seg = std::max<uint64_t>(1, resident_ctas(h) / h->P.nseg);
+    uint32_t k = h->opt_batch_tile > 0 ? static_cast<uint32_t>(h->opt_batch_tile) & ~1u : 0u;
+    if (k >= 2) return k;
+    for (k = kMaxTile; k > 2; k >>= 1) {
+      if ((shots + k - 1) / k >= 4 * per_seg) return k;
+    }
+    return 2;
+  }
   const uint64_t per_seg = std::max<uint64_t>(1, resident_ctas(h) / h->P.nseg);
   if (h->opt_batch_tile > 0) return static_cast<uint32_t>(h->opt_batch_tile);
   for (uint32_t k = kMaxTile; k > 1; k >>= 1) {
@@ -909,7 +918,7 @@ unsigned batch_grid(qb_decoder* h, uint64_t shots) {
   if (h->bat.items) {  // equal numbers of CTAs per segment
     const uint64_t nseg = h->P.nseg;
     const uint64_t tile = batch_tile(h, shots);
-    const uint64_t items = h->bat.pair ? (shots + 1) / 2 : (shots + tile - 1) / tile;
+    const uint64_t items = h->bat.ell && h->bat.pair ? (shots + 1) / 2 : (shots + tile - 1) / tile;
     const uint64_t per_seg = std::max<uint64_t>(1, std::min<uint64_t>(resident / nseg, items));
     return static_cast<unsigned>(per_seg * nseg);
   }

@@ -448,10 +448,11 @@ def test_int8_on_the_packed_fp16_kernel_is_bit_exact(oracle, name, shots, p):
     assert paired >= 4, "the packed kernel was not selected"
 
 
-@pytest.mark.parametrize("mode", ["float", "int16"])
+@pytest.mark.parametrize("mode", ["float", "int16", "int8"])
 def test_tma_tiles_ragged_tail_and_unaligned_buffers(oracle, mode):
-    """The lean batch kernel streams syndromes in tiles of up to 16 shots (one TMA bulk copy
-    per tile).  20001 shots leave a ragged last tile (odd row count -> plain loads), and a
+    """The lean batch kernels (one shot per thread: float / int16; two shots per thread on
+    packed fp16 instructions: int8) stream syndromes in tiles of up to 16 shots (one TMA bulk
+    copy per tile).  20001 shots leave a ragged last tile (odd row count -> plain loads), and a
     buffer that starts on an odd 104-byte row is only 8-byte aligned (every tile -> plain
     loads): both must give the same results as the aligned bulk copies and the oracle."""
     import torch
