@@ -453,6 +453,28 @@ def measure_variants(args, code, d_syn, d_est, d_conv, d_its, stream):
                     "p_data": pq, "p_meas": pq, "shots_per_launch": shots5,
                     "convergence_rate": float((d_conv[:shots5].min(dim=1).values == 1).double().mean().item()),
                     "mean_iterations": float(its.max(dim=1).values.double().mean().item())}
+    # ---- BASELINE config 4's loop, entirely on the device: sample -> syndrome -> decode ->
+    # classify through qb_campaign_run, with the reference-exact sampler and the skip sampler
+    from paper_2508_07879_b200 import _lib
+    from paper_2508_07879_b200.campaign import Campaign
+    trials = min(args.shots, 1 << 20)
+    camp = Campaign(code, DecoderConfig(max_iterations=args.max_iterations,
+                                        early_termination=not args.no_early_stop,
+                                        arithmetic=args.arithmetic))
+    try:
+        for name, sampler in (("campaign_reference_stream", 0), ("campaign_skip_sampler", 1)):
+            camp.decoder.set_option(_lib.OPT_SAMPLER, sampler)
+            camp.run_range(args.p, args.seed, 0, trials)  # warm-up (buffers, module load)
+            t0 = time.perf_counter()
+            reps = 3
+            for r in range(reps):
+                c = camp.run_range(args.p, args.seed, r * trials, trials)
+            dt = (time.perf_counter() - t0) / reps
+            out[name] = {"trials_per_s": trials / dt, "trials_per_call": trials, "p": args.p,
+                         "timer": "host perf_counter around qb_campaign_run (blocking), mean of 3",
+                         "non_converged_last_call": int(c[5])}
+    finally:
+        camp.close()
     return out
 
 

@@ -144,6 +144,13 @@ typedef enum {
   /* qb_decode_batch (host buffers): shots per pipeline chunk (H2D copy, kernel and D2H
    * copy of consecutive chunks overlap on three streams); 0 = auto. */
   QB_OPT_BATCH_CHUNK = 15,
+  /* qb_generate_syndromes / qb_campaign_run: 0 (default) = the reference's SplitMix64
+   * stream, bit for bit (one draw per variable); 1 = the same i.i.d. Bernoulli
+   * distribution sampled by geometric skips (one draw per FLIP; per-variable
+   * probabilities by thinning) - a different stream, keyed by (seed, trial) in the
+   * same way, for campaigns that need the statistics but not the reference's trials
+   * ("device RNG need not reproduce SplitMix64 bit-streams"). */
+  QB_OPT_SAMPLER = 16,
   /* Read-only (qb_get_option): the launch plans actually in use. */
   QB_OPT_INFO_BATCH_CTAS_PER_SM = 100,
   QB_OPT_INFO_BATCH_BLOCK = 101,

@@ -17,6 +17,7 @@ ARITH = {"float": 0, "int8": 1, "int16": 2, "half": 3}
 ARITH_NAMES = {v: k for k, v in ARITH.items()}
 
 OPT_KERNEL, OPT_LATENCY_IO, OPT_LATENCY_SHAPE, OPT_GROUP_THREADS, OPT_BATCH_CTAS_PER_SM = range(5)
+OPT_SAMPLER = 16  # 0 = the reference's SplitMix64 stream, 1 = geometric skips (same distribution)
 
 u32p = C.POINTER(C.c_uint32)
 u64p = C.POINTER(C.c_uint64)

@@ -104,4 +104,80 @@ noise_syndrome_kernel(const __grid_constant__ DecodeParams P, const __grid_const
   }
 }
 
+// ---- fast sampler (QB_OPT_SAMPLER = 1): same distribution, NOT the reference's stream ----
+//
+// The reference draws one uniform per variable; at p = 0.01 that is 1568 SplitMix64
+// outputs per [[784,24,24]] shot for ~16 flips.  Flips of an i.i.d. Bernoulli(p) sequence
+// are separated by geometric gaps, so this kernel draws one uniform per FLIP instead:
+//
+//   gap = floor(ln(u) / ln(1 - p)),  u uniform in (0, 1)      P(gap = g) = (1-p)^g p
+//
+// Non-uniform probabilities are sampled by thinning: gaps at p_max, a candidate v is kept
+// with probability p_v / p_max (second draw, integer threshold).  The stream is still a
+// counter-based SplitMix64 keyed by (seed, trial), so a campaign's result does not depend on
+// how its trials are split over launches or GPUs.  Logarithms are evaluated in fp64: about
+// p*N of them per shot.
+//
+// One THREAD per shot: each thread owns an odd-stride row of shared memory (syndrome words
+// then error words), ORs / XORs its flips into it, and the CTA copies the rows out with
+// coalesced stores.
+struct SkipParams {
+  double inv_log1m;   // 1 / ln(1 - p_max)  (<= -0.0; -inf when p_max = 0 => no flips)
+  uint32_t row;       // shared-memory row stride in words, odd, >= syn_w32 + est_w32
+};
+
+template <bool kPerVar>
+__global__ void noise_skip_kernel(const __grid_constant__ DecodeParams P,
+                                  const __grid_constant__ NoiseParams np,
+                                  const __grid_constant__ SkipParams sp) {
+  extern __shared__ uint32_t noise_smem[];  // [blockDim.x][row]
+  const uint32_t nthreads = blockDim.x, row = sp.row;
+  const uint32_t sw = P.syn_w32, ew = P.est_w32, N = P.N;
+  uint32_t* mine = noise_smem + threadIdx.x * row;
+  const double dN = static_cast<double>(N);
+  for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * nthreads; base < np.nshots;
+       base += static_cast<uint64_t>(gridDim.x) * nthreads) {
+    for (uint32_t w = 0; w < sw + ew; ++w) mine[w] = 0u;
+    const uint64_t shot = base + threadIdx.x;
+    if (shot < np.nshots) {
+      const uint64_t state0 = splitmix_mix(np.seed + kPhi * (np.first_trial + shot) + kPhi);
+      uint64_t ctr = state0;
+      double pos = -1.0;  // exact: integers far below 2^53
+      for (;;) {
+        ctr += kPhi;
+        const uint64_t z = splitmix_mix(ctr);
+        // 52 random bits + 1/2: every value is exact in fp64 and lies strictly inside (0, 1)
+        const double u = (static_cast<double>(z >> 12) + 0.5) * 0x1p-52;
+        const double gap = floor(log(u) * sp.inv_log1m);
+        pos += gap + 1.0;
+        if (!(pos < dN)) break;  // also ends the shot when p_max = 0 (gap = +inf)
+        const uint32_t v = static_cast<uint32_t>(pos);
+        if constexpr (kPerVar) {
+          ctr += kPhi;
+          if ((splitmix_mix(ctr) >> 11) >= np.thrs[v]) continue;  // thinning: keep w.p. p_v / p_max
+        }
+        mine[sw + (v >> 5)] |= 1u << (v & 31u);
+        for (uint32_t i = P.var_off[v]; i < P.var_off[v + 1]; ++i) {
+          const uint32_t m = P.edge_check[P.var_edges[i]];
+          mine[m >> 5] ^= 1u << (m & 31u);
+        }
+      }
+    }
+    __syncthreads();
+    const uint64_t left = np.nshots - base;
+    const uint32_t here = left < nthreads ? static_cast<uint32_t>(left) : nthreads;
+    for (uint32_t i = threadIdx.x; i < here * sw; i += nthreads) {
+      const uint32_t s = i / sw, w = i - s * sw;
+      np.syn[base * sw + i] = noise_smem[s * row + w];
+    }
+    if (np.err) {
+      for (uint32_t i = threadIdx.x; i < here * ew; i += nthreads) {
+        const uint32_t s = i / ew, w = i - s * ew;
+        np.err[base * ew + i] = noise_smem[s * row + sw + w];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace qb

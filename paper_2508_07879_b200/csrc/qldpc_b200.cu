@@ -164,6 +164,7 @@ struct qb_decoder {
   // memcpy protocol as ONE CUDA-graph launch (H2D copy -> cluster kernel -> D2H copy); two
   // instantiated graphs with different record tags alternate, so a stale record is detected
   int64_t opt_batch_tile = 0;  // shots per TMA syndrome tile, 0 = auto
+  int64_t opt_sampler = 0;      // qb_generate_syndromes: 0 = the reference's stream, 1 = geometric skips
   int64_t opt_batch_chunk = 0;  // qb_decode_batch: shots per pipeline chunk, 0 = auto (2^15)
   int64_t opt_slot_spread = 1;  // lean batch kernels: bank-spreading slot permutation
   int64_t opt_latency_graph = 1;
@@ -1682,6 +1683,10 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
         if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_SLOT_SPREAD: 0 or 1");
         h->opt_slot_spread = value;
         break;
+      case QB_OPT_SAMPLER:
+        if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_SAMPLER: 0 or 1");
+        h->opt_sampler = value;
+        return;
       case QB_OPT_BATCH_CHUNK:
         if (value < 0) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_CHUNK: >= 0");
         h->opt_batch_chunk = value;
@@ -1769,6 +1774,7 @@ int64_t qb_get_option(const qb_decoder* h, int option) {
     case QB_OPT_LATENCY_GRAPH: return h->opt_latency_graph;
     case QB_OPT_BATCH_TILE: return h->opt_batch_tile;
     case QB_OPT_BATCH_CHUNK: return h->opt_batch_chunk;
+    case QB_OPT_SAMPLER: return h->opt_sampler;
     case QB_OPT_SLOT_SPREAD: return h->opt_slot_spread;
     case QB_OPT_INFO_LAST_EVENT_NS: return static_cast<int64_t>(h->last_event_ns);
     case QB_OPT_BATCH_CTAS_PER_SM: return h->opt_batch_ctas;
@@ -1886,11 +1892,17 @@ qb_status qb_generate_syndromes(qb_decoder* h, uint64_t seed, double p, const do
     np.seed = seed;
     np.first_trial = first_trial;
     np.nshots = shots;
+    const bool skip = h->opt_sampler == 1;
+    double p_max = 0.0;
     if (probs) {
       std::vector<uint64_t> thr(P.N);
       for (uint32_t v = 0; v < P.N; ++v) {
         check_p(probs[v]);
-        thr[v] = noise_threshold(probs[v]);
+        p_max = std::max(p_max, probs[v]);
+      }
+      for (uint32_t v = 0; v < P.N; ++v) {
+        // skip sampler: acceptance threshold of the thinning step, p_v / p_max
+        thr[v] = noise_threshold(skip ? (p_max > 0.0 ? probs[v] / p_max : 0.0) : probs[v]);
       }
       if (!h->d_probs) CUDA_TRY(cudaMalloc(&h->d_probs, sizeof(uint64_t) * P.N));
       // synchronous: `thr` is a local
@@ -1900,6 +1912,7 @@ qb_status qb_generate_syndromes(qb_decoder* h, uint64_t seed, double p, const do
     } else {
       check_p(p);
       np.thr = noise_threshold(p);
+      p_max = p;
     }
     np.mode = css_interleave ? 1u : 0u;
     if (css_interleave) {
@@ -1911,6 +1924,27 @@ qb_status qb_generate_syndromes(qb_decoder* h, uint64_t seed, double p, const do
     }
     np.syn = reinterpret_cast<uint32_t*>(d_syndromes);
     np.err = reinterpret_cast<uint32_t*>(d_errors);
+    if (skip) {
+      // one thread per shot, one odd-stride shared-memory row per thread
+      SkipParams sp{};
+      sp.inv_log1m = 1.0 / std::log1p(-p_max);  // -inf at p_max = 0 (no flips), -0.0 at p_max = 1 (all flip)
+      sp.row = (P.syn_w32 + P.est_w32) | 1u;
+      unsigned threads = 128;
+      while (threads > 32 && static_cast<size_t>(threads) * sp.row * 4 > static_cast<size_t>(h->max_smem_optin)) threads /= 2;
+      const size_t smem = static_cast<size_t>(threads) * sp.row * 4;
+      if (smem > static_cast<size_t>(h->max_smem_optin)) {
+        fail(QB_INVALID_ARGUMENT, "generate_syndromes: graph too large for the skip sampler (QB_OPT_SAMPLER = 0 has no limit)");
+      }
+      auto* kern = np.thrs ? noise_skip_kernel<true> : noise_skip_kernel<false>;
+      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      const uint64_t blocks_needed = (shots + threads - 1) / threads;
+      const unsigned grid = static_cast<unsigned>(
+          std::min<uint64_t>(blocks_needed, static_cast<uint64_t>(h->sm_count) * 16));
+      kern<<<grid, threads, smem, st>>>(P, np, sp);
+      CUDA_TRY(cudaGetLastError());
+      ++h->launches;
+      return;
+    }
     const uint64_t blocks_needed = (shots + kNoiseWarps - 1) / kNoiseWarps;
     const unsigned grid = static_cast<unsigned>(
         std::min<uint64_t>(blocks_needed, static_cast<uint64_t>(h->sm_count) * 8));

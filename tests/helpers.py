@@ -37,3 +37,34 @@ def error_syndromes(code: codes.CssCode, rng: np.random.Generator, shots: int, p
     sx = code.hz.mat_vec(ex)
     sz = code.hx.mat_vec(ez)
     return ex, ez, gf2.pack_bits(np.concatenate([sx, sz], axis=-1))
+
+
+_M64 = (1 << 64) - 1
+_PHI = 0x9E3779B97F4A7C15
+
+
+def _splitmix_mix(z: int) -> int:
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def skip_sampler_flips(seed: int, trial: int, p: float, num_vars: int) -> list:
+    """Plain-Python statement of the geometric-skip sampler (QB_OPT_SAMPLER = 1, uniform p;
+    csrc/kernel_noise.cuh): the flipped variables of one trial, ascending.  Not a reference
+    algorithm - the reference draws one uniform per variable (proj/src/noise.cpp:67-78) -
+    only its SplitMix64 seeding and output function are the reference's
+    (proj/include/qldpc/noise.hpp:28-45)."""
+    import math
+    if p <= 0.0:
+        return []
+    inv = 1.0 / math.log1p(-p) if p < 1.0 else -0.0
+    ctr = _splitmix_mix((seed + _PHI * trial + _PHI) & _M64)
+    pos, out = -1.0, []
+    while True:
+        ctr = (ctr + _PHI) & _M64
+        u = ((_splitmix_mix(ctr) >> 12) + 0.5) * 2.0 ** -52
+        pos += math.floor(math.log(u) * inv) + 1.0
+        if not pos < num_vars:
+            return out
+        out.append(int(pos))

@@ -114,3 +114,28 @@ def test_magic_rounding_window():
     assert int(np.float16(1536.0).view(np.uint16)) == 0x6600   # the kernel's constant
     assert int(np.float16(127.0).view(np.uint16)) == 0x57F0    # saturation bound / sentinel
     assert int(np.float16(64.0).view(np.uint16)) == 0x5400     # degree-1 check sentinel
+
+
+def test_geometric_skip_sampling_has_the_bernoulli_law():
+    """The skip sampler's algorithm (tests/helpers.skip_sampler_flips, the statement the GPU
+    kernel is compared with bit for bit): gaps floor(ln u / ln(1-p)) between flips give i.i.d.
+    Bernoulli(p) variables - weight mean and variance of Binomial(N, p), uniform per-position
+    rate including both ends, strictly ascending positions, p = 0 / p = 1 edge cases."""
+    from tests.helpers import skip_sampler_flips
+    n, p, trials = 300, 0.04, 6000
+    counts = np.zeros(n)
+    weights = np.zeros(trials)
+    for t in range(trials):
+        f = skip_sampler_flips(11, t, p, n)
+        assert all(a < b for a, b in zip(f, f[1:])) and (not f or (0 <= f[0] and f[-1] < n))
+        counts[f] += 1
+        weights[t] = len(f)
+    var = n * p * (1 - p)
+    assert abs(weights.mean() - n * p) < 4 * np.sqrt(var / trials)
+    assert abs(weights.var() - var) < 5 * var * np.sqrt(2.0 / trials) + 0.01 * var
+    assert np.abs(counts / trials - p).max() < 5 * np.sqrt(p * (1 - p) / trials)
+    assert abs(counts[:10].sum() / (10 * trials) - p) < 4 * np.sqrt(p * (1 - p) / (10 * trials))
+    assert abs(counts[-10:].sum() / (10 * trials) - p) < 4 * np.sqrt(p * (1 - p) / (10 * trials))
+    assert skip_sampler_flips(3, 0, 0.0, n) == []
+    assert skip_sampler_flips(3, 0, 1.0, n) == list(range(n))
+    assert skip_sampler_flips(3, 5, p, n) != skip_sampler_flips(3, 6, p, n)

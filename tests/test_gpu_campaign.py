@@ -86,3 +86,40 @@ def test_half_precision_ler_within_reference_ci(ref):
         ours = run_campaign(code, p, 4242, 200000,
                             DecoderConfig(max_iterations=iters, arithmetic="half"))
         assert c - hw <= ours.logical_error_rate <= c + hw, (p, ours.logical_error_rate, c, hw)
+
+
+def test_skip_sampler_campaign_within_reference_ci_and_partition_independent(ref):
+    """QB_OPT_SAMPLER = 1 draws other trials than the reference (geometric gaps instead of
+    one uniform per qubit), so its campaign is judged like the fp16 path: failure rate inside
+    the 95 % Wilson interval of the reference's run_campaign on the same noise model, mean
+    iteration count close to it, and - the stream being keyed by (seed, trial) - counters
+    that do not depend on how the trial range is split."""
+    import math
+    code = codes.make_code("bb144")
+    rc = ref.code("bb144")
+    cfg = DecoderConfig(max_iterations=30)
+    camp = Campaign(code, cfg)
+    try:
+        camp.decoder.set_option(16, 1)
+        for p in (0.02, 0.04):
+            n = 12000
+            rr = ref.run_campaign(rc, 0, p, 4242, n, cfg, workers=0)
+            k = rr["logical_x"] + rr["logical_z"] + rr["logical_both"] + rr["non_converged"]
+            ph, z = k / n, 1.96
+            den = 1 + z * z / n
+            c = (ph + z * z / (2 * n)) / den
+            hw = z * math.sqrt(ph * (1 - ph) / n + z * z / (4 * n * n)) / den
+            ours = CampaignResult.from_counters(camp.run_range(p, 4242, 0, 200000))
+            assert c - hw <= ours.logical_error_rate <= c + hw, (p, ours.logical_error_rate, c, hw)
+            assert abs(ours.mean_iterations - rr["mean_iterations"]) < 0.05 * rr["mean_iterations"]
+            assert ours.baseline_logical_rate > 0.5
+        whole = camp.run_range(0.03, 99, 0, 5000)
+        total = np.zeros_like(whole)
+        for rank in range(3):
+            lo, hi = shard(5000, 3, rank)
+            total += camp.run_range(0.03, 99, lo, hi - lo)
+        assert np.array_equal(total, whole)
+        camp.decoder.set_option(16, 0)
+        assert not np.array_equal(camp.run_range(0.03, 99, 0, 5000), whole)
+    finally:
+        camp.close()

@@ -161,6 +161,26 @@ def test_validation_errors():
         decode(code.graph_x, np.zeros(2, dtype=np.uint64), DecoderConfig(), bits=72)
 
 
+def test_zero_shot_and_null_buffer_batches_through_the_c_abi():
+    """decode_batch on an empty span returns an empty result before any work
+    (proj/src/decoder.cpp:617); through the C-ABI that is QB_OK with no launch, while
+    a non-empty batch with a NULL buffer is rejected as an invalid argument."""
+    code = codes.make_code("bb72")
+    for mode in ("float", "int8"):
+        with Decoder(code, DecoderConfig(arithmetic=mode)) as dec:
+            before = dec.launch_count()
+            est, res, conv, its = dec.decode_batch_segments(np.zeros((0, 2), dtype=np.uint64))
+            assert est.shape == (0, 3) and res.shape == (0, 2)
+            assert conv.shape == (0, 2) and its.shape == (0, 2)
+            dec.decode_batch_raw(0, 0, 0, None, 0, 0)
+            assert dec.launch_count() == before
+            with pytest.raises(ValueError, match="NULL"):
+                dec.decode_batch_raw(4, 0, 0, None, 0, 0)
+            # the handle is still usable after the rejected call
+            out = dec.decode(np.zeros(2, dtype=np.uint64))
+            assert out.converged and out.iterations_used == 1
+
+
 def test_decoder_instances_are_reusable():
     """proj/tests/test_decoder.cpp:328-339."""
     code = codes.make_code("bb72")

@@ -35,6 +35,9 @@ def main():
     ap.add_argument("--modes", default="float,int8,half")
     ap.add_argument("--max-iterations", type=int, default=50)
     ap.add_argument("--seed", type=int, default=12345)
+    ap.add_argument("--sampler", type=int, default=0,
+                    help="QB_OPT_SAMPLER for the full-size runs: 0 = the reference's stream, 1 = "
+                         "geometric skips (the runs on the reference's own trials always use 0)")
     args = ap.parse_args()
     code = codes.make_code(args.code)
     ref = rc = None
@@ -48,10 +51,15 @@ def main():
     rows = []
     for mode in args.modes.split(","):
         camp = Campaign(code, DecoderConfig(max_iterations=args.max_iterations, arithmetic=mode))
+        # untimed warm-up at the full chunk size: batch buffers, counters and the kernels'
+        # lazy module load would otherwise be charged to the first point of the sweep
+        camp.run_range(0.01, args.seed + 1, 0, args.trials)
         for p in [float(x) for x in args.ps.split(",")]:
+            camp.decoder.set_option(16, args.sampler)
             t0 = time.perf_counter()
             r = CampaignResult.from_counters(camp.run_range(p, args.seed, 0, args.trials))
             dt = time.perf_counter() - t0
+            camp.decoder.set_option(16, 0)
             fails = r.logical_x + r.logical_z + r.logical_both + r.non_converged
             row = {"code": args.code, "mode": mode, "p": p, "trials": r.trials, "ler": r.logical_error_rate,
                    "ler_ci95": wilson(fails, r.trials), "non_converged": r.non_converged,
@@ -85,6 +93,14 @@ def main():
         print(f"| {r['mode']} | {r['p']} | {r['trials']} | {r['ler']:.3e} | {r['mean_iterations']:.2f} | "
               f"{refs} | {r.get('gpu_ler_on_ref_trials', float('nan')):.3e} | "
               f"{r.get('identical_on_ref_trials', '-')} | {r.get('within_ref_ci', '-')} |")
+    print("\nThroughput of the whole loop (sample, syndrome, decode, classify on the device; host "
+          "wall clock around qb_campaign_run, after one untimed warm-up run), M trials/s:\n")
+    ps = sorted({r["p"] for r in rows})
+    print("| mode | " + " | ".join(f"p = {p}" for p in ps) + " |")
+    print("|---|" + "---|" * len(ps))
+    for mode in args.modes.split(","):
+        by_p = {r["p"]: r["trials_per_s"] for r in rows if r["mode"] == mode}
+        print(f"| {mode} | " + " | ".join(f"{by_p[p] / 1e6:.1f}" if p in by_p else "-" for p in ps) + " |")
 
 
 if __name__ == "__main__":

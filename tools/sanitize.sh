@@ -23,7 +23,6 @@ for tool in $TOOLS; do
   fi
   extra=""
   [ "$tool" = racecheck ] && extra="--racecheck-report all"
-  [ "$tool" = initcheck ] && extra="--track-unused-memory no"
   timeout ${SANITIZE_TIMEOUT:-1500} compute-sanitizer --tool $tool $extra --target-processes all \
       --log-file $log python -m pytest $sel -m gpu -q $SKIP ${kexpr:+-k "$kexpr"} \
       > gpurun_out/${R}_${tool}_pytest.log 2>&1

@@ -8,8 +8,10 @@ if os.environ.get("QB_LIB"):
 from paper_2508_07879_b200.campaign import Campaign
 code = codes.make_code("bb784"); g = code.combined_graph
 shots = 1 << 20
+SAMPLER = int(os.environ.get("QB_SAMPLER", "0"))  # 1 = geometric-skip sampler (QB_OPT_SAMPLER)
 for arith in sys.argv[1:] or ["float"]:
     camp = Campaign(code, DecoderConfig(max_iterations=50, arithmetic=arith)); dec = camp.decoder
+    dec.set_option(_lib.OPT_SAMPLER, SAMPLER)
     sw, ew = gf2.num_words(g.num_checks), gf2.num_words(g.num_vars)
     dev = torch.device("cuda")
     d_syn = torch.zeros((shots, sw), dtype=torch.int64, device=dev); d_err = torch.zeros((shots, ew), dtype=torch.int64, device=dev)
@@ -29,6 +31,6 @@ for arith in sys.argv[1:] or ["float"]:
     import time
     t0 = time.perf_counter(); c = camp.run_range(0.01, 1, 0, shots); whole = (time.perf_counter() - t0) * 1e3
     t0 = time.perf_counter(); c = camp.run_range(0.01, 1, 0, shots); whole = (time.perf_counter() - t0) * 1e3
-    print(json.dumps({"arith": arith, "generate_ms": gen, "decode_ms": decd, "classify_ms": cls, "campaign_ms": whole,
+    print(json.dumps({"arith": arith, "sampler": SAMPLER, "generate_ms": gen, "decode_ms": decd, "classify_ms": cls, "campaign_ms": whole,
                       "campaign_Mtrials_s": shots / whole / 1e3}))
     camp.close()
