@@ -309,6 +309,7 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
       };
       localise(raw_a, par_a, syn_a, unsat_a);
       localise(raw_b, par_b, syn_b, unsat_b);
+      __syncwarp();  // every lane has read tstate[] before lane 0 advances it
       if (lane == 0) {
         // next pair: the following rows of this tile, else the first rows of the next tile
         const uint32_t tpairs = (tinfo[2 * tb + 1] + 1u) >> 1;
