@@ -142,7 +142,8 @@ typedef enum {
    * update is symmetric in its slots); 0 = slots in row order. */
   QB_OPT_SLOT_SPREAD = 14,
   /* qb_decode_batch (host buffers): shots per pipeline chunk (H2D copy, kernel and D2H
-   * copy of consecutive chunks overlap on three streams); 0 = auto. */
+   * copy of consecutive chunks overlap on three streams); 0 = auto (2^15).  Also the
+   * trials per sample / decode / classify round of qb_campaign_run (0 = 2^20). */
   QB_OPT_BATCH_CHUNK = 15,
   /* qb_generate_syndromes / qb_campaign_run: 0 (default) = the reference's SplitMix64
    * stream, bit for bit (one draw per variable); 1 = the same i.i.d. Bernoulli

@@ -2035,7 +2035,9 @@ qb_status qb_campaign_run(qb_decoder* h, uint64_t seed, double p, const double* 
     if (!h->d_counters) CUDA_TRY(cudaMalloc(&h->d_counters, 10 * sizeof(unsigned long long)));
     cudaStream_t st = h->stream;
     CUDA_TRY(cudaMemsetAsync(h->d_counters, 0, 10 * sizeof(unsigned long long), st));
-    const uint64_t chunk = std::min<uint64_t>(trials, 1ull << 20);
+    // trials per sample / decode / classify round: QB_OPT_BATCH_CHUNK when set, else 2^20
+    const uint64_t max_chunk = h->opt_batch_chunk > 0 ? static_cast<uint64_t>(h->opt_batch_chunk) : (1ull << 20);
+    const uint64_t chunk = std::min<uint64_t>(trials, max_chunk);
     ensure_batch(h, chunk, false);
     for (uint64_t done = 0; done < trials; done += chunk) {
       const uint64_t n = std::min<uint64_t>(chunk, trials - done);

@@ -57,6 +57,14 @@ def test_campaign_is_independent_of_the_partition():
                 lo, hi = shard(5000, world, rank)
                 total += camp.run_range(0.03, 99, lo, hi - lo)
             assert np.array_equal(total, whole)
+        # several sample / decode / classify rounds inside one call (QB_OPT_BATCH_CHUNK),
+        # including one-trial rounds (odd counts exercise the packed kernels' half-empty pair)
+        small = camp.run_range(0.03, 99, 0, 40)
+        for chunk, trials, want in ((1, 40, small), (64, 5000, whole), (1001, 5000, whole),
+                                    (4999, 5000, whole)):
+            camp.decoder.set_option(15, chunk)
+            assert np.array_equal(camp.run_range(0.03, 99, 0, trials), want), chunk
+        camp.decoder.set_option(15, 0)
     finally:
         camp.close()
 
@@ -119,6 +127,9 @@ def test_skip_sampler_campaign_within_reference_ci_and_partition_independent(ref
             lo, hi = shard(5000, 3, rank)
             total += camp.run_range(0.03, 99, lo, hi - lo)
         assert np.array_equal(total, whole)
+        camp.decoder.set_option(15, 999)   # five and a bit rounds of 999 trials per call
+        assert np.array_equal(camp.run_range(0.03, 99, 0, 5000), whole)
+        camp.decoder.set_option(15, 0)
         camp.decoder.set_option(16, 0)
         assert not np.array_equal(camp.run_range(0.03, 99, 0, 5000), whole)
     finally:
