@@ -12,6 +12,7 @@ SAMPLER = int(os.environ.get("QB_SAMPLER", "0"))  # 1 = geometric-skip sampler (
 for arith in sys.argv[1:] or ["float"]:
     camp = Campaign(code, DecoderConfig(max_iterations=50, arithmetic=arith)); dec = camp.decoder
     dec.set_option(_lib.OPT_SAMPLER, SAMPLER)
+    dec.set_option(15, int(os.environ.get("QB_CHUNK", "0")))  # trials per campaign round, 0 = default
     sw, ew = gf2.num_words(g.num_checks), gf2.num_words(g.num_vars)
     dev = torch.device("cuda")
     d_syn = torch.zeros((shots, sw), dtype=torch.int64, device=dev); d_err = torch.zeros((shots, ew), dtype=torch.int64, device=dev)
@@ -31,6 +32,6 @@ for arith in sys.argv[1:] or ["float"]:
     import time
     t0 = time.perf_counter(); c = camp.run_range(0.01, 1, 0, shots); whole = (time.perf_counter() - t0) * 1e3
     t0 = time.perf_counter(); c = camp.run_range(0.01, 1, 0, shots); whole = (time.perf_counter() - t0) * 1e3
-    print(json.dumps({"arith": arith, "sampler": SAMPLER, "generate_ms": gen, "decode_ms": decd, "classify_ms": cls, "campaign_ms": whole,
+    print(json.dumps({"arith": arith, "sampler": SAMPLER, "chunk": int(os.environ.get("QB_CHUNK", "0")), "generate_ms": gen, "decode_ms": decd, "classify_ms": cls, "campaign_ms": whole,
                       "campaign_Mtrials_s": shots / whole / 1e3}))
     camp.close()
