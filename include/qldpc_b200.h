@@ -297,6 +297,68 @@ qb_status qb_classify_batch_device(qb_decoder* h, uint64_t shots,
                                    const uint32_t* d_iterations,
                                    uint64_t* counters, void* stream);
 
+/* ---- Soft (noisy) syndromes: per-shot priors -----------------------------------------
+ *
+ * The reference takes priors per Decoder (decoder.hpp:31-32, decoder.cpp:108-131); soft
+ * syndrome information is per SHOT.  On an extended graph [H | I] the identity column of
+ * check m is a degree-1 "measurement error" variable whose prior is the reliability
+ * |LLR_m| of the measured bit: the reference handles it through its
+ * degree-1-variable path (decoder.cpp:324-329) with one Decoder constructed per shot.
+ * Here the loader lets every check ABSORB its first degree-1 variable, and the calls below
+ * take that variable's prior per shot:
+ *
+ *   soft[shot][m], m in [0, num_checks) = prior of qb_soft_vars()[m] for this shot
+ *     QB_ARITH_FLOAT / QB_ARITH_HALF : float   (what the reference stores: float(prior))
+ *     QB_ARITH_INT8                  : int8_t  the QUANTISED prior, non-zero, |x| <= 127
+ *     QB_ARITH_INT16                 : int16_t the QUANTISED prior, non-zero, |x| <= 32767
+ *   (quantised = quantize_saturate(prior, quant_scale, kmax), decoder.cpp:115-122, :500-509;
+ *   the reference rejects priors that quantise to 0.)  Entries of checks without an absorbed
+ *   variable (qb_soft_vars()[m] == 0xffffffff) are ignored.  Every other prior is the
+ *   decoder's (qb_config::priors).
+ *
+ * Results equal those of a reference Decoder built for each shot on the same graph with
+ * `priors[qb_soft_vars()[m]] = soft[shot][m]` (de-quantised: value / quant_scale).
+ * QB_INVALID_ARGUMENT when the decoder's batch kernel is not the degree-padded one. */
+qb_status qb_soft_vars(const qb_decoder* h, uint32_t* vars /* [num_checks] out */);
+qb_status qb_decode_batch_soft(qb_decoder* h, uint64_t shots, const uint64_t* syndromes,
+                               const void* soft, uint64_t* estimates,
+                               uint64_t* residuals /* may be NULL */, uint8_t* converged,
+                               uint32_t* iterations);
+qb_status qb_decode_batch_soft_device(qb_decoder* h, uint64_t shots,
+                                      const uint64_t* d_syndromes, const void* d_soft,
+                                      uint64_t* d_estimates,
+                                      uint64_t* d_residuals /* may be NULL */,
+                                      uint8_t* d_converged, uint32_t* d_iterations,
+                                      void* stream);
+
+/* Device generator of soft syndromes (BASELINE config 5; the reference has no such noise
+ * model): data variables flip with probability p (or probs[v]; the entries of
+ * absorbed variables are ignored), every check m with an absorbed variable is then measured
+ * through a Gaussian channel  l_m = (1 - 2 s~_m) mu + N(0, sigma^2)  around its noiseless
+ * bit s~_m: d_syndromes receives the hard bits [l_m < 0], d_soft the reliabilities
+ * 2 mu |l_m| / sigma^2 in the decoder's soft format (integer modes: quantised with the
+ * decoder's quant_scale, clamped to [1, kmax]), d_errors (may be NULL) the data errors plus
+ * one error on the absorbed variable of every flipped measurement, so that
+ * H_ext * error == syndrome.  Counter-based stream keyed by (seed, trial, check). */
+qb_status qb_generate_soft_syndromes(qb_decoder* h, uint64_t seed, double p,
+                                     const double* probs, double mu, double sigma,
+                                     uint64_t first_trial, uint64_t shots,
+                                     uint64_t* d_syndromes, void* d_soft,
+                                     uint64_t* d_errors, void* stream);
+
+/* Campaigns on extended graphs.  qb_set_auxiliary_vars marks the variables that are NOT data
+ * qubits (packed mask over num_vars, host memory; NULL clears): for a converged shot
+ * H_ext r = 0 means H r_data = r_aux, so a residual with a bit on an auxiliary variable has
+ * a data part with non-zero syndrome and is counted as a logical error of its component
+ * (the tests of qb_set_logicals then only see data bits).  With a mask set, qb_campaign_run
+ * samples variable v from draw v (no X/Z interleave).  qb_campaign_run_soft is the same
+ * loop with qb_generate_soft_syndromes + qb_decode_batch_soft_device: sample, soft
+ * measurement, decode, classify, all on the device. */
+qb_status qb_set_auxiliary_vars(qb_decoder* h, const uint64_t* mask);
+qb_status qb_campaign_run_soft(qb_decoder* h, uint64_t seed, double p, const double* probs,
+                               double mu, double sigma, uint64_t first_trial,
+                               uint64_t trials, uint64_t* counters);
+
 /* Pinned (page-locked, device-mapped) host memory for batch I/O. */
 qb_status qb_host_alloc(void** out, size_t bytes);
 void qb_host_free(void* p);

@@ -449,3 +449,36 @@ int oracle_decode_many(const oracle_graph *g, const oracle_segment *segs, uint32
   free(is);
   return rc;
 }
+
+/* Soft (noisy) syndromes: priors that change per shot.  The reference takes priors per
+ * Decoder (decoder.hpp:31-32; quantised / stored in the constructor, decoder.cpp:108-131),
+ * so per-shot soft information means one Decoder per shot: shot i is decoded
+ * with the base priors of `cfg` (1.0 when empty) except priors[soft_vars[k]] = soft[i][k].
+ * Everything else is oracle_decode / oracle_decode_many. */
+int oracle_decode_many_soft(const oracle_graph *g, const oracle_segment *segs, uint32_t nseg,
+                            const oracle_config *cfg, uint64_t shots, const uint64_t *syndromes,
+                            const uint32_t *soft_vars, uint32_t nsoft, const double *soft,
+                            uint64_t *estimates, uint64_t *residuals, uint8_t *converged,
+                            uint32_t *iterations, int per_segment) {
+  const uint32_t N = g->num_vars;
+  const uint64_t sw = (g->num_checks + 63) / 64, ew = (N + 63) / 64;
+  const int has_priors = cfg->priors && cfg->num_priors != 0;
+  if (has_priors && cfg->num_priors != N) return ORACLE_INVALID;
+  double *pri = malloc(sizeof(double) * N);
+  for (uint32_t n = 0; n < N; ++n) pri[n] = has_priors ? cfg->priors[n] : 1.0;
+  oracle_config c = *cfg;
+  c.priors = pri;
+  c.num_priors = N;
+  int rc = ORACLE_OK;
+  for (uint64_t i = 0; i < shots && rc == ORACLE_OK; ++i) {
+    for (uint32_t k = 0; k < nsoft; ++k) {
+      if (soft_vars[k] < N) pri[soft_vars[k]] = soft[i * nsoft + k];
+    }
+    rc = oracle_decode_many(g, segs, nseg, &c, 1, syndromes + i * sw, estimates + i * ew,
+                            residuals ? residuals + i * sw : NULL,
+                            converged + i * (per_segment ? nseg : 1),
+                            iterations + i * (per_segment ? nseg : 1), per_segment);
+  }
+  free(pri);
+  return rc;
+}

@@ -142,6 +142,30 @@ class Oracle:
             raise ValueError("oracle: invalid configuration")
         return est, res, conv, its
 
+    def decode_many_soft(self, graph, cfg, syndromes: np.ndarray, soft_vars, soft,
+                         segments=None, per_segment=True):
+        """Per-shot priors: shot i is decoded with cfg's priors except
+        priors[soft_vars[k]] = soft[i][k] (doubles; one reference Decoder per shot)."""
+        g, segs, nseg, c, keep = self._pack(graph, segments, cfg)
+        syn = np.ascontiguousarray(syndromes, dtype=np.uint64)
+        shots = syn.shape[0]
+        sv = np.ascontiguousarray(soft_vars, dtype=np.uint32)
+        so = np.ascontiguousarray(soft, dtype=np.float64).reshape(shots, sv.size)
+        est = np.zeros((shots, _words(graph.num_vars)), dtype=np.uint64)
+        res = np.zeros((shots, _words(graph.num_checks)), dtype=np.uint64)
+        k = nseg if per_segment else 1
+        conv = np.zeros((shots, k), dtype=np.uint8)
+        its = np.zeros((shots, k), dtype=np.uint32)
+        self.lib.oracle_decode_many_soft.restype = C.c_int
+        rc = self.lib.oracle_decode_many_soft(C.byref(g), segs, C.c_uint32(nseg), C.byref(c),
+                                              C.c_uint64(shots), _p(syn, u64p), _p(sv, u32p),
+                                              C.c_uint32(sv.size), _p(so, f64p), _p(est, u64p),
+                                              _p(res, u64p), _p(conv, u8p), _p(its, u32p),
+                                              C.c_int(1 if per_segment else 0))
+        if rc != 0:
+            raise ValueError("oracle: invalid configuration")
+        return est, res, conv, its
+
     # -- node ops (KATs) ------------------------------------------------------
     def check_node_update(self, q: Sequence[float], s_bit: int, alpha: float) -> np.ndarray:
         qa = np.ascontiguousarray(q, dtype=np.float64)
@@ -369,6 +393,24 @@ class Ref:
         self._check(self.lib.ref_decoder_new_graph(graph_or_code.ptr, *args, C.byref(out)))
         return RefDecoder(self, out, graph_or_code.num_checks, graph_or_code.num_vars,
                           keep=graph_or_code)
+
+    def decode_many_soft(self, graph: RefGraph, cfg, syndromes: np.ndarray, soft_vars, soft):
+        """One unmodified reference Decoder PER SHOT with priors[soft_vars[k]] = soft[i][k]
+        (ref_decode_many_soft); single segment, as the reference's graph constructor."""
+        pri, args = self._cfg_args(cfg)
+        syn = np.ascontiguousarray(syndromes, dtype=np.uint64)
+        shots = syn.shape[0]
+        sv = np.ascontiguousarray(soft_vars, dtype=np.uint32)
+        so = np.ascontiguousarray(soft, dtype=np.float64).reshape(shots, sv.size)
+        est = np.zeros((shots, _words(graph.num_vars)), dtype=np.uint64)
+        res = np.zeros((shots, _words(graph.num_checks)), dtype=np.uint64)
+        conv = np.zeros(shots, dtype=np.uint8)
+        its = np.zeros(shots, dtype=np.uint32)
+        self._check(self.lib.ref_decode_many_soft(
+            graph.ptr, *args, _p(sv, u32p), C.c_uint32(sv.size), _p(so, f64p), C.c_uint64(shots),
+            _p(syn, u64p), C.c_uint64(graph.num_checks), _p(est, u64p), _p(res, u64p),
+            _p(conv, u8p), _p(its, u32p)))
+        return est, res, conv, its
 
     def decode_batch(self, graph: RefGraph, syndromes: np.ndarray, cfg, workers: int = 1,
                      bits_each: Optional[Sequence[int]] = None):

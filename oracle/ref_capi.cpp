@@ -346,6 +346,40 @@ int ref_decode_batch(const void* graph, std::uint64_t shots,
   });
 }
 
+// Soft (noisy) syndromes: the reference's priors are per Decoder (decoder.hpp:31-32), so
+// per-shot priors mean ONE Decoder PER SHOT: shot i uses `priors` with
+// priors[soft_vars[k]] = soft[i][k].  Single-segment graph constructor, as ref_decode_many.
+int ref_decode_many_soft(const void* graph, std::uint64_t max_iter, double alpha,
+                         int early, int arith, double quant_scale,
+                         const double* priors, std::uint64_t n_priors,
+                         const std::uint32_t* soft_vars, std::uint32_t nsoft,
+                         const double* soft, std::uint64_t shots,
+                         const std::uint64_t* syndromes, std::uint64_t bits,
+                         std::uint64_t* estimates, std::uint64_t* residuals,
+                         std::uint8_t* converged, std::uint32_t* iterations) {
+  return guarded([&] {
+    const auto* g = static_cast<const TannerGraph*>(graph);
+    DecoderConfig cfg =
+        make_cfg(max_iter, alpha, early, arith, quant_scale, priors, n_priors);
+    if (cfg.priors.empty()) cfg.priors.assign(g->num_vars, 1.0);
+    const std::size_t sw = (bits + 63) / 64;
+    const std::size_t ew = (g->num_vars + 63) / 64;
+    const std::size_t rw = (g->num_checks + 63) / 64;
+    DecodeOutcome out;
+    for (std::uint64_t i = 0; i < shots; ++i) {
+      for (std::uint32_t k = 0; k < nsoft; ++k) {
+        if (soft_vars[k] < g->num_vars) cfg.priors[soft_vars[k]] = soft[i * nsoft + k];
+      }
+      Decoder d(*g, cfg);
+      d.decode_into(vec_from_words(syndromes + i * sw, bits), out);
+      words_from_vec(out.error_estimate, estimates + i * ew);
+      if (residuals) words_from_vec(out.syndrome_residual, residuals + i * rw);
+      converged[i] = out.converged ? 1 : 0;
+      iterations[i] = static_cast<std::uint32_t>(out.iterations_used);
+    }
+  });
+}
+
 // ------------------------------------------------------------- node ops ----
 
 int ref_check_node_update(const double* q, std::uint64_t deg, int s_bit,

@@ -78,6 +78,18 @@ SYMBOLS = {
                                   C.c_uint64, u64p]),
     "qb_classify_batch_device": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
                                            C.c_void_p, C.c_void_p, C.c_void_p, u64p, C.c_void_p]),
+    "qb_soft_vars": (C.c_int, [C.c_void_p, u32p]),
+    "qb_decode_batch_soft": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.c_void_p]),
+    "qb_decode_batch_soft_device": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
+                                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                              C.c_void_p]),
+    "qb_generate_soft_syndromes": (C.c_int, [C.c_void_p, C.c_uint64, C.c_double, f64p, C.c_double,
+                                             C.c_double, C.c_uint64, C.c_uint64, C.c_void_p,
+                                             C.c_void_p, C.c_void_p, C.c_void_p]),
+    "qb_set_auxiliary_vars": (C.c_int, [C.c_void_p, u64p]),
+    "qb_campaign_run_soft": (C.c_int, [C.c_void_p, C.c_uint64, C.c_double, f64p, C.c_double,
+                                       C.c_double, C.c_uint64, C.c_uint64, u64p]),
     "qb_last_kernel_ns": (C.c_uint64, [C.c_void_p]),
     "qb_launch_count": (C.c_uint64, [C.c_void_p]),
 }

@@ -20,7 +20,7 @@ import numpy as np
 from . import _lib
 from .codes import CssCode, SparseMatrix
 from .decoder import Decoder, DecoderConfig, _raise
-from .gf2 import num_words, pack_bits
+from .gf2 import num_words, pack_bits, unpack_bits
 
 COUNTER_NAMES = ("exact", "stabilizer", "logical_x", "logical_z", "logical_both",
                  "non_converged", "baseline_fail", "converged_both", "iteration_sum", "trials")
@@ -153,14 +153,22 @@ def shard(trials: int, world: int, rank: int) -> Tuple[int, int]:
     return rank * trials // world, (rank + 1) * trials // world
 
 
-def reduce_counters(counters: np.ndarray, group=None, device=None) -> np.ndarray:
-    """Sum of the counter vectors of every rank; identity without a process group."""
+def reduce_counters(counters: np.ndarray, group=None, device=None, world: int = 1) -> np.ndarray:
+    """Sum of the counter vectors of every rank (one all_reduce; the analogue of the
+    reference's integer sum over workers, noise.cpp:306-324).  Without a process group this
+    is the identity for world == 1 and an ERROR for world > 1: returning one shard's
+    counters as if they were the campaign's would look valid and be wrong."""
     try:
         import torch
         import torch.distributed as dist
     except ImportError:  # pragma: no cover
+        if world > 1:
+            raise RuntimeError("reduce_counters: world > 1 needs torch.distributed")
         return counters
     if not (dist.is_available() and dist.is_initialized()):
+        if world > 1:
+            raise RuntimeError("reduce_counters: world > 1 but no process group is initialised "
+                               "(torch.distributed.init_process_group)")
         return counters
     t = torch.as_tensor(np.asarray(counters, dtype=np.int64))
     if device is not None:
@@ -208,20 +216,152 @@ class Campaign:
 
 
 def run_campaign(code: CssCode, p: float, seed: int, trials: int, cfg: DecoderConfig,
-                 device: int = 0, world: int = 1, rank: int = 0, group=None) -> CampaignResult:
+                 device: int = 0, world: int = 1, rank: int = 0, group=None,
+                 range_fn=None, reduce_device="cuda") -> CampaignResult:
     """reference: run_campaign(code, NoiseModel{independent-xz, p, seed}, trials, cfg).
     With world > 1 every rank calls this with its own `rank`; all ranks return the
-    same aggregated result."""
+    same aggregated result (contiguous shard per rank, noise.cpp:253-254, then ONE
+    all_reduce of the ten counters).
+
+    `range_fn(p, seed, first_trial, trials) -> counters` replaces the device decoder for the
+    rank's trial range (tests drive this very function on CPU ranks over gloo, with
+    `reduce_device="cpu"`); the default builds a Campaign on `device`."""
     if not (0.0 <= p <= 1.0):
         raise ValueError("NoiseModel: p must lie in [0, 1]")
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("run_campaign: rank must lie in [0, world)")
     lo, hi = shard(trials, world, rank)
-    camp = Campaign(code, cfg, device=device)
+    camp = None
+    if range_fn is None:
+        camp = Campaign(code, cfg, device=device)
+        range_fn = camp.run_range
     try:
-        counters = camp.run_range(p, seed, lo, hi - lo) if hi > lo else \
+        counters = np.asarray(range_fn(p, seed, lo, hi - lo), dtype=np.uint64) if hi > lo else \
             np.zeros(len(COUNTER_NAMES), dtype=np.uint64)
     finally:
-        camp.close()
+        if camp is not None:
+            camp.close()
     if world > 1:
         import torch
-        counters = reduce_counters(counters, group, torch.device("cuda", device))
+        dev = torch.device("cuda", device) if reduce_device == "cuda" else torch.device("cpu")
+        counters = reduce_counters(counters, group, dev, world=world)
     return CampaignResult.from_counters(counters)
+
+
+# ---- BASELINE config 5: phenomenological noise on the extended graph ---------------------
+
+class PhenomenologicalCampaign:
+    """Campaigns on diag([Hz | I], [Hx | I]) (codes.extended_graph): data qubits flip with
+    probability p, every measured syndrome bit is noisy - either flipped with probability q
+    (hard syndromes, constant prior ln((1-q)/q) on the measurement-error variables) or read
+    through a Gaussian channel (soft syndromes, per-shot priors |LLR_m|).  Sample, measure,
+    decode and classify all run on the device (qb_campaign_run / qb_campaign_run_soft).
+
+    A trial FAILS unless both components converge and the data residual has zero syndrome
+    and is no logical operator; in the ten counters a data residual with non-zero syndrome
+    is booked as a logical error of its component.  The reference has no such noise model
+    (SPEC.md:15): this is new-build behaviour on top of its decoder semantics."""
+
+    def __init__(self, code: CssCode, cfg: DecoderConfig, p_data: float, p_meas: float,
+                 device: int = 0):
+        from .codes import build_tanner_graph, extended_graph
+        self.code = code
+        h, segs = extended_graph(code)
+        self.h_ext, self.segments = h, segs
+        self.graph = build_tanner_graph(h)
+        n, mz, mx = code.n, code.hz.rows, code.hx.rows
+        self.data_slices = (slice(0, n), slice(n + mz, 2 * n + mz))
+        self.p_data, self.p_meas = float(p_data), float(p_meas)
+        if cfg.priors is None:
+            llr_d = float(np.log((1 - p_data) / p_data))
+            llr_m = float(np.log((1 - p_meas) / p_meas))
+            pri = np.concatenate([np.full(n, llr_d), np.full(mz, llr_m), np.full(n, llr_d),
+                                  np.full(mx, llr_m)])
+            cfg = dataclasses.replace(cfg, priors=pri.tolist())
+        self.probs = np.concatenate([np.full(n, p_data), np.full(mz, p_meas), np.full(n, p_data),
+                                     np.full(mx, p_meas)])
+        self.decoder = Decoder(self.graph, cfg, device=device, segments=segs)
+        lib = _lib.load()
+        tx, tz = residual_tests(code)  # over 2n bits: place the data parts in the extended layout
+        bx, bz = unpack_bits(tx, 2 * n), unpack_bits(tz, 2 * n)
+        nv = self.graph.num_vars
+        ex = np.zeros((bx.shape[0], nv), dtype=np.uint8)
+        ez = np.zeros((bz.shape[0], nv), dtype=np.uint8)
+        ex[:, self.data_slices[0]] = bx[:, :n]
+        ez[:, self.data_slices[1]] = bz[:, n:]
+        self.tests_bits = (ex, ez)
+        self._tests = (np.ascontiguousarray(pack_bits(ex)), np.ascontiguousarray(pack_bits(ez)))
+        st = lib.qb_set_logicals(self.decoder._h, self._tests[0].ctypes.data_as(_lib.u64p),
+                                 self._tests[0].shape[0],
+                                 self._tests[1].ctypes.data_as(_lib.u64p), self._tests[1].shape[0])
+        if st != _lib.QB_OK:
+            _raise(st, self.decoder._h)
+        aux = np.ones(nv, dtype=np.uint8)
+        aux[self.data_slices[0]] = 0
+        aux[self.data_slices[1]] = 0
+        self.aux_bits = aux
+        self._aux = np.ascontiguousarray(pack_bits(aux))
+        st = lib.qb_set_auxiliary_vars(self.decoder._h, self._aux.ctypes.data_as(_lib.u64p))
+        if st != _lib.QB_OK:
+            _raise(st, self.decoder._h)
+
+    def run_range(self, seed: int, first_trial: int, trials: int) -> np.ndarray:
+        """Hard noisy syndromes: every variable v flips with probs[v]."""
+        counters = np.zeros(len(COUNTER_NAMES), dtype=np.uint64)
+        st = _lib.load().qb_campaign_run(self.decoder._h, seed, 0.0,
+                                         self.probs.ctypes.data_as(_lib.f64p), first_trial, trials,
+                                         counters.ctypes.data_as(_lib.u64p))
+        if st != _lib.QB_OK:
+            _raise(st, self.decoder._h)
+        return counters
+
+    def run_range_soft(self, seed: int, mu: float, sigma: float, first_trial: int,
+                       trials: int) -> np.ndarray:
+        """Soft syndromes: data flips at p_data, Gaussian measurement channel (mu, sigma)."""
+        counters = np.zeros(len(COUNTER_NAMES), dtype=np.uint64)
+        st = _lib.load().qb_campaign_run_soft(self.decoder._h, seed, self.p_data, None, float(mu),
+                                              float(sigma), first_trial, trials,
+                                              counters.ctypes.data_as(_lib.u64p))
+        if st != _lib.QB_OK:
+            _raise(st, self.decoder._h)
+        return counters
+
+    def host_counters(self, err_bits: np.ndarray, est_bits: np.ndarray, conv: np.ndarray,
+                      its: np.ndarray, syn_bits: np.ndarray) -> np.ndarray:
+        """The classification rule restated on the host (numpy), for tests."""
+        c = np.zeros(len(COUNTER_NAMES), dtype=np.uint64)
+        r = err_bits ^ est_bits
+        segs = [(int(a), int(b), int(v0), int(v1)) for a, b, v0, v1 in self.segments]
+        both = conv.min(axis=1) == 1
+        harmful, base_harmful = [], []
+        for k, (c0, c1, v0, v1) in enumerate(segs):
+            t = self.tests_bits[k].astype(np.int32)
+            def bad(vec, need_zero_syn):
+                seg = np.zeros_like(vec)
+                seg[:, v0:v1] = vec[:, v0:v1]
+                zero = ~seg.any(axis=1)
+                aux = (seg & self.aux_bits[None, :]).any(axis=1)
+                odd = ((seg.astype(np.int32) @ t.T) & 1).any(axis=1)
+                out = ~zero & (aux | odd)
+                if need_zero_syn is not None:
+                    out = ~zero & (need_zero_syn | aux | odd)
+                return out, zero
+            h_r, zero_r = bad(r, None)
+            h_e, _ = bad(err_bits, syn_bits[:, c0:c1].any(axis=1))
+            harmful.append((h_r, zero_r))
+            base_harmful.append(h_e)
+        (hx, zx), (hz, zz) = harmful
+        c[0] = int((both & zx & zz).sum())
+        c[1] = int((both & ~(zx & zz) & ~hx & ~hz).sum())
+        c[2] = int((both & hx & ~hz).sum())
+        c[3] = int((both & ~hx & hz).sum())
+        c[4] = int((both & hx & hz).sum())
+        c[5] = int((~both).sum())
+        c[6] = int((base_harmful[0] | base_harmful[1]).sum())
+        c[7] = int(both.sum())
+        c[8] = int(its.max(axis=1).astype(np.uint64).sum())
+        c[9] = err_bits.shape[0]
+        return c
+
+    def close(self) -> None:
+        self.decoder.close()

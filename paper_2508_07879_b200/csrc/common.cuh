@@ -94,6 +94,12 @@ struct ShotIO {
   // debug dumps of the final edge messages (nullptr unless qb_decode_debug)
   void* q_dump;
   void* r_dump;
+  // per-shot priors of the absorbed degree-1 variables ("soft syndromes", kernel_ell.cuh):
+  // [nshots][M] float (float / half modes), int8 (int8) or int16 (int16); nullptr = none
+  const void* soft;
+  uint32_t soft_bytes;  // element size of `soft`: 4, 1 or 2
+  // batch kernels: also dump the messages of shot `dump_shot` to q_dump / r_dump
+  uint32_t dump_shot;
 };
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {

@@ -25,6 +25,11 @@ struct ClassifyParams {
   const uint32_t* tests_x;  // [n_x][est_w32]: odd overlap => X residual is a logical error
   const uint32_t* tests_z;  // [n_z][est_w32]
   uint32_t n_x, n_z;
+  // optional [est_w32]: variables that are NOT data qubits (the measurement-error variables of
+  // an extended graph [H | I]).  H_ext r = 0 for a converged residual r means H r_data = r_aux,
+  // so a residual with a bit on an auxiliary variable has a data part with NON-ZERO syndrome:
+  // it counts as a logical error of its component (qb_set_auxiliary_vars).
+  const uint32_t* aux_mask;
   unsigned long long* counters;  // [10], see qb_campaign_run
 };
 
@@ -57,6 +62,7 @@ classify_kernel(const __grid_constant__ DecodeParams P, const __grid_constant__ 
   for (uint64_t shot = static_cast<uint64_t>(blockIdx.x) * kClassifyWarps + warp; shot < cp.nshots;
        shot += stride) {
     bool ex_zero = true, ez_zero = true, rx_zero = true, rz_zero = true;
+    bool ex_aux = false, ez_aux = false, rx_aux = false, rz_aux = false;
     for (uint32_t w = lane; w < P.est_w32; w += 32u) {
       const uint32_t e = cp.err[shot * P.est_w32 + w];
       const uint32_t r = e ^ cp.est[shot * P.est_w32 + w];
@@ -67,11 +73,22 @@ classify_kernel(const __grid_constant__ DecodeParams P, const __grid_constant__ 
       ez_zero = ez_zero && (e & mz) == 0;
       rx_zero = rx_zero && (r & mx) == 0;
       rz_zero = rz_zero && (r & mz) == 0;
+      if (cp.aux_mask) {
+        const uint32_t am = cp.aux_mask[w];
+        ex_aux = ex_aux || (e & mx & am) != 0;
+        ez_aux = ez_aux || (e & mz & am) != 0;
+        rx_aux = rx_aux || (r & mx & am) != 0;
+        rz_aux = rz_aux || (r & mz & am) != 0;
+      }
     }
     ex_zero = __all_sync(0xffffffffu, ex_zero);
     ez_zero = __all_sync(0xffffffffu, ez_zero);
     rx_zero = __all_sync(0xffffffffu, rx_zero);
     rz_zero = __all_sync(0xffffffffu, rz_zero);
+    ex_aux = __any_sync(0xffffffffu, ex_aux);
+    ez_aux = __any_sync(0xffffffffu, ez_aux);
+    rx_aux = __any_sync(0xffffffffu, rx_aux);
+    rz_aux = __any_sync(0xffffffffu, rz_aux);
     bool sx_zero = true, sz_zero = true;
     for (uint32_t w = lane; w < P.syn_w32; w += 32u) {
       const uint32_t sw = cp.syn[shot * P.syn_w32 + w];
@@ -90,18 +107,18 @@ classify_kernel(const __grid_constant__ DecodeParams P, const __grid_constant__ 
         cls = 0;  // exact
       } else {
         const bool x_harmless =
-            rx_zero || !any_odd_overlap(cp.tests_x, cp.n_x, resid, P.est_w32, lane);
+            rx_zero || (!rx_aux && !any_odd_overlap(cp.tests_x, cp.n_x, resid, P.est_w32, lane));
         const bool z_harmless =
-            rz_zero || !any_odd_overlap(cp.tests_z, cp.n_z, resid, P.est_w32, lane);
+            rz_zero || (!rz_aux && !any_odd_overlap(cp.tests_z, cp.n_z, resid, P.est_w32, lane));
         cls = (x_harmless && z_harmless) ? 1 : (!x_harmless && !z_harmless) ? 4 : x_harmless ? 3 : 2;
       }
     }
     // identity decoder on the same error: e is harmless iff it has zero syndrome and
     // even overlap with every logical of the opposite type
     const bool bx_harmless =
-        ex_zero || (sx_zero && !any_odd_overlap(cp.tests_x, cp.n_x, error, P.est_w32, lane));
+        ex_zero || (sx_zero && !ex_aux && !any_odd_overlap(cp.tests_x, cp.n_x, error, P.est_w32, lane));
     const bool bz_harmless =
-        ez_zero || (sz_zero && !any_odd_overlap(cp.tests_z, cp.n_z, error, P.est_w32, lane));
+        ez_zero || (sz_zero && !ez_aux && !any_odd_overlap(cp.tests_z, cp.n_z, error, P.est_w32, lane));
     if (lane == 0) {
       atomicAdd(&local[cls], 1ull);
       if (!(bx_harmless && bz_harmless)) atomicAdd(&local[6], 1ull);

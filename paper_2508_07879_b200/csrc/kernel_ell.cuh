@@ -285,11 +285,34 @@ __device__ __forceinline__ uint32_t vn_ell(const DecodeParams& P, ArithI32, unsi
   return vn_ell_int<ArithI32, DC, DV>(P, base, eo, gamma);
 }
 
+// ---- per-shot priors of the absorbed variables ("soft syndromes") -------------------
+// ShotIO::soft holds, for every shot, one value per check: the prior of the degree-1
+// variable that check absorbs (on [H | I] graphs the measurement-error variable of that
+// check, i.e. the reliability |LLR| of the measured syndrome bit).  Element type by mode:
+// float (float / half), int8 (int8), int16 (int16) - the integer values are the already
+// quantised priors, what the reference's quantize_saturate (decoder.cpp:115-122) yields.
+template <class A>
+__device__ __forceinline__ typename A::Msg load_soft(const ShotIO& io, uint64_t idx);
+template <>
+__device__ __forceinline__ float load_soft<ArithF32>(const ShotIO& io, uint64_t idx) {
+  return static_cast<const float*>(io.soft)[idx] + 0.0f;  // -0.0 -> +0.0, as the loader does
+}
+template <>
+__device__ __forceinline__ __half load_soft<ArithF16>(const ShotIO& io, uint64_t idx) {
+  return prior_as_msg<ArithF16>(static_cast<const float*>(io.soft)[idx]);
+}
+template <>
+__device__ __forceinline__ int32_t load_soft<ArithI32>(const ShotIO& io, uint64_t idx) {
+  return io.soft_bytes == 1u ? static_cast<int32_t>(static_cast<const int8_t*>(io.soft)[idx])
+                             : static_cast<int32_t>(static_cast<const int16_t*>(io.soft)[idx]);
+}
+
 // ---- the kernel -------------------------------------------------------------------
 // Work item = (shot, segment); a CTA serves one segment for its whole life and
 // draws shots from that segment's ticket queue (as decode_lean_kernel).
+// kSoft: the absorbed variables' priors come per shot from ShotIO::soft.
 
-template <class A, int DC, int DV, int CPT, int VPT, int MAXT, int MINB>
+template <class A, int DC, int DV, int CPT, int VPT, int MAXT, int MINB, bool kSoft = false>
 __global__ void __launch_bounds__(MAXT, MINB)
 decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant__ ShotIO io) {
   static_assert(DV <= DC, "padded variable slots live in the q half of the zero block");
@@ -388,6 +411,19 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
   if (warp == 0 && lane < gspan && shot < io.nshots) {
     raw_next = io.syn[shot * P.syn_w32 + gw0 + lane];
   }
+  // per-shot priors of this thread's absorbed variables, fetched one shot ahead
+  Msg soft_next[kSoft ? CPT : 1];
+  auto fetch_soft = [&](uint64_t sh) {
+    if constexpr (kSoft) {
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        if (cl[k] < Ms && ((absorb >> (8 * k)) & 0xffu) != kNoAbsorb) {
+          soft_next[k] = load_soft<A>(io, sh * P.M + seg.c0 + cl[k]);
+        }
+      }
+    }
+  };
+  if (shot < io.nshots) fetch_soft(shot);
   uint32_t ipar = 0;
   __syncthreads();
 
@@ -431,6 +467,15 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
 #pragma unroll
       for (int i = 0; i < DV; ++i) *reinterpret_cast<Msg*>(msgs + eo[k][i]) = init;
     }
+    if constexpr (kSoft) {  // this shot's priors of the absorbed variables: q = gamma for the whole decode
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        const uint32_t aslot = (absorb >> (8 * k)) & 0xffu;
+        if (cl[k] < Ms && aslot != kNoAbsorb) {
+          *reinterpret_cast<Msg*>(msgs + co[k] + aslot * kMsg) = soft_next[k];
+        }
+      }
+    }
     uint32_t eprev = 0, aprev = 0;  // decisions of this thread's variables / absorbed variables
     __syncthreads();
 
@@ -441,6 +486,7 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
     if (warp == 0 && lane < gspan && next != kNoShot) {  // prefetch the next shot's syndrome
       raw_next = io.syn[static_cast<uint64_t>(next) * P.syn_w32 + gw0 + lane];
     }
+    if (next != kNoShot) fetch_soft(next);
 
     // ---------------- iterations ----------------
     uint32_t iter = 0;
@@ -448,7 +494,10 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
     for (;;) {
       ++iter;
       uint32_t eb = 0;
-      int32_t adelta = 0;
+      // Bitmap and counter are only WRITTEN between the two barriers of an iteration and only
+      // READ (the stop test) between the second barrier and the next iteration's first one:
+      // the flips of absorbed variables found in the check stage wait in `achg` until then.
+      uint32_t achg = 0;
 #pragma unroll
       for (int k = 0; k < CPT; ++k) {
         cn_ell<DC>(P, A{}, msgs + co[k], (synbits >> k) & 1u);
@@ -457,15 +506,10 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
           const unsigned char* slot = msgs + co[k] + aslot * kMsg;
           const uint32_t e = absorbed_decision(A{}, *reinterpret_cast<const Msg*>(slot),
                                                *reinterpret_cast<const Msg*>(slot + DC * kMsg));
-          if (e != ((aprev >> k) & 1u)) {  // it flips the parity of its one check
-            aprev ^= 1u << k;
-            const uint32_t bit = 1u << (cl[k] & 31u);
-            const uint32_t old = atomicXor(&par[cl[k] >> 5], bit);
-            adelta += (old & bit) ? -1 : 1;
-          }
+          achg |= (e ^ ((aprev >> k) & 1u)) << k;  // it flips the parity of its one check
         }
       }
-      if (adelta) atomicAdd(const_cast<uint32_t*>(unsat), static_cast<uint32_t>(adelta));
+      aprev ^= achg;
       __syncthreads();
 #pragma unroll
       for (int k = 0; k < VPT; ++k) {
@@ -474,8 +518,16 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
       eb &= valid;
       const uint32_t changed = eb ^ eprev;
       eprev = eb;
-      if (changed) {  // a hard decision flipped: toggle its checks, keep the counter exact
+      if (changed | achg) {  // a hard decision flipped: toggle its checks, keep the counter exact
         int32_t delta = 0;
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+          if ((achg >> k) & 1u) {
+            const uint32_t bit = 1u << (cl[k] & 31u);
+            const uint32_t old = atomicXor(&par[cl[k] >> 5], bit);
+            delta += (old & bit) ? -1 : 1;
+          }
+        }
 #pragma unroll
         for (int k = 0; k < VPT; ++k) {
           if ((changed >> k) & 1u) {

@@ -90,7 +90,7 @@ __device__ __forceinline__ uint32_t vn_ell_h2(unsigned char* base, const uint32_
   return h22u(total) & 0x80008000u;
 }
 
-template <int DC, int DV, int CPT, int VPT, int MAXT, int MINB, bool kI8>
+template <int DC, int DV, int CPT, int VPT, int MAXT, int MINB, bool kI8, bool kSoft = false>
 __global__ void __launch_bounds__(MAXT, MINB)
 decode_ell_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_constant__ ShotIO io) {
   static_assert(DV <= DC, "padded variable slots live in the q half of the zero block");
@@ -195,6 +195,30 @@ decode_ell_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_consta
     raw_a = io.syn[(2 * pair) * P.syn_w32 + gw0 + lane];
     if (2 * pair + 1 < io.nshots) raw_b = io.syn[(2 * pair + 1) * P.syn_w32 + gw0 + lane];
   }
+  // per-shot priors of this thread's absorbed variables (ShotIO::soft: int8 in int8 mode,
+  // float in half mode), both shots of the pair in one half2, fetched one pair ahead
+  uint32_t soft_next[kSoft ? CPT : 1];
+  auto soft_h = [&](uint64_t idx) -> __half {
+    if constexpr (kI8) {
+      return __float2half_rn(static_cast<float>(static_cast<const int8_t*>(io.soft)[idx]));  // exact
+    } else {
+      return prior_as_msg<ArithF16>(static_cast<const float*>(io.soft)[idx]);
+    }
+  };
+  auto fetch_soft = [&](uint64_t pr) {
+    if constexpr (kSoft) {
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        if (cl[k] < Ms && ((absorb >> (8 * k)) & 0xffu) != kNoAbsorb) {
+          const uint64_t ia = (2 * pr) * P.M + seg.c0 + cl[k];
+          const __half a = soft_h(ia);
+          const __half b = 2 * pr + 1 < io.nshots ? soft_h(ia + P.M) : a;
+          soft_next[k] = h22u(__halves2half2(a, b));
+        }
+      }
+    }
+  };
+  if (pair < npairs) fetch_soft(pair);
   uint32_t ipar = 0;
   __syncthreads();
 
@@ -252,6 +276,15 @@ decode_ell_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_consta
 #pragma unroll
       for (int i = 0; i < DV; ++i) *reinterpret_cast<__half2*>(msgs + eo[k][i]) = init;
     }
+    if constexpr (kSoft) {  // this pair's priors of the absorbed variables
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        const uint32_t aslot = (absorb >> (8 * k)) & 0xffu;
+        if (cl[k] < Ms && aslot != kNoAbsorb) {
+          *reinterpret_cast<uint32_t*>(msgs + co[k] + aslot * kMsg) = soft_next[k];
+        }
+      }
+    }
     uint32_t eprev_a = 0, eprev_b = 0, aprev_a = 0, aprev_b = 0;
     __syncthreads();
 
@@ -271,6 +304,7 @@ decode_ell_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_consta
         if (na + 1 < io.nshots) raw_b = io.syn[(na + 1) * P.syn_w32 + gw0 + lane];
       }
     }
+    if (next != kNoShot) fetch_soft(next);
 
     // ---------------- iterations ----------------
     uint32_t iter = 0, iter_a = 0, iter_b = 0;
@@ -278,7 +312,10 @@ decode_ell_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_consta
     uint32_t fin_a = 0, fin_b = 0, afin_a = 0, afin_b = 0;  // decisions when each shot stopped
     for (;;) {
       ++iter;
-      int32_t ad_a = 0, ad_b = 0;
+      // Bitmaps and counters are only WRITTEN between the two barriers of an iteration and
+      // only READ (the stop test) after the second one: flips of absorbed variables found in
+      // the check stage wait in achg_a / achg_b until the variable stage's toggles.
+      uint32_t achg_a = 0, achg_b = 0;
 #pragma unroll
       for (int k = 0; k < CPT; ++k) {
         cn_ell_h2<DC, kI8>(P, msgs + co[k], synpair[k]);
@@ -287,22 +324,14 @@ decode_ell_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_consta
           const unsigned char* slot = msgs + co[k] + aslot * kMsg;
           const uint32_t sg = h22u(__hadd2(*reinterpret_cast<const __half2*>(slot),
                                            *reinterpret_cast<const __half2*>(slot + DC * kMsg)));
-          const uint32_t ea = (sg >> 15) & 1u, ebb = sg >> 31;
-          const uint32_t bit = 1u << (cl[k] & 31u);
-          if (live_a && ea != ((aprev_a >> k) & 1u)) {
-            aprev_a ^= 1u << k;
-            const uint32_t old = atomicXor(&par_a[cl[k] >> 5], bit);
-            ad_a += (old & bit) ? -1 : 1;
-          }
-          if (live_b && ebb != ((aprev_b >> k) & 1u)) {
-            aprev_b ^= 1u << k;
-            const uint32_t old = atomicXor(&par_b[cl[k] >> 5], bit);
-            ad_b += (old & bit) ? -1 : 1;
-          }
+          achg_a |= (((sg >> 15) & 1u) ^ ((aprev_a >> k) & 1u)) << k;
+          achg_b |= ((sg >> 31) ^ ((aprev_b >> k) & 1u)) << k;
         }
       }
-      if (ad_a) atomicAdd(const_cast<uint32_t*>(unsat_a), static_cast<uint32_t>(ad_a));
-      if (ad_b) atomicAdd(const_cast<uint32_t*>(unsat_b), static_cast<uint32_t>(ad_b));
+      if (!live_a) achg_a = 0;
+      if (!live_b) achg_b = 0;
+      aprev_a ^= achg_a;
+      aprev_b ^= achg_b;
       __syncthreads();
       // posterior sign bits (bits 15 / 31) shift into one accumulator: after VPT variables
       // shot a's decisions sit in bits [16-VPT, 15], shot b's in [32-VPT, 31]
@@ -316,8 +345,16 @@ decode_ell_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_consta
       uint32_t eb_a = (acc >> (16 - VPT)) & ((1u << VPT) - 1u), eb_b = acc >> (32 - VPT);
       eb_a &= valid;
       eb_b &= valid;
-      auto toggle = [&](uint32_t changed, uint32_t* par, volatile uint32_t* ctr) {
+      auto toggle = [&](uint32_t changed, uint32_t achg, uint32_t* par, volatile uint32_t* ctr) {
         int32_t delta = 0;
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+          if ((achg >> k) & 1u) {
+            const uint32_t bit = 1u << (cl[k] & 31u);
+            const uint32_t old = atomicXor(&par[cl[k] >> 5], bit);
+            delta += (old & bit) ? -1 : 1;
+          }
+        }
 #pragma unroll
         for (int k = 0; k < VPT; ++k) {
           if ((changed >> k) & 1u) {
@@ -337,12 +374,12 @@ decode_ell_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_consta
       if (live_a) {
         const uint32_t ch = eb_a ^ eprev_a;
         eprev_a = eb_a;
-        if (ch) toggle(ch, par_a, unsat_a);
+        if (ch | achg_a) toggle(ch, achg_a, par_a, unsat_a);
       }
       if (live_b) {
         const uint32_t ch = eb_b ^ eprev_b;
         eprev_b = eb_b;
-        if (ch) toggle(ch, par_b, unsat_b);
+        if (ch | achg_b) toggle(ch, achg_b, par_b, unsat_b);
       }
       __syncthreads();
       const bool last = iter >= P.max_iter;

@@ -180,4 +180,88 @@ __global__ void noise_skip_kernel(const __grid_constant__ DecodeParams P,
   }
 }
 
+
+// ---- soft (noisy) syndrome measurement: BASELINE config 5 ---------------------------
+//
+// Acts in place on the output of the samplers above when only the DATA variables of an
+// extended graph [H | I] were allowed to flip, so that `syn` holds the noiseless syndrome
+// s~ = H e_data.  Every check m is then "measured" through a Gaussian channel
+//
+//   l_m = (1 - 2 s~_m) * mu + sigma * g,   g ~ N(0, 1)
+//
+// and replaced by what a soft-input decoder sees: the hard bit s_m = [l_m < 0] and the
+// reliability |LLR_m| = 2 mu |l_m| / sigma^2, which becomes the per-shot prior of check m's
+// absorbed measurement-error variable (ShotIO::soft).  A flipped measurement (s_m != s~_m)
+// is recorded as an error on that variable, so that err still satisfies H_ext err = syn.
+// The reference has no such model; the stream is a counter-based SplitMix64
+// keyed by (seed, trial, check), Box-Muller in fp64 - independent of the launch partition.
+struct SoftParams {
+  uint64_t seed;
+  uint64_t first_trial;
+  uint64_t nshots;
+  double mu, sigma;
+  double llr_scale;     // 2 mu / sigma^2
+  double quant_scale;   // integer modes: prior = clamp(round(LLR * quant_scale), 1, kmax)
+  int32_t kmax;         // 0: float output
+  uint32_t elem_bytes;  // 4 (float), 1 (int8), 2 (int16)
+  uint32_t* syn;        // [nshots][syn_w32] in: s~, out: s
+  uint32_t* err;        // [nshots][est_w32] or nullptr: measurement flips are ORed in
+  void* soft;           // [nshots][M] out
+};
+
+constexpr uint64_t kSoftSalt = 0x5851F42D4C957F2Dull;
+
+__global__ void __launch_bounds__(kNoiseWarps * 32)
+soft_measure_kernel(const __grid_constant__ DecodeParams P, const __grid_constant__ SoftParams sp) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kNoiseWarps;
+  const uint32_t M = P.M;
+  for (uint64_t shot = static_cast<uint64_t>(blockIdx.x) * kNoiseWarps + warp; shot < sp.nshots;
+       shot += stride) {
+    const uint64_t trial = sp.first_trial + shot;
+    const uint64_t state0 = splitmix_mix((sp.seed ^ kSoftSalt) + kPhi * trial + kPhi);
+    for (uint32_t w = 0; w < P.syn_w32; ++w) {
+      const uint32_t m = w * 32u + lane;
+      const uint32_t in = sp.syn[shot * P.syn_w32 + w];
+      bool s = m < M && ((in >> lane) & 1u);
+      // only a check with an absorbed measurement-error variable is measured noisily; any
+      // other check keeps its bit (its soft value is never read by the decoder)
+      const uint32_t slot = m < M ? P.ell_abs[m] : kNoAbsorb;
+      if (slot != kNoAbsorb) {
+        const uint64_t z1 = splitmix_mix(state0 + static_cast<uint64_t>(2u * m + 1u) * kPhi);
+        const uint64_t z2 = splitmix_mix(state0 + static_cast<uint64_t>(2u * m + 2u) * kPhi);
+        const double u1 = (static_cast<double>(z1 >> 12) + 0.5) * 0x1p-52;  // in (0, 1)
+        const double u2 = (static_cast<double>(z2 >> 12) + 0.5) * 0x1p-52;
+        const double g = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+        const bool s0 = (in >> lane) & 1u;
+        const double l = (s0 ? -sp.mu : sp.mu) + sp.sigma * g;
+        s = l < 0.0;
+        const double llr = sp.llr_scale * fabs(l);
+        const uint64_t idx = shot * M + m;
+        if (sp.kmax == 0) {
+          static_cast<float*>(sp.soft)[idx] = static_cast<float>(llr);
+        } else {
+          // quantize_saturate (decoder.cpp:500-509) with the reference's "must not be 0" rule
+          // (decoder.cpp:115-120) enforced by clamping up to 1
+          const double scaled = llr * sp.quant_scale;
+          int32_t q = scaled >= static_cast<double>(sp.kmax) ? sp.kmax
+                                                             : static_cast<int32_t>(llrint(scaled));
+          q = q < 1 ? 1 : q;
+          if (sp.elem_bytes == 1u) {
+            static_cast<int8_t*>(sp.soft)[idx] = static_cast<int8_t>(q);
+          } else {
+            static_cast<int16_t*>(sp.soft)[idx] = static_cast<int16_t>(q);
+          }
+        }
+        if (s != s0 && sp.err) {  // a measurement flip: an error on the check's absorbed variable
+          const uint32_t v = P.edge_var[P.check_off[m] + slot];
+          atomicOr(&sp.err[shot * P.est_w32 + (v >> 5)], 1u << (v & 31u));
+        }
+      }
+      const uint32_t out = __ballot_sync(0xffffffffu, s);
+      if (lane == 0) sp.syn[shot * P.syn_w32 + w] = out;
+    }
+  }
+}
+
 }  // namespace qb

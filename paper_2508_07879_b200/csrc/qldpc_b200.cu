@@ -90,6 +90,7 @@ constexpr int kSchedWords = 2 + kMaxSegments;      // scheduler words per concur
 
 struct LaunchPlan {
   KernelFn kernel = nullptr;
+  KernelFn kernel_soft = nullptr;  // same shape, per-shot priors of the absorbed variables
   const char* name = "";
   bool regular = false;
   bool cluster = false;
@@ -141,6 +142,12 @@ struct qb_decoder {
   uint32_t n_tests_x = 0, n_tests_z = 0;
   uint32_t* c_err = nullptr;  // [batch_cap][est_w32] sampled errors
   unsigned long long* d_counters = nullptr;
+  // per-shot priors of the absorbed variables ("soft syndromes")
+  unsigned char* b_soft = nullptr;       // [batch_cap][M] elements of soft_bytes
+  uint32_t soft_bytes = 4;               // 4 float (float / half), 1 int8, 2 int16
+  double quant_scale = 0.0;              // integer modes: the scale priors were quantised with
+  std::vector<uint32_t> soft_var;        // [M] variable whose prior soft[m] replaces, or ~0u
+  uint32_t* d_aux_mask = nullptr;        // [est_w32] non-data variables (qb_set_auxiliary_vars)
 
   // options
   int64_t opt_kernel = 0, opt_latency_io = 0, opt_latency_shape = 0, opt_group_threads = 0,
@@ -205,7 +212,9 @@ void free_batch(qb_decoder* h) {
   cudaFree(h->b_iters);
   cudaFree(h->b_conv);
   cudaFree(h->c_err);
+  cudaFree(h->b_soft);
   h->c_err = nullptr;
+  h->b_soft = nullptr;
   h->b_syn = h->b_est = h->b_res = h->b_iters = nullptr;
   h->b_conv = nullptr;
   h->batch_cap = 0;
@@ -233,6 +242,7 @@ void destroy(qb_decoder* h) {
   cudaFree(h->d_tests_x);
   cudaFree(h->d_tests_z);
   cudaFree(h->d_counters);
+  cudaFree(h->d_aux_mask);
   if (h->h_db) cudaFreeHost(h->h_db);
   if (h->h_rec) cudaFreeHost(h->h_rec);
   cudaFree(h->d_rec_dev);
@@ -478,14 +488,14 @@ constexpr EllVariant kEllVariants[] = {
 };
 constexpr int kNumEllVariants = sizeof(kEllVariants) / sizeof(kEllVariants[0]);
 
-template <class A>
+template <class A, bool kSoft = false>
 KernelFn ell_kernel_t(int idx) {
   switch (idx) {
-    case 0: return decode_ell_kernel<A, 4, 2, 1, 2, 1024, 1>;
-    case 1: return decode_ell_kernel<A, 7, 3, 3, 5, 192, 5>;
-    case 2: return decode_ell_kernel<A, 7, 3, 3, 5, 320, 3>;
-    case 3: return decode_ell_kernel<A, 8, 4, 2, 4, 512, 2>;
-    default: return decode_ell_kernel<A, 12, 6, 1, 2, 1024, 1>;
+    case 0: return decode_ell_kernel<A, 4, 2, 1, 2, 1024, 1, kSoft>;
+    case 1: return decode_ell_kernel<A, 7, 3, 3, 5, 192, 5, kSoft>;
+    case 2: return decode_ell_kernel<A, 7, 3, 3, 5, 320, 3, kSoft>;
+    case 3: return decode_ell_kernel<A, 8, 4, 2, 4, 512, 2, kSoft>;
+    default: return decode_ell_kernel<A, 12, 6, 1, 2, 1024, 1, kSoft>;
   }
 }
 
@@ -517,6 +527,15 @@ KernelFn ell_kernel(int arith, int idx) {
     default: return ell_kernel_t<ArithF16>(idx);
   }
 }
+// ... with the absorbed variables' priors read per shot (qb_decode_batch_soft)
+KernelFn ell_soft_kernel(int arith, int idx) {
+  switch (arith) {
+    case QB_ARITH_FLOAT: return ell_kernel_t<ArithF32, true>(idx);
+    case QB_ARITH_INT8:
+    case QB_ARITH_INT16: return ell_kernel_t<ArithI32, true>(idx);
+    default: return ell_kernel_t<ArithF16, true>(idx);
+  }
+}
 KernelFn ell_lat_kernel(int arith, int idx) {
   switch (arith) {
     case QB_ARITH_FLOAT: return ell_lat_kernel_t<ArithF32>(idx);
@@ -530,14 +549,14 @@ uint32_t ell_msg_bytes(int arith) { return arith == QB_ARITH_HALF ? 2u : 4u; }
 // two shots per thread on packed fp16 instructions (kernel_ell_h2.cuh): half mode, and int8
 // mode when the loader has verified the fp16 form of the Q16 scaling
 constexpr int kEllH2MaxT[] = {1024, 160, 320, 512, 1024};
-template <bool kI8>
+template <bool kI8, bool kSoft = false>
 KernelFn ell_h2_kernel_t(int idx) {
   switch (idx) {
-    case 0: return decode_ell_h2_kernel<4, 2, 1, 2, 1024, 1, kI8>;
-    case 1: return decode_ell_h2_kernel<7, 3, 3, 5, 160, 4, kI8>;
-    case 2: return decode_ell_h2_kernel<7, 3, 3, 5, 320, 2, kI8>;
-    case 3: return decode_ell_h2_kernel<8, 4, 2, 4, 512, 1, kI8>;
-    default: return decode_ell_h2_kernel<12, 6, 1, 2, 1024, 1, kI8>;
+    case 0: return decode_ell_h2_kernel<4, 2, 1, 2, 1024, 1, kI8, kSoft>;
+    case 1: return decode_ell_h2_kernel<7, 3, 3, 5, 160, 4, kI8, kSoft>;
+    case 2: return decode_ell_h2_kernel<7, 3, 3, 5, 320, 2, kI8, kSoft>;
+    case 3: return decode_ell_h2_kernel<8, 4, 2, 4, 512, 1, kI8, kSoft>;
+    default: return decode_ell_h2_kernel<12, 6, 1, 2, 1024, 1, kI8, kSoft>;
   }
 }
 
@@ -566,6 +585,10 @@ void finish_plan(qb_decoder* h, LaunchPlan& pl) {
                       : h->smem_bytes;
   CUDA_TRY(cudaFuncSetAttribute(pl.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(pl.smem)));
+  if (pl.kernel_soft) {
+    CUDA_TRY(cudaFuncSetAttribute(pl.kernel_soft, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(pl.smem)));
+  }
   if (pl.cluster) {
     pl.ctas_per_sm = 1;
     return;
@@ -714,6 +737,9 @@ void choose_plans(qb_decoder* h) {
         pl.kernel = !pair                       ? ell_kernel(h->arith, idx)
                     : h->arith == QB_ARITH_INT8 ? ell_h2_kernel_t<true>(idx)
                                                 : ell_h2_kernel_t<false>(idx);
+        pl.kernel_soft = !pair                       ? ell_soft_kernel(h->arith, idx)
+                         : h->arith == QB_ARITH_INT8 ? ell_h2_kernel_t<true, true>(idx)
+                                                     : ell_h2_kernel_t<false, true>(idx);
         pl.name = pair ? "decode_ell_h2_kernel" : "decode_ell_kernel";
         pl.ngroups = 1;
         pl.group_threads = T;
@@ -869,15 +895,22 @@ void launch_plan(qb_decoder* h, const LaunchPlan& pl, const ShotIO& io, unsigned
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, pl.kernel, P, io));
+  KernelFn kernel = pl.kernel;
+  if (io.soft) {
+    if (!pl.kernel_soft) fail(QB_RUNTIME_ERROR, "launch plan has no per-shot-prior kernel");
+    kernel = pl.kernel_soft;
+  }
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, P, io));
   ++h->launches;
 }
 
-void ensure_batch(qb_decoder* h, uint64_t shots, bool want_resid) {
-  if (shots <= h->batch_cap && (!want_resid || h->b_res)) return;
+void ensure_batch(qb_decoder* h, uint64_t shots, bool want_resid, bool want_soft = false) {
+  if (shots <= h->batch_cap && (!want_resid || h->b_res) && (!want_soft || h->b_soft)) return;
   const uint64_t cap = std::max<uint64_t>(shots, h->batch_cap);
+  const bool soft = want_soft || h->b_soft != nullptr;
   free_batch(h);
   const DecodeParams& P = h->P;
+  if (soft) CUDA_TRY(cudaMalloc(&h->b_soft, cap * P.M * h->soft_bytes));
   CUDA_TRY(cudaMalloc(&h->b_syn, cap * P.syn_w32 * 4));
   CUDA_TRY(cudaMalloc(&h->b_est, cap * P.est_w32 * 4));
   CUDA_TRY(cudaMalloc(&h->b_res, cap * P.syn_w32 * 4));
@@ -926,12 +959,25 @@ unsigned batch_grid(qb_decoder* h, uint64_t shots) {
   return static_cast<unsigned>(std::min<uint64_t>(shots, resident));
 }
 
+// The per-shot-prior path exists where the loader absorbs degree-1 variables into their
+// checks: the degree-padded batch kernels (kernel_ell.cuh).
+void require_soft(qb_decoder* h, const char* who) {
+  if (!h->bat.kernel_soft) {
+    fail(QB_INVALID_ARGUMENT,
+         std::string(who) + ": per-shot priors need a graph served by the degree-padded kernel "
+                            "(e.g. the extended graph [H | I]); this decoder's batch kernel is " +
+             h->bat.name);
+  }
+}
+
 void run_batch_device(qb_decoder* h, uint64_t shots, const uint32_t* d_syn, uint32_t* d_est,
                       uint32_t* d_res, uint8_t* d_conv, uint32_t* d_iters, cudaStream_t stream,
-                      int sched_slot = 0) {
+                      int sched_slot = 0, const void* d_soft = nullptr) {
   if (shots == 0) return;
   if (shots > 0x7fff0000ull) fail(QB_INVALID_ARGUMENT, "too many shots for one launch");
   ShotIO io{};
+  io.soft = d_soft;
+  io.soft_bytes = h->soft_bytes;
   io.nshots = shots;
   io.syn = d_syn;
   io.est = d_est;
@@ -1588,11 +1634,17 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
         h->max_dv = std::max(h->max_dv, graph->var_offsets[n + 1] - graph->var_offsets[n]);
       }
     }
+    h->soft_bytes = arith == QB_ARITH_INT8 ? 1u : arith == QB_ARITH_INT16 ? 2u : 4u;
+    h->quant_scale = arith == QB_ARITH_INT8 || arith == QB_ARITH_INT16
+                         ? (config->quant_scale != 0.0 ? config->quant_scale
+                                                       : (arith == QB_ARITH_INT8 ? 8.0 : 256.0))
+                         : 0.0;
     {
       // degree-padded kernel: every check absorbs its first degree-1 variable (that variable
       // is then updated by the check's thread); the others are listed per segment
       std::vector<uint32_t> abs_slot(M, kNoAbsorb), vars(N, 0);
       std::vector<uint8_t> absorbed(N, 0);
+      h->soft_var.assign(M, 0xffffffffu);
       for (uint32_t m = 0; m < M; ++m) {
         const uint32_t e0 = graph->check_offsets[m], e1 = graph->check_offsets[m + 1];
         for (uint32_t e = e0; e < e1 && e - e0 < kNoAbsorb; ++e) {
@@ -1600,6 +1652,7 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
           if (graph->var_offsets[v + 1] - graph->var_offsets[v] == 1) {
             abs_slot[m] = e - e0;
             absorbed[v] = 1;
+            h->soft_var[m] = v;
             break;
           }
         }
@@ -1978,6 +2031,212 @@ qb_status qb_set_logicals(qb_decoder* h, const uint64_t* x_tests, uint32_t n_x,
   });
 }
 
+}  // extern "C"
+
+namespace {
+
+void launch_classify(qb_decoder* h, uint64_t n, const uint32_t* err, const uint32_t* est,
+                     const uint32_t* syn, const uint8_t* conv, const uint32_t* iters,
+                     cudaStream_t st) {
+  const DecodeParams& P = h->P;
+  ClassifyParams cp{};
+  cp.nshots = n;
+  cp.err = err;
+  cp.est = est;
+  cp.syn = syn;
+  cp.conv = conv;
+  cp.iters = iters;
+  cp.tests_x = h->d_tests_x;
+  cp.tests_z = h->d_tests_z;
+  cp.n_x = h->n_tests_x;
+  cp.n_z = h->n_tests_z;
+  cp.aux_mask = h->d_aux_mask;
+  cp.counters = h->d_counters;
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(
+      (n + kClassifyWarps - 1) / kClassifyWarps, static_cast<uint64_t>(h->sm_count) * 8));
+  const size_t smem = static_cast<size_t>(kClassifyWarps) * 2 * P.est_w32 * 4;
+  classify_kernel<<<grid, kClassifyWarps * 32, smem, st>>>(P, cp);
+  CUDA_TRY(cudaGetLastError());
+  ++h->launches;
+}
+
+void add_counters(qb_decoder* h, uint64_t* counters, cudaStream_t st) {
+  unsigned long long host_counters[10];
+  CUDA_TRY(cudaMemcpyAsync(host_counters, h->d_counters, sizeof(host_counters),
+                           cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  for (int k = 0; k < 10; ++k) counters[k] += host_counters[k];
+}
+
+// Soft measurement of the noiseless syndromes in d_syn (kernel_noise.cuh).
+void launch_soft_measure(qb_decoder* h, uint64_t seed, double mu, double sigma,
+                         uint64_t first_trial, uint64_t shots, uint32_t* d_syn, void* d_soft,
+                         uint32_t* d_err, cudaStream_t st) {
+  SoftParams sp{};
+  sp.seed = seed;
+  sp.first_trial = first_trial;
+  sp.nshots = shots;
+  sp.mu = mu;
+  sp.sigma = sigma;
+  sp.llr_scale = 2.0 * mu / (sigma * sigma);
+  sp.quant_scale = h->quant_scale;
+  sp.kmax = h->P.kmax;
+  sp.elem_bytes = h->soft_bytes;
+  sp.syn = d_syn;
+  sp.err = d_err;
+  sp.soft = d_soft;
+  const uint64_t blocks_needed = (shots + kNoiseWarps - 1) / kNoiseWarps;
+  const unsigned grid = static_cast<unsigned>(
+      std::min<uint64_t>(blocks_needed, static_cast<uint64_t>(h->sm_count) * 8));
+  soft_measure_kernel<<<grid, kNoiseWarps * 32, 0, st>>>(h->P, sp);
+  CUDA_TRY(cudaGetLastError());
+  ++h->launches;
+}
+
+// Flip probabilities for the data variables only: the absorbed (measurement-error) variables
+// get probability 0, their flips come from the soft measurement channel.
+std::vector<double> data_only_probs(const qb_decoder* h, double p, const double* probs) {
+  const DecodeParams& P = h->P;
+  std::vector<double> out(P.N);
+  for (uint32_t v = 0; v < P.N; ++v) out[v] = probs ? probs[v] : p;
+  for (uint32_t m = 0; m < P.M; ++m) {
+    if (h->soft_var[m] != 0xffffffffu) out[h->soft_var[m]] = 0.0;
+  }
+  return out;
+}
+
+void check_soft_channel(double mu, double sigma) {
+  if (!(mu > 0.0) || !(sigma > 0.0) || !std::isfinite(mu) || !std::isfinite(sigma)) {
+    fail(QB_INVALID_ARGUMENT, "soft measurement: mu and sigma must be positive and finite");
+  }
+}
+
+// One campaign: sample -> (soft measurement) -> decode -> classify in rounds of `chunk`
+// trials on the handle's stream, ten counters back at the end.
+void campaign_core(qb_decoder* h, uint64_t seed, double p, const double* probs, bool soft, double mu,
+                   double sigma, uint64_t first_trial, uint64_t trials, uint64_t* counters) {
+  const DecodeParams& P = h->P;
+  if (!counters) fail(QB_INVALID_ARGUMENT, "campaign_run: NULL counters");
+  if (P.nseg != 2 || !h->d_tests_x || !h->d_tests_z) {
+    fail(QB_INVALID_ARGUMENT, "campaign_run: call qb_set_logicals on a CssCode decoder first");
+  }
+  if (!(p >= 0.0 && p <= 1.0)) fail(QB_INVALID_ARGUMENT, "NoiseModel: p must lie in [0, 1]");
+  if (soft) {
+    require_soft(h, "campaign_run_soft");
+    check_soft_channel(mu, sigma);
+  }
+  if (trials == 0) return;
+  if (!h->d_counters) CUDA_TRY(cudaMalloc(&h->d_counters, 10 * sizeof(unsigned long long)));
+  cudaStream_t st = h->stream;
+  CUDA_TRY(cudaMemsetAsync(h->d_counters, 0, 10 * sizeof(unsigned long long), st));
+  // trials per sample / decode / classify round: QB_OPT_BATCH_CHUNK when set, else 2^20
+  const uint64_t max_chunk = h->opt_batch_chunk > 0 ? static_cast<uint64_t>(h->opt_batch_chunk) : (1ull << 20);
+  const uint64_t chunk = std::min<uint64_t>(trials, max_chunk);
+  ensure_batch(h, chunk, false, soft);
+  // the reference's draw order (X_0, Z_0, X_1, ...) exists for a plain CSS code only; on an
+  // extended graph (auxiliary variables, or per-variable probabilities that do not pair up)
+  // draw v belongs to variable v
+  const bool interleave = !h->d_aux_mask && !soft && P.segs[0].v1 * 2 == P.N;
+  std::vector<double> dprobs;
+  if (soft) {
+    dprobs = data_only_probs(h, p, probs);
+    probs = dprobs.data();
+  }
+  for (uint64_t done = 0; done < trials; done += chunk) {
+    const uint64_t n = std::min<uint64_t>(chunk, trials - done);
+    qb_status stc = qb_generate_syndromes(h, seed, p, probs, interleave ? 1 : 0, first_trial + done, n,
+                                          reinterpret_cast<uint64_t*>(h->b_syn),
+                                          reinterpret_cast<uint64_t*>(h->c_err), st);
+    if (stc != QB_OK) fail(stc, h->err);
+    if (soft) {
+      launch_soft_measure(h, seed, mu, sigma, first_trial + done, n, h->b_syn, h->b_soft, h->c_err, st);
+    }
+    run_batch_device(h, n, h->b_syn, h->b_est, nullptr, h->b_conv, h->b_iters, st, 0,
+                     soft ? h->b_soft : nullptr);
+    launch_classify(h, n, h->c_err, h->b_est, h->b_syn, h->b_conv, h->b_iters, st);
+  }
+  add_counters(h, counters, st);
+}
+
+// qb_decode_batch / qb_decode_batch_soft: chunks rotate over kPipeSlots streams, each with
+// its own device buffers and scheduler words, so that with pinned host buffers the H2D copy
+// of chunk i+1, the kernel of chunk i and the D2H copy of chunk i-1 run concurrently (one
+// copy engine per direction).
+void decode_batch_host(qb_decoder* h, uint64_t shots, const uint64_t* syndromes, const void* soft,
+                       uint64_t* estimates, uint64_t* residuals, uint8_t* converged,
+                       uint32_t* iterations) {
+  if (shots == 0) return;
+  if (!syndromes || !estimates || !converged || !iterations) {
+    fail(QB_INVALID_ARGUMENT, "decode_batch: NULL buffer");
+  }
+  const DecodeParams& P = h->P;
+  const uint64_t max_chunk = h->opt_batch_chunk > 0 ? static_cast<uint64_t>(h->opt_batch_chunk) & ~1ull
+                                                    : (1ull << 15);  // measured: 103.6 M/s at 2^15, 102.6 at 2^16, 99.3 at 2^17
+  const uint64_t chunk = std::min<uint64_t>(shots, std::max<uint64_t>(max_chunk, 2));
+  ensure_batch(h, chunk * kPipeSlots, residuals != nullptr, soft != nullptr);
+  const size_t soft_row = static_cast<size_t>(P.M) * h->soft_bytes;
+  bool used[kPipeSlots] = {};
+  uint64_t done = 0;
+  for (int slot = 0; done < shots; slot = (slot + 1) % kPipeSlots) {
+    const uint64_t n = std::min<uint64_t>(chunk, shots - done);
+    const uint64_t off = static_cast<uint64_t>(slot) * chunk;
+    cudaStream_t st = h->pipe_stream[slot];
+    if (used[slot]) CUDA_TRY(cudaEventSynchronize(h->pipe_event[slot]));
+    uint32_t* d_syn = h->b_syn + off * P.syn_w32;
+    uint32_t* d_est = h->b_est + off * P.est_w32;
+    uint32_t* d_res = h->b_res + off * P.syn_w32;
+    uint8_t* d_conv = h->b_conv + off * P.nseg;
+    uint32_t* d_it = h->b_iters + off * P.nseg;
+    unsigned char* d_soft = soft ? h->b_soft + off * soft_row : nullptr;
+    CUDA_TRY(cudaMemcpyAsync(d_syn,
+                             reinterpret_cast<const uint32_t*>(syndromes) + done * P.syn_w32,
+                             n * P.syn_w32 * 4, cudaMemcpyHostToDevice, st));
+    if (soft) {
+      CUDA_TRY(cudaMemcpyAsync(d_soft, static_cast<const unsigned char*>(soft) + done * soft_row,
+                               n * soft_row, cudaMemcpyHostToDevice, st));
+    }
+    run_batch_device(h, n, d_syn, d_est, residuals ? d_res : nullptr, d_conv, d_it, st, slot, d_soft);
+    CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(estimates) + done * P.est_w32, d_est,
+                             n * P.est_w32 * 4, cudaMemcpyDeviceToHost, st));
+    if (residuals) {
+      CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(residuals) + done * P.syn_w32, d_res,
+                               n * P.syn_w32 * 4, cudaMemcpyDeviceToHost, st));
+    }
+    CUDA_TRY(cudaMemcpyAsync(converged + done * P.nseg, d_conv, n * P.nseg,
+                             cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(iterations + done * P.nseg, d_it, n * P.nseg * 4,
+                             cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaEventRecord(h->pipe_event[slot], st));
+    used[slot] = true;
+    done += n;
+  }
+  for (int slot = 0; slot < kPipeSlots; ++slot) {
+    if (used[slot]) CUDA_TRY(cudaEventSynchronize(h->pipe_event[slot]));
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+qb_status qb_set_auxiliary_vars(qb_decoder* h, const uint64_t* mask) {
+  if (!h) return QB_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    const DecodeParams& P = h->P;
+    cudaFree(h->d_aux_mask);
+    h->d_aux_mask = nullptr;
+    if (!mask) return;
+    CUDA_TRY(cudaMalloc(&h->d_aux_mask, P.est_w32 * 4));
+    CUDA_TRY(cudaMemcpy(h->d_aux_mask, mask, P.est_w32 * 4, cudaMemcpyHostToDevice));
+  });
+}
+
+qb_status qb_soft_vars(const qb_decoder* h, uint32_t* vars) {
+  if (!h || !vars) return QB_INVALID_ARGUMENT;
+  std::memcpy(vars, h->soft_var.data(), h->soft_var.size() * sizeof(uint32_t));
+  return QB_OK;
+}
+
 qb_status qb_classify_batch_device(qb_decoder* h, uint64_t shots, const uint64_t* d_errors,
                                    const uint64_t* d_estimates, const uint64_t* d_syndromes,
                                    const uint8_t* d_converged, const uint32_t* d_iterations,
@@ -1995,29 +2254,10 @@ qb_status qb_classify_batch_device(qb_decoder* h, uint64_t shots, const uint64_t
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (!h->d_counters) CUDA_TRY(cudaMalloc(&h->d_counters, 10 * sizeof(unsigned long long)));
     CUDA_TRY(cudaMemsetAsync(h->d_counters, 0, 10 * sizeof(unsigned long long), st));
-    ClassifyParams cp{};
-    cp.nshots = shots;
-    cp.err = reinterpret_cast<const uint32_t*>(d_errors);
-    cp.est = reinterpret_cast<const uint32_t*>(d_estimates);
-    cp.syn = reinterpret_cast<const uint32_t*>(d_syndromes);
-    cp.conv = d_converged;
-    cp.iters = d_iterations;
-    cp.tests_x = h->d_tests_x;
-    cp.tests_z = h->d_tests_z;
-    cp.n_x = h->n_tests_x;
-    cp.n_z = h->n_tests_z;
-    cp.counters = h->d_counters;
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(
-        (shots + kClassifyWarps - 1) / kClassifyWarps, static_cast<uint64_t>(h->sm_count) * 8));
-    const size_t smem = static_cast<size_t>(kClassifyWarps) * 2 * P.est_w32 * 4;
-    classify_kernel<<<grid, kClassifyWarps * 32, smem, st>>>(P, cp);
-    CUDA_TRY(cudaGetLastError());
-    ++h->launches;
-    unsigned long long host_counters[10];
-    CUDA_TRY(cudaMemcpyAsync(host_counters, h->d_counters, sizeof(host_counters),
-                             cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    for (int k = 0; k < 10; ++k) counters[k] += host_counters[k];
+    launch_classify(h, shots, reinterpret_cast<const uint32_t*>(d_errors),
+                    reinterpret_cast<const uint32_t*>(d_estimates),
+                    reinterpret_cast<const uint32_t*>(d_syndromes), d_converged, d_iterations, st);
+    add_counters(h, counters, st);
   });
 }
 
@@ -2025,52 +2265,36 @@ qb_status qb_campaign_run(qb_decoder* h, uint64_t seed, double p, const double* 
                           uint64_t first_trial, uint64_t trials, uint64_t* counters) {
   if (!h) return QB_INVALID_ARGUMENT;
   return guarded(h, [&] {
-    const DecodeParams& P = h->P;
-    if (!counters) fail(QB_INVALID_ARGUMENT, "campaign_run: NULL counters");
-    if (P.nseg != 2 || !h->d_tests_x || !h->d_tests_z) {
-      fail(QB_INVALID_ARGUMENT, "campaign_run: call qb_set_logicals on a CssCode decoder first");
-    }
+    campaign_core(h, seed, p, probs, false, 0.0, 0.0, first_trial, trials, counters);
+  });
+}
+
+qb_status qb_campaign_run_soft(qb_decoder* h, uint64_t seed, double p, const double* probs,
+                               double mu, double sigma, uint64_t first_trial, uint64_t trials,
+                               uint64_t* counters) {
+  if (!h) return QB_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    campaign_core(h, seed, p, probs, true, mu, sigma, first_trial, trials, counters);
+  });
+}
+
+qb_status qb_generate_soft_syndromes(qb_decoder* h, uint64_t seed, double p, const double* probs,
+                                     double mu, double sigma, uint64_t first_trial,
+                                     uint64_t shots, uint64_t* d_syndromes, void* d_soft,
+                                     uint64_t* d_errors, void* stream) {
+  if (!h) return QB_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    if (shots == 0) return;
+    if (!d_syndromes || !d_soft) fail(QB_INVALID_ARGUMENT, "generate_soft_syndromes: NULL output");
     if (!(p >= 0.0 && p <= 1.0)) fail(QB_INVALID_ARGUMENT, "NoiseModel: p must lie in [0, 1]");
-    if (trials == 0) return;
-    if (!h->d_counters) CUDA_TRY(cudaMalloc(&h->d_counters, 10 * sizeof(unsigned long long)));
-    cudaStream_t st = h->stream;
-    CUDA_TRY(cudaMemsetAsync(h->d_counters, 0, 10 * sizeof(unsigned long long), st));
-    // trials per sample / decode / classify round: QB_OPT_BATCH_CHUNK when set, else 2^20
-    const uint64_t max_chunk = h->opt_batch_chunk > 0 ? static_cast<uint64_t>(h->opt_batch_chunk) : (1ull << 20);
-    const uint64_t chunk = std::min<uint64_t>(trials, max_chunk);
-    ensure_batch(h, chunk, false);
-    for (uint64_t done = 0; done < trials; done += chunk) {
-      const uint64_t n = std::min<uint64_t>(chunk, trials - done);
-      // sample + syndrome (kernel_noise.cuh), decode (batch plan), classify
-      qb_status stc = qb_generate_syndromes(h, seed, p, probs, 1, first_trial + done, n,
-                                            reinterpret_cast<uint64_t*>(h->b_syn),
-                                            reinterpret_cast<uint64_t*>(h->c_err), st);
-      if (stc != QB_OK) fail(stc, h->err);
-      run_batch_device(h, n, h->b_syn, h->b_est, nullptr, h->b_conv, h->b_iters, st);
-      ClassifyParams cp{};
-      cp.nshots = n;
-      cp.err = h->c_err;
-      cp.est = h->b_est;
-      cp.syn = h->b_syn;
-      cp.conv = h->b_conv;
-      cp.iters = h->b_iters;
-      cp.tests_x = h->d_tests_x;
-      cp.tests_z = h->d_tests_z;
-      cp.n_x = h->n_tests_x;
-      cp.n_z = h->n_tests_z;
-      cp.counters = h->d_counters;
-      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(
-          (n + kClassifyWarps - 1) / kClassifyWarps, static_cast<uint64_t>(h->sm_count) * 8));
-      const size_t smem = static_cast<size_t>(kClassifyWarps) * 2 * P.est_w32 * 4;
-      classify_kernel<<<grid, kClassifyWarps * 32, smem, st>>>(P, cp);
-      CUDA_TRY(cudaGetLastError());
-      ++h->launches;
-    }
-    unsigned long long host_counters[10];
-    CUDA_TRY(cudaMemcpyAsync(host_counters, h->d_counters, sizeof(host_counters),
-                             cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    for (int k = 0; k < 10; ++k) counters[k] += host_counters[k];
+    check_soft_channel(mu, sigma);
+    const std::vector<double> dprobs = data_only_probs(h, p, probs);
+    qb_status stc = qb_generate_syndromes(h, seed, p, dprobs.data(), 0, first_trial, shots,
+                                          d_syndromes, d_errors, stream);
+    if (stc != QB_OK) fail(stc, h->err);
+    launch_soft_measure(h, seed, mu, sigma, first_trial, shots,
+                        reinterpret_cast<uint32_t*>(d_syndromes), d_soft,
+                        reinterpret_cast<uint32_t*>(d_errors), static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -2079,52 +2303,37 @@ qb_status qb_decode_batch(qb_decoder* h, uint64_t shots, const uint64_t* syndrom
                           uint32_t* iterations) {
   if (!h) return QB_INVALID_ARGUMENT;
   return guarded(h, [&] {
+    decode_batch_host(h, shots, syndromes, nullptr, estimates, residuals, converged, iterations);
+  });
+}
+
+qb_status qb_decode_batch_soft(qb_decoder* h, uint64_t shots, const uint64_t* syndromes,
+                               const void* soft, uint64_t* estimates, uint64_t* residuals,
+                               uint8_t* converged, uint32_t* iterations) {
+  if (!h) return QB_INVALID_ARGUMENT;
+  return guarded(h, [&] {
     if (shots == 0) return;
-    if (!syndromes || !estimates || !converged || !iterations) {
-      fail(QB_INVALID_ARGUMENT, "decode_batch: NULL buffer");
+    require_soft(h, "decode_batch_soft");
+    if (!soft) fail(QB_INVALID_ARGUMENT, "decode_batch_soft: NULL soft buffer");
+    decode_batch_host(h, shots, syndromes, soft, estimates, residuals, converged, iterations);
+  });
+}
+
+qb_status qb_decode_batch_soft_device(qb_decoder* h, uint64_t shots, const uint64_t* d_syndromes,
+                                      const void* d_soft, uint64_t* d_estimates,
+                                      uint64_t* d_residuals, uint8_t* d_converged,
+                                      uint32_t* d_iterations, void* stream) {
+  if (!h) return QB_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    if (shots == 0) return;
+    require_soft(h, "decode_batch_soft_device");
+    if (!d_syndromes || !d_soft || !d_estimates || !d_converged || !d_iterations) {
+      fail(QB_INVALID_ARGUMENT, "decode_batch_soft_device: NULL buffer");
     }
-    const DecodeParams& P = h->P;
-    // Chunks rotate over kPipeSlots streams, each with its own device buffers and
-    // scheduler words, so that with pinned host buffers the H2D copy of chunk i+1,
-    // the kernel of chunk i and the D2H copy of chunk i-1 run concurrently (one
-    // copy engine per direction).
-    const uint64_t max_chunk = h->opt_batch_chunk > 0 ? static_cast<uint64_t>(h->opt_batch_chunk) & ~1ull
-                                                      : (1ull << 15);  // measured: 103.6 M/s at 2^15, 102.6 at 2^16, 99.3 at 2^17
-    const uint64_t chunk = std::min<uint64_t>(shots, std::max<uint64_t>(max_chunk, 2));
-    ensure_batch(h, chunk * kPipeSlots, residuals != nullptr);
-    bool used[kPipeSlots] = {};
-    uint64_t done = 0;
-    for (int slot = 0; done < shots; slot = (slot + 1) % kPipeSlots) {
-      const uint64_t n = std::min<uint64_t>(chunk, shots - done);
-      const uint64_t off = static_cast<uint64_t>(slot) * chunk;
-      cudaStream_t st = h->pipe_stream[slot];
-      if (used[slot]) CUDA_TRY(cudaEventSynchronize(h->pipe_event[slot]));
-      uint32_t* d_syn = h->b_syn + off * P.syn_w32;
-      uint32_t* d_est = h->b_est + off * P.est_w32;
-      uint32_t* d_res = h->b_res + off * P.syn_w32;
-      uint8_t* d_conv = h->b_conv + off * P.nseg;
-      uint32_t* d_it = h->b_iters + off * P.nseg;
-      CUDA_TRY(cudaMemcpyAsync(d_syn,
-                               reinterpret_cast<const uint32_t*>(syndromes) + done * P.syn_w32,
-                               n * P.syn_w32 * 4, cudaMemcpyHostToDevice, st));
-      run_batch_device(h, n, d_syn, d_est, residuals ? d_res : nullptr, d_conv, d_it, st, slot);
-      CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(estimates) + done * P.est_w32, d_est,
-                               n * P.est_w32 * 4, cudaMemcpyDeviceToHost, st));
-      if (residuals) {
-        CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(residuals) + done * P.syn_w32, d_res,
-                                 n * P.syn_w32 * 4, cudaMemcpyDeviceToHost, st));
-      }
-      CUDA_TRY(cudaMemcpyAsync(converged + done * P.nseg, d_conv, n * P.nseg,
-                               cudaMemcpyDeviceToHost, st));
-      CUDA_TRY(cudaMemcpyAsync(iterations + done * P.nseg, d_it, n * P.nseg * 4,
-                               cudaMemcpyDeviceToHost, st));
-      CUDA_TRY(cudaEventRecord(h->pipe_event[slot], st));
-      used[slot] = true;
-      done += n;
-    }
-    for (int slot = 0; slot < kPipeSlots; ++slot) {
-      if (used[slot]) CUDA_TRY(cudaEventSynchronize(h->pipe_event[slot]));
-    }
+    run_batch_device(h, shots, reinterpret_cast<const uint32_t*>(d_syndromes),
+                     reinterpret_cast<uint32_t*>(d_estimates),
+                     reinterpret_cast<uint32_t*>(d_residuals), d_converged, d_iterations,
+                     static_cast<cudaStream_t>(stream), 0, d_soft);
   });
 }
 

@@ -272,6 +272,88 @@ class Decoder:
             _raise(st, self._h)
 
 
+    # -- soft (noisy) syndromes: per-shot priors of the absorbed variables ---------------
+    SOFT_DTYPES = {"float": np.float32, "half": np.float32, "int8": np.int8, "int16": np.int16}
+
+    def soft_vars(self) -> np.ndarray:
+        """qb_soft_vars: for every check the variable whose prior a soft value replaces
+        (0xffffffff: none)."""
+        out = np.zeros(self.num_checks(), dtype=np.uint32)
+        st = self._lib.qb_soft_vars(self._h, _ptr(out, _lib.u32p))
+        if st != _lib.QB_OK:
+            _raise(st, self._h)
+        return out
+
+    def soft_dtype(self):
+        return self.SOFT_DTYPES[self._cfg.arithmetic]
+
+    def quantize_soft(self, llr: np.ndarray) -> np.ndarray:
+        """Reliabilities (LLR magnitudes, any shape) -> the decoder's soft format: float32, or
+        quantize_saturate(llr, quant_scale, kmax) (decoder.cpp:500-509) with results of 0
+        clamped to +-1 (the reference rejects a prior that quantises to 0, decoder.cpp:115-120)."""
+        llr = np.asarray(llr, dtype=np.float64)
+        if self._cfg.arithmetic in ("float", "half"):
+            return llr.astype(np.float32)
+        kmax = 127 if self._cfg.arithmetic == "int8" else 32767
+        scale = self._cfg.quant_scale or (8.0 if self._cfg.arithmetic == "int8" else 256.0)
+        scaled = llr * scale
+        q = np.where(scaled >= 0, np.floor(scaled + 0.5), -np.floor(-scaled + 0.5))  # llround
+        q = np.clip(q, -kmax, kmax)
+        q = np.where(q == 0, np.where(np.signbit(scaled), -1, 1), q)
+        return q.astype(self.soft_dtype())
+
+    def _check_soft(self, soft: np.ndarray, shots: int) -> np.ndarray:
+        soft = np.ascontiguousarray(soft, dtype=self.soft_dtype())
+        if soft.shape != (shots, self.num_checks()):
+            raise ValueError(f"decode_batch_soft: soft values must be ({shots}, {self.num_checks()})")
+        if self._cfg.arithmetic in ("int8", "int16"):
+            used = self.soft_vars() != 0xffffffff
+            if (soft[:, used] == 0).any() or (soft[:, used] == np.iinfo(soft.dtype).min).any():
+                raise ValueError("decode_batch_soft: a quantised prior is 0 (the reference rejects "
+                                 "it, decoder.cpp:115-120) or below -kmax")
+        elif not np.isfinite(soft).all():
+            raise ValueError("decode_batch_soft: a prior is not finite")
+        return soft
+
+    def decode_batch_soft_segments(self, syndromes: np.ndarray, soft: np.ndarray,
+                                   want_residual: bool = True):
+        """qb_decode_batch_soft on host arrays: syndromes (shots, ceil(M/64)) uint64 words and
+        soft (shots, M) per-shot priors of the absorbed variables in soft_dtype()."""
+        syndromes = np.ascontiguousarray(syndromes, dtype=np.uint64)
+        if syndromes.ndim != 2 or syndromes.shape[1] != self._sw:
+            raise ValueError(f"decode_batch: syndromes must be (shots, {self._sw}) uint64 words")
+        shots = syndromes.shape[0]
+        soft = self._check_soft(soft, shots)
+        est = np.zeros((shots, self._ew), dtype=np.uint64)
+        res = np.zeros((shots, self._sw), dtype=np.uint64) if want_residual else None
+        conv = np.zeros((shots, self.num_segments), dtype=np.uint8)
+        its = np.zeros((shots, self.num_segments), dtype=np.uint32)
+        st = self._lib.qb_decode_batch_soft(self._h, shots, syndromes.ctypes.data, soft.ctypes.data,
+                                            est.ctypes.data, None if res is None else res.ctypes.data,
+                                            conv.ctypes.data, its.ctypes.data)
+        if st != _lib.QB_OK:
+            _raise(st, self._h)
+        return est, res, conv, its
+
+    def decode_batch_soft_device(self, shots: int, d_syn: int, d_soft: int, d_est: int,
+                                 d_res: Optional[int], d_conv: int, d_its: int, stream: int = 0) -> None:
+        st = self._lib.qb_decode_batch_soft_device(self._h, shots, d_syn, d_soft, d_est, d_res,
+                                                   d_conv, d_its, stream)
+        if st != _lib.QB_OK:
+            _raise(st, self._h)
+
+    def generate_soft_syndromes(self, seed: int, p: float, mu: float, sigma: float, shots: int,
+                                d_syn: int, d_soft: int, d_err: Optional[int] = None,
+                                first_trial: int = 0, probs: Optional[Sequence[float]] = None,
+                                stream: int = 0) -> None:
+        """qb_generate_soft_syndromes: data flips + Gaussian soft measurement on the device."""
+        pr = None if probs is None else np.ascontiguousarray(probs, dtype=np.float64)
+        st = self._lib.qb_generate_soft_syndromes(self._h, seed, float(p), _ptr(pr, _lib.f64p),
+                                                  float(mu), float(sigma), first_trial, shots,
+                                                  d_syn, d_soft, d_err, stream)
+        if st != _lib.QB_OK:
+            _raise(st, self._h)
+
     def latency_run(self, pool: np.ndarray, warmup: int, measure: int):
         """qb_latency_run: the reference's run_bench protocol at batch 1
         (proj/src/bench.cpp:182-337) -> (wall_ns[measure], kernel_ns[measure], digest)."""

@@ -214,3 +214,32 @@ def test_oracle_rejects_what_the_reference_rejects(oracle, ref):
         with pytest.raises(ValueError):
             ref.decoder(rg, cfg)
     assert oracle.validate(g, DecoderConfig())
+
+
+@pytest.mark.parametrize("mode,scale", [("float", 0.0), ("int8", 8.0), ("int16", 256.0)])
+def test_per_shot_priors_oracle_equals_one_reference_decoder_per_shot(oracle, ref, mode, scale):
+    """Soft syndromes (BASELINE config 5): the reference has priors per Decoder only
+    (decoder.hpp:31-32), so the oracle's per-shot-prior entry point must equal one
+    unmodified reference Decoder constructed per shot on the extended graph [H | I]."""
+    from paper_2508_07879_b200 import DecoderConfig, codes, gf2
+    code = codes.make_code("bb72")
+    h, segs = codes.extended_graph(code)
+    g = codes.build_tanner_graph(h)
+    rng = np.random.default_rng(21)
+    shots, n, mz, mx = 200, code.n, code.hz.rows, code.hx.rows
+    meas = np.concatenate([np.arange(n, n + mz), np.arange(2 * n + mz, 2 * n + mz + mx)]).astype(np.uint32)
+    err = (rng.random((shots, g.num_vars)) < 0.02).astype(np.uint8)
+    syn = gf2.pack_bits(h.mat_vec(err))
+    soft = np.abs(1.0 + 0.6 * rng.standard_normal((shots, meas.size))) * 5.0 + 0.2
+    if mode != "float":
+        soft = np.maximum(np.round(soft * scale), 1.0) / scale
+    cfg = DecoderConfig(max_iterations=25, arithmetic=mode, quant_scale=scale,
+                        priors=[4.0] * g.num_vars)
+    oe, ores, oc, oi = oracle.decode_many_soft(g, cfg, syn, meas, soft, None, per_segment=False)
+    rg = ref.graph_from_coo(h.rows, h.cols, h.coo())
+    re_, rres, rc, ri = ref.decode_many_soft(rg, cfg, syn, meas, soft)
+    assert np.array_equal(oe, re_) and np.array_equal(ores, rres)
+    assert np.array_equal(oc[:, 0], rc) and np.array_equal(oi[:, 0], ri)
+    # and the per-shot values matter: a constant prior gives different outcomes
+    fe, _, _, _ = oracle.decode_many(g, cfg, syn, None, per_segment=False)
+    assert not np.array_equal(fe, oe)
