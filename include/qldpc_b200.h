@@ -286,6 +286,17 @@ qb_status qb_set_logicals(qb_decoder* h, const uint64_t* x_tests, uint32_t n_x,
 qb_status qb_campaign_run(qb_decoder* h, uint64_t seed, double p,
                           const double* probs, uint64_t first_trial,
                           uint64_t trials, uint64_t* counters);
+/* The same campaign on SEVERAL GPUs of one node from one process: `handles[g]` is a decoder
+ * created on its own device (same graph / config, qb_set_logicals called on each).  GPU g
+ * decodes the contiguous shard [g*T/n, (g+1)*T/n) of the trial range (the reference's worker
+ * split, proj/src/noise.cpp:253-254; trial streams are keyed by the global trial id, so the
+ * result does not depend on n), all devices run concurrently, and the ten counters are
+ * summed with ONE ncclAllReduce(ncclSum, ncclUint64, 10) over NVLink (the integer sum of
+ * noise.cpp:306-324) - the path's only collective.  NCCL is bound at run time (dlopen of
+ * libnccl.so.2); QB_RUNTIME_ERROR if it is absent.  ADDS to `counters` like qb_campaign_run. */
+qb_status qb_campaign_run_multi(qb_decoder* const* handles, uint32_t n, uint64_t seed,
+                                double p, const double* probs, uint64_t first_trial,
+                                uint64_t trials, uint64_t* counters);
 /* The classification step alone, on buffers already resident in DEVICE memory
  * (errors from qb_generate_syndromes, outputs of qb_decode_batch_device);
  * ADDS to the same ten host counters. */

@@ -76,6 +76,8 @@ SYMBOLS = {
     "qb_set_logicals": (C.c_int, [C.c_void_p, u64p, C.c_uint32, u64p, C.c_uint32]),
     "qb_campaign_run": (C.c_int, [C.c_void_p, C.c_uint64, C.c_double, f64p, C.c_uint64,
                                   C.c_uint64, u64p]),
+    "qb_campaign_run_multi": (C.c_int, [C.POINTER(C.c_void_p), C.c_uint32, C.c_uint64, C.c_double,
+                                        f64p, C.c_uint64, C.c_uint64, u64p]),
     "qb_classify_batch_device": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
                                            C.c_void_p, C.c_void_p, C.c_void_p, u64p, C.c_void_p]),
     "qb_soft_vars": (C.c_int, [C.c_void_p, u32p]),

@@ -8,6 +8,9 @@
 
 #include <cuda_runtime.h>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -15,6 +18,7 @@
 #include <cstdio>
 #include <cstring>
 #include <limits>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -2112,11 +2116,10 @@ void check_soft_channel(double mu, double sigma) {
 }
 
 // One campaign: sample -> (soft measurement) -> decode -> classify in rounds of `chunk`
-// trials on the handle's stream, ten counters back at the end.
-void campaign_core(qb_decoder* h, uint64_t seed, double p, const double* probs, bool soft, double mu,
-                   double sigma, uint64_t first_trial, uint64_t trials, uint64_t* counters) {
+// trials, ENQUEUED on the handle's stream; the ten counters stay in h->d_counters.
+void campaign_enqueue(qb_decoder* h, uint64_t seed, double p, const double* probs, bool soft, double mu,
+                      double sigma, uint64_t first_trial, uint64_t trials) {
   const DecodeParams& P = h->P;
-  if (!counters) fail(QB_INVALID_ARGUMENT, "campaign_run: NULL counters");
   if (P.nseg != 2 || !h->d_tests_x || !h->d_tests_z) {
     fail(QB_INVALID_ARGUMENT, "campaign_run: call qb_set_logicals on a CssCode decoder first");
   }
@@ -2125,10 +2128,10 @@ void campaign_core(qb_decoder* h, uint64_t seed, double p, const double* probs, 
     require_soft(h, "campaign_run_soft");
     check_soft_channel(mu, sigma);
   }
-  if (trials == 0) return;
   if (!h->d_counters) CUDA_TRY(cudaMalloc(&h->d_counters, 10 * sizeof(unsigned long long)));
   cudaStream_t st = h->stream;
   CUDA_TRY(cudaMemsetAsync(h->d_counters, 0, 10 * sizeof(unsigned long long), st));
+  if (trials == 0) return;
   // trials per sample / decode / classify round: QB_OPT_BATCH_CHUNK when set, else 2^20
   const uint64_t max_chunk = h->opt_batch_chunk > 0 ? static_cast<uint64_t>(h->opt_batch_chunk) : (1ull << 20);
   const uint64_t chunk = std::min<uint64_t>(trials, max_chunk);
@@ -2155,7 +2158,82 @@ void campaign_core(qb_decoder* h, uint64_t seed, double p, const double* probs, 
                      soft ? h->b_soft : nullptr);
     launch_classify(h, n, h->c_err, h->b_est, h->b_syn, h->b_conv, h->b_iters, st);
   }
-  add_counters(h, counters, st);
+}
+
+void campaign_core(qb_decoder* h, uint64_t seed, double p, const double* probs, bool soft, double mu,
+                   double sigma, uint64_t first_trial, uint64_t trials, uint64_t* counters) {
+  if (!counters) fail(QB_INVALID_ARGUMENT, "campaign_run: NULL counters");
+  campaign_enqueue(h, seed, p, probs, soft, mu, sigma, first_trial, trials);
+  if (trials == 0) return;
+  add_counters(h, counters, h->stream);
+}
+
+// ---- NCCL, bound at run time (dlopen): the library has no link-time dependency on it, and
+// single-GPU users never load it.  Only ncclCommInitAll / ncclAllReduce / group calls.
+struct NcclApi {
+  void* lib = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl_api() {
+  static NcclApi api;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (api.lib) return api;
+  void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!lib) fail(QB_RUNTIME_ERROR, std::string("NCCL not available: ") + dlerror());
+  auto sym = [&](const char* name) {
+    void* f = dlsym(lib, name);
+    if (!f) fail(QB_RUNTIME_ERROR, std::string("NCCL symbol missing: ") + name);
+    return f;
+  };
+  api.CommInitAll = reinterpret_cast<decltype(api.CommInitAll)>(sym("ncclCommInitAll"));
+  api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+  api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+  api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+  api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+  api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+  api.lib = lib;
+  return api;
+}
+
+#define NCCL_TRY(api, expr)                                                                \
+  do {                                                                                     \
+    ncclResult_t r__ = (expr);                                                             \
+    if (r__ != ncclSuccess) {                                                              \
+      fail(QB_RUNTIME_ERROR, std::string("NCCL error in " #expr ": ") + (api).GetErrorString(r__)); \
+    }                                                                                      \
+  } while (0)
+
+// communicators per device list, created on first use and kept for the life of the process
+struct CommSet {
+  std::vector<int> devices;
+  std::vector<ncclComm_t> comms;
+};
+std::vector<CommSet>& comm_cache() {
+  static std::vector<CommSet> cache;
+  return cache;
+}
+std::mutex g_comm_mu;
+
+const std::vector<ncclComm_t>& comms_for(NcclApi& api, const std::vector<int>& devices) {
+  std::lock_guard<std::mutex> lock(g_comm_mu);
+  for (const CommSet& cs : comm_cache()) {
+    if (cs.devices == devices) return cs.comms;
+  }
+  CommSet cs;
+  cs.devices = devices;
+  cs.comms.resize(devices.size());
+  NCCL_TRY(api, api.CommInitAll(cs.comms.data(), static_cast<int>(devices.size()), devices.data()));
+  comm_cache().push_back(std::move(cs));
+  return comm_cache().back().comms;
 }
 
 // qb_decode_batch / qb_decode_batch_soft: chunks rotate over kPipeSlots streams, each with
@@ -2266,6 +2344,66 @@ qb_status qb_campaign_run(qb_decoder* h, uint64_t seed, double p, const double* 
   if (!h) return QB_INVALID_ARGUMENT;
   return guarded(h, [&] {
     campaign_core(h, seed, p, probs, false, 0.0, 0.0, first_trial, trials, counters);
+  });
+}
+
+qb_status qb_campaign_run_multi(qb_decoder* const* handles, uint32_t n, uint64_t seed, double p,
+                                const double* probs, uint64_t first_trial, uint64_t trials,
+                                uint64_t* counters) {
+  if (!handles || n == 0 || !handles[0]) return QB_INVALID_ARGUMENT;
+  qb_decoder* h0 = handles[0];
+  return guarded(h0, [&] {
+    if (!counters) fail(QB_INVALID_ARGUMENT, "campaign_run_multi: NULL counters");
+    std::vector<int> devices(n);
+    for (uint32_t g = 0; g < n; ++g) {
+      if (!handles[g]) fail(QB_INVALID_ARGUMENT, "campaign_run_multi: NULL handle");
+      devices[g] = handles[g]->device;
+      for (uint32_t k = 0; k < g; ++k) {
+        if (devices[k] == devices[g]) {
+          fail(QB_INVALID_ARGUMENT, "campaign_run_multi: two handles on device " +
+                                        std::to_string(devices[g]) + " (one decoder per GPU)");
+        }
+      }
+    }
+    NcclApi& api = nccl_api();
+    const std::vector<ncclComm_t>& comms = comms_for(api, devices);
+    // contiguous shard per GPU (noise.cpp:253-254); every GPU's rounds are enqueued before any
+    // host wait, so the devices run side by side
+    for (uint32_t g = 0; g < n; ++g) {
+      qb_decoder* h = handles[g];
+      CUDA_TRY(cudaSetDevice(h->device));
+      const uint64_t lo = static_cast<uint64_t>(g) * trials / n, hi = static_cast<uint64_t>(g + 1) * trials / n;
+      try {
+        campaign_enqueue(h, seed, p, probs, false, 0.0, 0.0, first_trial + lo, hi - lo);
+      } catch (const StatusError& e) {
+        if (h != h0) h0->err = e.msg;
+        throw;
+      }
+    }
+    // the path's ONLY collective: one all-reduce(sum) of the ten uint64 counters, in place on
+    // every GPU (the integer sum over workers of noise.cpp:306-324)
+    NCCL_TRY(api, api.GroupStart());
+    for (uint32_t g = 0; g < n; ++g) {
+      qb_decoder* h = handles[g];
+      NCCL_TRY(api, api.AllReduce(h->d_counters, h->d_counters, 10, ncclUint64, ncclSum, comms[g], h->stream));
+    }
+    NCCL_TRY(api, api.GroupEnd());
+    unsigned long long first[10] = {};
+    for (uint32_t g = 0; g < n; ++g) {
+      qb_decoder* h = handles[g];
+      CUDA_TRY(cudaSetDevice(h->device));
+      unsigned long long got[10];
+      CUDA_TRY(cudaMemcpyAsync(got, h->d_counters, sizeof(got), cudaMemcpyDeviceToHost, h->stream));
+      CUDA_TRY(cudaStreamSynchronize(h->stream));
+      if (g == 0) {
+        std::memcpy(first, got, sizeof(got));
+      } else if (std::memcmp(first, got, sizeof(got)) != 0) {
+        fail(QB_RUNTIME_ERROR, "campaign_run_multi: ranks disagree after the all-reduce");
+      }
+    }
+    if (first[9] != trials) fail(QB_RUNTIME_ERROR, "campaign_run_multi: trial count mismatch after the all-reduce");
+    for (int k = 0; k < 10; ++k) counters[k] += first[k];
+    CUDA_TRY(cudaSetDevice(h0->device));
   });
 }
 

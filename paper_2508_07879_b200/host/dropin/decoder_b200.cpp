@@ -9,10 +9,13 @@
 #include "qldpc/decoder.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <limits>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "qldpc_b200.h"
 
@@ -41,6 +44,46 @@ int arith_code(Arithmetic a) {
   throw std::invalid_argument("DecoderConfig: unknown arithmetic mode");
 }
 
+// Which GPU a new Decoder lives on.  The reference's constructors have no device argument,
+// so the choice comes from the environment:
+//   QB_DEVICE=<ordinal>        every Decoder on that GPU (default 0)
+//   QB_DEVICES=<o0,o1,...>     Decoders are dealt round-robin over the list - the reference
+//                              builds one Decoder per worker thread (decode_batch,
+//                              decoder.cpp:636-641; run_campaign, noise.cpp:236-254), so its
+//                              own worker fan-out then spreads over the GPUs of the node.
+int next_device() {
+  static std::atomic<unsigned> counter{0};
+  auto parse = [](const std::string& tok) {
+    std::size_t pos = 0;
+    int v = -1;
+    try {
+      v = std::stoi(tok, &pos);
+    } catch (const std::exception&) {
+      pos = 0;
+    }
+    if (pos != tok.size() || tok.empty() || v < 0) {
+      throw std::invalid_argument("QB_DEVICE / QB_DEVICES: '" + tok + "' is not a CUDA ordinal");
+    }
+    return v;
+  };
+  if (const char* list = std::getenv("QB_DEVICES"); list && *list) {
+    std::vector<int> devs;
+    std::string tok;
+    for (const char* c = list;; ++c) {
+      if (*c == ',' || *c == 0) {
+        devs.push_back(parse(tok));
+        tok.clear();
+        if (*c == 0) break;
+      } else {
+        tok.push_back(*c);
+      }
+    }
+    return devs[counter.fetch_add(1, std::memory_order_relaxed) % devs.size()];
+  }
+  if (const char* one = std::getenv("QB_DEVICE"); one && *one) return parse(one);
+  return 0;
+}
+
 qb_decoder* make_handle(const TannerGraph& graph, const DecoderConfig& cfg,
                         const std::vector<qb_segment>& segs) {
   qb_graph g{static_cast<std::uint32_t>(graph.num_checks),
@@ -52,7 +95,8 @@ qb_decoder* make_handle(const TannerGraph& graph, const DecoderConfig& cfg,
               cfg.priors.empty() ? nullptr : cfg.priors.data(), cfg.priors.size()};
   qb_decoder* h = nullptr;
   const qb_status st = qb_decoder_create(&g, segs.empty() ? nullptr : segs.data(),
-                                         static_cast<std::uint32_t>(segs.size()), &c, 0, &h);
+                                         static_cast<std::uint32_t>(segs.size()), &c, next_device(),
+                                         &h);
   if (st != QB_OK) raise(st, nullptr);
   return h;
 }

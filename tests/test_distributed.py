@@ -1,8 +1,9 @@
-"""Multi-rank host path on CPU (gloo, world_size 2): the trial partition and the
-final counter all-reduce of paper_2508_07879_b200.campaign - the only
-collective on the path - checked against a single-process run.
-Each rank classifies its shard with the CPU oracle standing in for the GPU
-kernels (this is a test: the product path never does that)."""
+"""Multi-rank host path on CPU (gloo, world_size 2): campaign.run_campaign(world=2) itself -
+its trial partition and the final counter all-reduce, the only collective on the path
+ - checked against a single-process run, plus bench.py's own rank spawning.
+The per-rank counter function is INJECTED (range_fn): each rank classifies its shard with
+the CPU oracle standing in for the GPU kernels (this is a test: the product path never
+does that), everything around it is the product's code."""
 import os
 import socket
 import sys
@@ -63,12 +64,18 @@ def _worker(rank, world, port, trials, out):
                       WORLD_SIZE=str(world))
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
-    from paper_2508_07879_b200.campaign import CampaignResult, reduce_counters, shard
+    from paper_2508_07879_b200.campaign import COUNTER_NAMES, run_campaign
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    lo, hi = shard(trials, world, rank)
-    total = reduce_counters(_oracle_counters(lo, hi))
-    res = CampaignResult.from_counters(total)
-    out.put((rank, total.tolist(), res.logical_error_rate, (lo, hi)))
+    seen = []
+
+    def range_fn(p, seed, first, count):  # stands in for Campaign.run_range on this rank's GPU
+        seen.append((first, first + count))
+        return _oracle_counters(first, first + count)
+
+    res = run_campaign(None, 0.04, 20260822, trials, None, world=world, rank=rank,
+                       range_fn=range_fn, reduce_device="cpu")
+    total = [getattr(res, k) for k in COUNTER_NAMES[:6]] + [res.trials]
+    out.put((rank, total, res.logical_error_rate, res.mean_iterations, seen[0] if seen else (0, 0)))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -88,11 +95,39 @@ def test_two_rank_campaign_reduction_matches_single_process():
         p.join(timeout=60)
         assert p.exitcode == 0
     single = _oracle_counters(0, trials)
-    for rank, total, ler, (lo, hi) in results:
+    want = CampaignResult.from_counters(single)
+    for rank, total, ler, mean_it, (lo, hi) in results:
         assert (lo, hi) == shard(trials, world, rank)
-        assert total == single.tolist(), f"rank {rank} sees a different aggregate"
-        assert ler == CampaignResult.from_counters(single).logical_error_rate
+        assert total == [int(x) for x in single[:6]] + [trials], f"rank {rank} sees a different aggregate"
+        assert ler == want.logical_error_rate and mean_it == want.mean_iterations
     assert single[9] == trials
+
+
+def test_run_campaign_refuses_world_gt_1_without_a_process_group():
+    """One shard's counters must never be returned as the campaign's (reduce_counters)."""
+    from paper_2508_07879_b200.campaign import COUNTER_NAMES, run_campaign
+    fn = lambda p, seed, first, count: np.zeros(len(COUNTER_NAMES), dtype=np.uint64)
+    with pytest.raises(RuntimeError, match="no process group"):
+        run_campaign(None, 0.01, 1, 100, None, world=2, rank=0, range_fn=fn, reduce_device="cpu")
+    with pytest.raises(ValueError, match="rank"):
+        run_campaign(None, 0.01, 1, 100, None, world=2, rank=2, range_fn=fn, reduce_device="cpu")
+    assert run_campaign(None, 0.01, 1, 100, None, range_fn=fn).trials == 0
+
+
+def test_bench_spawns_its_own_ranks():
+    """`python bench.py --gpus 2` with no launcher must start 2 ranks itself and say so
+    (--dry-spawn: the rank plumbing on gloo, no GPU)."""
+    import json
+    import subprocess
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-spawn",
+                        "--shots", "100001"], capture_output=True, text=True, timeout=240, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["gpus_requested"] == 2
+    assert line["trials"] == 100001 and line["exact"] == 100001
+    assert line["trial_id_sum"] == line["trial_id_sum_expected"]
 
 
 def test_shard_partition_is_contiguous_and_complete():

@@ -134,3 +134,36 @@ def test_skip_sampler_campaign_within_reference_ci_and_partition_independent(ref
         assert not np.array_equal(camp.run_range(0.03, 99, 0, 5000), whole)
     finally:
         camp.close()
+
+
+def test_multi_gpu_entry_point_on_the_gpus_present(ref):
+    """qb_campaign_run_multi: one decoder per visible GPU, contiguous shards, ONE
+    ncclAllReduce of the ten counters (NCCL bound at run time).  On a 1-GPU box this still
+    exercises the whole path - communicator creation, grouped all-reduce, agreement check -
+    and the result must equal the reference's run_campaign."""
+    import ctypes as C
+    import torch
+    from paper_2508_07879_b200 import _lib
+    lib = _lib.load()
+    code = codes.make_code("bb72")
+    cfg = DecoderConfig(max_iterations=10)
+    ngpu = torch.cuda.device_count()
+    camps = [Campaign(code, cfg, device=d) for d in range(ngpu)]
+    try:
+        handles = (C.c_void_p * ngpu)(*[c.decoder._h for c in camps])
+        counters = np.zeros(10, dtype=np.uint64)
+        for first, count in ((0, 2500), (2500, 1500)):  # ADDS, like qb_campaign_run
+            st = lib.qb_campaign_run_multi(handles, ngpu, 20260822, 0.01, None, first, count,
+                                           counters.ctypes.data_as(_lib.u64p))
+            assert st == 0, lib.qb_last_error(camps[0].decoder._h).decode()
+        theirs = ref.run_campaign(ref.code("bb72"), 0, 0.01, 20260822, 4000, cfg, workers=0)
+        _same(CampaignResult.from_counters(counters), theirs)
+        assert np.array_equal(counters, camps[0].run_range(0.01, 20260822, 0, 4000))
+        # two handles on one device are refused (NCCL needs one rank per GPU)
+        dup = (C.c_void_p * 2)(camps[0].decoder._h, camps[0].decoder._h)
+        st = lib.qb_campaign_run_multi(dup, 2, 1, 0.01, None, 0, 10, counters.ctypes.data_as(_lib.u64p))
+        assert st == _lib.QB_INVALID_ARGUMENT
+        assert b"one decoder per GPU" in lib.qb_last_error(camps[0].decoder._h)
+    finally:
+        for c in camps:
+            c.close()

@@ -56,3 +56,23 @@ def test_reference_acceptance_runner_passes_against_the_gpu_decoder():
     print(out.stdout[-3000:])
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
     assert out.stdout.count("PASS") >= 8 and "FAIL" not in out.stdout
+
+
+@pytest.mark.gpu
+def test_dropin_shim_device_selection_from_the_environment():
+    """The reference's constructors carry no device argument: the shim reads QB_DEVICE /
+    QB_DEVICES (round-robin over the list, one Decoder per reference worker thread)."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "acceptance_dropin")
+    if not os.path.exists(exe):
+        pytest.skip("prebuilt oracle/_ref/acceptance_dropin absent (needs /root/reference to build)")
+    base = dict(os.environ)
+    base["LD_LIBRARY_PATH"] = os.pathsep.join([os.path.join(ROOT, "paper_2508_07879_b200"),
+                                               base.get("LD_LIBRARY_PATH", "")])
+    cwd = os.path.join(ROOT, "oracle", "_ref")
+    ok = subprocess.run([exe], capture_output=True, text=True, env={**base, "QB_DEVICES": "0,0"},
+                        timeout=900, cwd=cwd)
+    assert ok.returncode == 0 and "FAIL" not in ok.stdout, ok.stdout[-2000:] + ok.stderr[-2000:]
+    for bad in ({"QB_DEVICE": "gpu0"}, {"QB_DEVICE": "97"}):
+        out = subprocess.run([exe], capture_output=True, text=True, env={**base, **bad},
+                             timeout=900, cwd=cwd)
+        assert out.returncode != 0 or "FAIL" in out.stdout, bad
