@@ -83,9 +83,9 @@ typedef struct qb_decoder qb_decoder;
 
 /* Kernel selection and I/O policy knobs (qb_set_option). */
 typedef enum {
-  /* 0 = auto, 1 = generic CSR kernel, 2 = regular (register-resident tables)
-   * kernels; selecting 2 on a graph they cannot run is an error.  3 = like 0
-   * but without the lean single-shot cluster kernel (regular v2 kernels). */
+  /* 0 = auto, 1 = generic CSR kernel (the "second opinion": any graph, tables read from
+   * memory), 2 = auto, but it is an error unless the graph is (6,3)-regular (i.e. the
+   * lean kernels serve it). */
   QB_OPT_KERNEL = 0,
   /* Single-shot I/O: 0 = syndrome in the kernel parameters, results to mapped
    * pinned host memory + completion flag (no memcpy, no stream sync);
@@ -94,26 +94,28 @@ typedef enum {
    * cluster polls a block of mapped host memory, so a decode costs no kernel
    * launch at all (the kernel retires after QB_OPT_DOORBELL_IDLE_MS idle). */
   QB_OPT_LATENCY_IO = 1,
-  /* Single-shot launch shape: 0 = auto, 1 = one CTA per shot, 2 = one thread
-   * block cluster per shot (one CTA per segment, results merged over DSMEM). */
+  /* Single-shot launch shape: 0 = auto / 2 = one thread block cluster per shot, CTA rank =
+   * segment (a decoder built from a plain graph has one segment: one CTA per shot);
+   * 1 = one CTA per shot whatever the segment count (one warp group per segment: the
+   * generic kernel). */
   QB_OPT_LATENCY_SHAPE = 2,
   /* Threads per segment group (0 = auto). */
   QB_OPT_GROUP_THREADS = 3,
   /* CTAs per SM for the persistent batch kernel (0 = auto). */
   QB_OPT_BATCH_CTAS_PER_SM = 4,
   /* Batch item kernel variant (checks x variables per thread, CTAs per SM):
-   * 0 = auto, 1..6 = a specific instantiation (see kLeanVariants). */
+   * 0 = auto, else one of the instantiations 1, 3, 4, 6, 8, 11 (see kLeanVariants). */
   QB_OPT_BATCH_VARIANT = 5,
-  /* Single-shot regular kernel: 1, 2 or 4 checks (and twice as many variables)
+  /* Single-shot cluster kernel: 1 or 2 checks (and twice as many variables)
    * per thread; 0 = auto. */
   QB_OPT_LATENCY_NODES_PER_THREAD = 6,
-  /* Regular kernel: 1 (default) lets uniform-prior decoders use the
+  /* (6,3)-regular kernels: 1 (default) lets uniform-prior decoders use the
    * instantiation with the prior as a kernel constant and (fp32) without the
    * provably unreachable 1e30 clamp; 0 forces the general instantiation. */
   QB_OPT_FAST_PATH = 7,
-  /* Batch work decomposition on regular codes: 0 = auto, 1 = one CTA per shot
-   * (one warp group per segment), 2 = one CTA per (shot, segment) work item
-   * drawn from per-segment queues (the lean item kernel; the auto choice). */
+  /* Batch work decomposition: 0 = auto / 2 = one CTA per (shot, segment) work item drawn
+   * from per-segment queues (the lean and degree-padded item kernels), 1 = one CTA per
+   * shot with one warp group per segment (the generic kernel). */
   QB_OPT_BATCH_SHAPE = 8,
   QB_OPT_DOORBELL_IDLE_MS = 9,
   /* Half and int8 modes, batch calls on (6,3)-regular codes: 1 (default) = decode
@@ -206,7 +208,11 @@ qb_status qb_decode_batch(qb_decoder* h, uint64_t shots,
                           uint8_t* converged, uint32_t* iterations);
 
 /* Same, with every buffer already resident in DEVICE memory (16-byte aligned)
- * and the launch enqueued on `stream` (a cudaStream_t, NULL = default). */
+ * and the launch enqueued on `stream` (a cudaStream_t, NULL = default); returns without
+ * synchronising.  A decoder is NOT thread-safe (as the reference's, decoder.hpp:75-76), but
+ * one host thread may keep several of these launches in flight on different streams: each
+ * takes its own scheduler words from a ring of 16.  qb_classify_batch_device and the
+ * campaign calls share one counter buffer per handle and block until their result is back. */
 qb_status qb_decode_batch_device(qb_decoder* h, uint64_t shots,
                                  const uint64_t* d_syndromes,
                                  uint64_t* d_estimates,

@@ -26,12 +26,30 @@
 //    1 + 2 * iterations barriers per item.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
-#include "kernel_regular.cuh"
+#include "kernel_generic.cuh"
 
 namespace qb {
 
+namespace cg = cooperative_groups;
+
+constexpr int kDC = 6;  // the bivariate-bicycle family: every check has degree 6,
+constexpr int kDV = 3;  // every variable degree 3
 constexpr uint32_t kNoShot = 0xffffffffu;
+
+// min1 / min2 of six non-negative integer keys (13 min/max operations).
+__device__ __forceinline__ void two_smallest6(const int32_t (&a)[6], int32_t& m1, int32_t& m2) {
+  const int32_t l0 = min(a[0], a[1]), h0 = max(a[0], a[1]);
+  const int32_t l1 = min(a[2], a[3]), h1 = max(a[2], a[3]);
+  const int32_t l2 = min(a[4], a[5]), h2 = max(a[4], a[5]);
+  m1 = min(min(l0, l1), l2);
+  // Everything except one instance of the minimum: the other two pair-minima
+  // (their smaller one is the median of the three) and the three pair-maxima.
+  const int32_t med = max(min(l0, l1), min(max(l0, l1), l2));
+  m2 = min(med, min(min(h0, h1), h2));
+}
 
 // Message-block layout per arithmetic: byte stride between checks, byte offset
 // of the r half.  Strides are conflict-free for the check-side vector access of

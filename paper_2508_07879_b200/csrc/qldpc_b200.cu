@@ -24,7 +24,6 @@
 
 #include "common.cuh"
 #include "kernel_generic.cuh"
-#include "kernel_regular.cuh"
 #include "kernel_lean.cuh"
 #include "kernel_lean_h2.cuh"
 #include "kernel_ell.cuh"
@@ -91,6 +90,13 @@ using LatKernelFn = void (*)(DecodeParams, ShotIO, LatencyCtl, SynInline);
 
 constexpr int kPipeSlots = 3;                      // qb_decode_batch: chunks in flight
 constexpr int kSchedWords = 2 + kMaxSegments;      // scheduler words per concurrent launch
+// Every launch needs its own ticket / finished-CTA words while it is in flight (the last CTA
+// rewinds them).  Slot 0: single shots; 1 .. kPipeSlots: the chunk pipeline of
+// qb_decode_batch; the rest is a ring handed out launch by launch to the device-buffer entry
+// points (qb_decode_batch_device on caller streams, campaigns), so launches of one handle on
+// DIFFERENT streams do not share words unless more than kSchedRing of them are in flight.
+constexpr int kSchedRing = 16;
+constexpr int kSchedSlots = 1 + kPipeSlots + kSchedRing;
 
 struct LaunchPlan {
   KernelFn kernel = nullptr;
@@ -121,6 +127,7 @@ struct qb_decoder {
   int arith = 0;
   std::vector<void*> dev_allocs;  // tables, freed in the destructor
   unsigned int* d_sched = nullptr;
+  uint32_t sched_next = 0;  // next ring slot
 
   // single-shot staging: mapped pinned host memory (+ device mirrors for the
   // memcpy protocol)
@@ -345,54 +352,24 @@ KernelFn generic_kernel(int arith) {
   }
 }
 
-// (6,3)-regular instantiations: nodes-per-thread class 1, 2, 4 = (checks, vars)
-// per thread (1,2), (2,4), (4,8); FAST = uniform prior (+ clamp-free proof for fp32).
-template <class A, bool kFast>
-KernelFn regular_kernel_tf(int npt, bool cluster) {
-  if (cluster) {
-    switch (npt) {
-      case 1: return decode_regular_cluster_kernel<A, 1, 2, kFast>;
-      case 2: return decode_regular_cluster_kernel<A, 2, 4, kFast>;
-      default: return decode_regular_cluster_kernel<A, 4, 8, kFast>;
-    }
-  }
-  switch (npt) {
-    case 1: return decode_regular_kernel<A, 1, 2, kFast, 1024, 1>;
-    case 2: return decode_regular_kernel<A, 2, 4, kFast, 512, 2>;
-    default: return decode_regular_kernel<A, 4, 8, kFast, 256, 4>;
-  }
-}
-
-template <class A>
-KernelFn regular_kernel_t(int npt, bool cluster, bool fast) {
-  return fast ? regular_kernel_tf<A, true>(npt, cluster) : regular_kernel_tf<A, false>(npt, cluster);
-}
-
-KernelFn regular_kernel(int arith, int npt, bool cluster, bool fast) {
-  switch (arith) {
-    case QB_ARITH_FLOAT: return regular_kernel_t<ArithF32>(npt, cluster, fast);
-    case QB_ARITH_INT8: return regular_kernel_t<ArithI8>(npt, cluster, fast);
-    case QB_ARITH_INT16: return regular_kernel_t<ArithI16>(npt, cluster, fast);
-    default: return regular_kernel_t<ArithF16>(npt, cluster, fast);
-  }
-}
-
 // Lean item-kernel variants: (checks, variables) per thread, launch bounds.
 struct LeanVariant {
   int cpt, vpt, maxt, minb;
 };
+// Variant numbers are stable identifiers (QB_OPT_BATCH_VARIANT); 2, 5, 7, 9 and 10 were
+// measured, never selected by the loader and retired (maxt = 0).
 constexpr LeanVariant kLeanVariants[] = {
-    {1, 2, 1024, 1},  // 1: widest CTA, any segment size up to 1024 checks
-    {1, 2, 448, 3},   // 2: 48 registers, three 13-warp CTAs per SM on [[784,24,24]]
+    {1, 2, 1024, 1},  // 1: widest CTA, any segment size up to 960 checks
+    {0, 0, 0, 0},     // 2: retired
     {2, 4, 256, 3},   // 3
-    {3, 5, 192, 5},   // 4
-    {4, 8, 128, 6},   // 5
+    {3, 5, 192, 5},   // 4: 64 registers, six CTAs per SM on [[784,24,24]]: the early-stop choice
+    {0, 0, 0, 0},     // 5: retired
     {2, 4, 512, 2},   // 6
-    {3, 5, 160, 5},   // 7: 80 registers, five 5-warp CTAs per SM
-    {3, 5, 160, 4},   // 8: 102 registers
-    {2, 4, 224, 4},   // 9: 72 registers, four 7-warp CTAs per SM
-    {3, 5, 160, 7},   // 10: 56 registers, seven 5-warp CTAs per SM
-    {3, 5, 160, 8},   // 11: 48 registers, eight 5-warp CTAs per SM
+    {0, 0, 0, 0},     // 7: retired
+    {3, 5, 160, 4},   // 8: 102 registers, the packed (two shots per thread) kernels' choice
+    {0, 0, 0, 0},     // 9: retired
+    {0, 0, 0, 0},     // 10: retired
+    {3, 5, 160, 8},   // 11: 48 registers, eight 5-warp CTAs per SM: fixed iteration counts
 };
 constexpr int kNumLeanVariants = sizeof(kLeanVariants) / sizeof(kLeanVariants[0]);
 
@@ -400,14 +377,9 @@ template <class A, bool kFast>
 KernelFn lean_kernel_tf(int variant) {
   switch (variant) {
     case 1: return decode_lean_kernel<A, 1, 2, kFast, 1024, 1>;
-    case 2: return decode_lean_kernel<A, 1, 2, kFast, 448, 3>;
     case 3: return decode_lean_kernel<A, 2, 4, kFast, 256, 3>;
     case 4: return decode_lean_kernel<A, 3, 5, kFast, 192, 5>;
-    case 5: return decode_lean_kernel<A, 4, 8, kFast, 128, 6>;
-    case 7: return decode_lean_kernel<A, 3, 5, kFast, 160, 5>;
     case 8: return decode_lean_kernel<A, 3, 5, kFast, 160, 4>;
-    case 9: return decode_lean_kernel<A, 2, 4, kFast, 224, 4>;
-    case 10: return decode_lean_kernel<A, 3, 5, kFast, 160, 7>;
     case 11: return decode_lean_kernel<A, 3, 5, kFast, 160, 8>;
     default: return decode_lean_kernel<A, 2, 4, kFast, 512, 2>;
   }
@@ -442,14 +414,11 @@ template <bool kFast>
 KernelFn lean_h2_kernel_tf(int variant) {
   switch (variant) {
     case 1: return decode_lean_h2_kernel<1, 2, kFast, 1024, 1>;
-    case 2: return decode_lean_h2_kernel<1, 2, kFast, 448, 3>;
     case 3: return decode_lean_h2_kernel<2, 4, kFast, 256, 3>;
     case 4: return decode_lean_h2_kernel<3, 5, kFast, 192, 5>;
-    case 5: return decode_lean_h2_kernel<4, 8, kFast, 128, 6>;
-    case 7: return decode_lean_h2_kernel<3, 5, kFast, 160, 5>;
     case 8: return decode_lean_h2_kernel<3, 5, kFast, 160, 4>;
-    case 9: return decode_lean_h2_kernel<2, 4, kFast, 224, 4>;
-    default: return decode_lean_h2_kernel<2, 4, kFast, 512, 2>;
+    case 6: return decode_lean_h2_kernel<2, 4, kFast, 512, 2>;
+    default: return nullptr;
   }
 }
 
@@ -709,7 +678,7 @@ void choose_plans(qb_decoder* h) {
   drop_latency_graphs(h);  // they bake in the kernel and its launch shape
   const bool use_regular = h->regular63 && h->opt_kernel != 1;
   if (h->opt_kernel == 2 && !h->regular63) {
-    fail(QB_INVALID_ARGUMENT, "regular kernel needs a (6,3)-regular graph with at most 8 segments");
+    fail(QB_INVALID_ARGUMENT, "the (6,3)-regular kernels need a (6,3)-regular graph with at most 8 segments");
   }
   h->lat_ell = LaunchPlan{};
   if (!use_regular) {
@@ -777,29 +746,13 @@ void choose_plans(qb_decoder* h) {
     }
     return;
   }
-  auto regular_plan = [&](int npt, bool cluster) {
-    LaunchPlan pl{};
-    pl.regular = true;
-    pl.npt = npt;
-    pl.cluster = cluster;
-    pl.kernel = regular_kernel(h->arith, npt, cluster, h->fast_ok && h->opt_fast != 0);
-    pl.name = cluster ? "decode_regular_cluster_kernel" : "decode_regular_kernel";
-    pl.ngroups = P.nseg;
-    pl.group_threads = regular_group_threads(P, npt, 2 * npt);
-    finish_plan(h, pl);
-    return pl;
-  };
-  const uint32_t max_block[5] = {0, 1024, 512, 0, 256};
-  auto fits = [&](int npt, bool cluster) {
-    const uint32_t T = regular_group_threads(P, npt, 2 * npt);
-    return (cluster ? T : T * P.nseg) <= (cluster ? 1024u : max_block[npt]);
-  };
-  // single shot: fewest nodes per thread that fits; a cluster when there is more
-  // than one segment (unless the caller pins the shape)
-  const bool want_cluster = h->opt_latency_shape == 2 || (h->opt_latency_shape == 0 && P.nseg > 1);
+  // single shot: the lean cluster kernel, CTA rank = segment (a cluster of one for a decoder
+  // built from a plain graph: ONE CTA per shot); QB_OPT_LATENCY_SHAPE = 1 asks for one CTA
+  // per shot whatever the segment count, which is the generic kernel's shape
+  h->lat = generic_plan(h);
   h->lat_lean_kernel = nullptr;
-  if (h->opt_latency_shape != 1 && h->opt_kernel != 3 && P.seg_mmax <= 960 &&
-      P.seg_nmax <= 960 * 2 && P.syn_w32 <= kInlineSynWords) {
+  if (h->opt_latency_shape != 1 && P.seg_mmax <= 960 && P.seg_nmax <= 960 * 2 &&
+      P.syn_w32 <= kInlineSynWords) {
     for (int npt : {1, 2}) {
       if (h->opt_latency_npt && npt != h->opt_latency_npt) continue;
       const uint32_t T = regular_group_threads(P, npt, 2 * npt);
@@ -815,16 +768,6 @@ void choose_plans(qb_decoder* h) {
       break;
     }
   }
-  bool lat_done = false;
-  for (int npt : {1, 2, 4}) {
-    if (h->opt_latency_npt && npt != h->opt_latency_npt) continue;
-    if (fits(npt, want_cluster)) {
-      h->lat = regular_plan(npt, want_cluster);
-      lat_done = true;
-      break;
-    }
-  }
-  if (!lat_done) h->lat = generic_plan(h);
   bool bat_done = false;
   const bool fast = h->fast_ok && h->opt_fast != 0;
   if (h->opt_batch_shape != 1 && P.seg_mmax <= 960) {
@@ -836,12 +779,16 @@ void choose_plans(qb_decoder* h) {
     // measured on [[784,24,24]] (fp32): with early stop the 64-register build at six CTAs per
     // SM wins (107.9 vs 101.1 M/s); at a fixed iteration count the 48-register build at eight
     // CTAs per SM hides the dependent chains better (24.8 vs 23.5 M/s)
-    const int order_f32[] = {4, 3, 5, 2, 6, 1, 1}, order_h2[] = {8, 3, 5, 2, 6, 1, 1},
-              order_fixed[] = {11, 4, 3, 5, 2, 6, 1};
+    const int order_f32[] = {4, 3, 6, 1, 1, 1, 1}, order_h2[] = {8, 3, 6, 1, 1, 1, 1},
+              order_fixed[] = {11, 4, 3, 6, 1, 1, 1};
     const int* order_auto = pair_wanted ? order_h2 : P.early ? order_f32 : order_fixed;
     for (int idx = 0; idx < 7 && !bat_done; ++idx) {
       const int variant = h->opt_batch_npt ? static_cast<int>(h->opt_batch_npt) : order_auto[idx];
       const LeanVariant& lv = kLeanVariants[variant - 1];
+      if (lv.maxt == 0) {
+        if (h->opt_batch_npt) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_VARIANT: that variant is retired (1, 3, 4, 6, 8, 11 exist)");
+        continue;
+      }
       const uint32_t T = regular_group_threads(P, lv.cpt, lv.vpt);
       if (T <= static_cast<uint32_t>(lv.maxt)) {
         KernelFn i8_pair = nullptr;
@@ -849,17 +796,19 @@ void choose_plans(qb_decoder* h) {
           i8_pair = fast ? lean_h2_i8_kernel_tf<true>(variant) : lean_h2_i8_kernel_tf<false>(variant);
           if (!i8_pair && !h->opt_batch_npt) continue;  // shape not built for int8 pairs: next one
         }
-        const bool pair = pair_wanted && (!i8 || i8_pair != nullptr);
+        KernelFn h2_pair = nullptr;
+        if (!i8 && pair_wanted) {
+          h2_pair = fast ? lean_h2_kernel_tf<true>(variant) : lean_h2_kernel_tf<false>(variant);
+          if (!h2_pair && !h->opt_batch_npt) continue;  // shape not built for pairs: next one
+        }
+        const bool pair = pair_wanted && (i8 ? i8_pair != nullptr : h2_pair != nullptr);
         LaunchPlan pl{};
         pl.regular = true;
         pl.items = true;
         pl.lean = true;
         pl.npt = variant;
         pl.pair = pair;
-        pl.kernel = !pl.pair ? lean_kernel(h->arith, variant, fast)
-                    : i8     ? i8_pair
-                    : fast   ? lean_h2_kernel_tf<true>(variant)
-                             : lean_h2_kernel_tf<false>(variant);
+        pl.kernel = !pl.pair ? lean_kernel(h->arith, variant, fast) : i8 ? i8_pair : h2_pair;
         pl.name = pl.pair ? "decode_lean_h2_kernel" : "decode_lean_kernel";
         pl.ngroups = 1;
         pl.group_threads = T;
@@ -871,13 +820,7 @@ void choose_plans(qb_decoder* h) {
       }
     }
   }
-  for (int npt : {2, 4, 1}) {
-    if (!bat_done && fits(npt, false)) {
-      h->bat = regular_plan(npt, false);
-      bat_done = true;
-    }
-  }
-  if (!bat_done) h->bat = generic_plan(h);
+  if (!bat_done) h->bat = generic_plan(h);  // QB_OPT_BATCH_SHAPE = 1, or segments over 960 checks
 }
 
 void launch_plan(qb_decoder* h, const LaunchPlan& pl, const ShotIO& io, unsigned grid,
@@ -976,8 +919,9 @@ void require_soft(qb_decoder* h, const char* who) {
 
 void run_batch_device(qb_decoder* h, uint64_t shots, const uint32_t* d_syn, uint32_t* d_est,
                       uint32_t* d_res, uint8_t* d_conv, uint32_t* d_iters, cudaStream_t stream,
-                      int sched_slot = 0, const void* d_soft = nullptr) {
+                      int sched_slot = -1, const void* d_soft = nullptr) {
   if (shots == 0) return;
+  if (sched_slot < 0) sched_slot = 1 + kPipeSlots + static_cast<int>(h->sched_next++ % kSchedRing);
   if (shots > 0x7fff0000ull) fail(QB_INVALID_ARGUMENT, "too many shots for one launch");
   ShotIO io{};
   io.soft = d_soft;
@@ -1074,6 +1018,11 @@ bool records_ready(const qb_decoder* h, uint32_t seq) {
       if (rec[s * h->rec_stride + 8 * k] != seq) return false;
     }
   }
+  // The data words are read after this returns: keep those loads behind the tag loads on
+  // weakly ordered hosts (aarch64 / Grace).  The protocol relies on each 32-byte sector
+  // store of the GPU (eight adjacent lanes of one STG over PCIe / C2C) becoming visible to
+  // the host as a unit - true of every platform this runs on, not an architectural promise.
+  std::atomic_thread_fence(std::memory_order_acquire);
   return true;
 }
 
@@ -1296,6 +1245,8 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
 }
 
 }  // namespace
+
+qb_status set_option_unchecked(qb_decoder* h, int option, int64_t value);
 
 extern "C" {
 
@@ -1673,8 +1624,8 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
     }
     make_plans(h);
 
-    CUDA_TRY(cudaMalloc(&h->d_sched, kPipeSlots * kSchedWords * sizeof(unsigned int)));
-    CUDA_TRY(cudaMemset(h->d_sched, 0, kPipeSlots * kSchedWords * sizeof(unsigned int)));
+    CUDA_TRY(cudaMalloc(&h->d_sched, kSchedSlots * kSchedWords * sizeof(unsigned int)));
+    CUDA_TRY(cudaMemset(h->d_sched, 0, kSchedSlots * kSchedWords * sizeof(unsigned int)));
     for (int k = 0; k < kPipeSlots; ++k) {
       CUDA_TRY(cudaStreamCreateWithFlags(&h->pipe_stream[k], cudaStreamNonBlocking));
       CUDA_TRY(cudaEventCreateWithFlags(&h->pipe_event[k], cudaEventDisableTiming));
@@ -1720,10 +1671,41 @@ void qb_decoder_destroy(qb_decoder* h) { destroy(h); }
 
 qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
   if (!h) return QB_INVALID_ARGUMENT;
+  // a value the launch planner rejects must not stick: remember the plan-affecting options
+  // and put them back (and re-plan) if make_plans throws
+  struct Saved {
+    int64_t kernel, io, shape, threads, ctas, npt, lat_npt, bshape, pair, idle, fast, spread;
+  } const old{h->opt_kernel, h->opt_latency_io, h->opt_latency_shape, h->opt_group_threads,
+              h->opt_batch_ctas, h->opt_batch_npt, h->opt_latency_npt, h->opt_batch_shape,
+              h->opt_batch_pair, h->opt_idle_ms, h->opt_fast, h->opt_slot_spread};
+  const qb_status st = set_option_unchecked(h, option, value);
+  if (st != QB_OK) {
+    const std::string why = h->err;
+    h->opt_kernel = old.kernel;
+    h->opt_latency_io = old.io;
+    h->opt_latency_shape = old.shape;
+    h->opt_group_threads = old.threads;
+    h->opt_batch_ctas = old.ctas;
+    h->opt_batch_npt = old.npt;
+    h->opt_latency_npt = old.lat_npt;
+    h->opt_batch_shape = old.bshape;
+    h->opt_batch_pair = old.pair;
+    h->opt_idle_ms = old.idle;
+    h->opt_fast = old.fast;
+    h->opt_slot_spread = old.spread;
+    guarded(h, [&] { make_plans(h); });  // the previous options planned fine before
+    h->err = why;
+  }
+  return st;
+}
+
+}  // extern "C"
+
+qb_status set_option_unchecked(qb_decoder* h, int option, int64_t value) {
   return guarded(h, [&] {
     switch (option) {
       case QB_OPT_KERNEL:
-        if (value < 0 || value > 3) fail(QB_INVALID_ARGUMENT, "QB_OPT_KERNEL: 0 .. 3");
+        if (value < 0 || value > 2) fail(QB_INVALID_ARGUMENT, "QB_OPT_KERNEL: 0 .. 2");
         h->opt_kernel = value;
         break;
       case QB_OPT_BATCH_VARIANT:
@@ -1776,8 +1758,8 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
         h->opt_fast = value;
         break;
       case QB_OPT_LATENCY_NODES_PER_THREAD:
-        if (value != 0 && value != 1 && value != 2 && value != 4) {
-          fail(QB_INVALID_ARGUMENT, "QB_OPT_LATENCY_NODES_PER_THREAD: 0, 1, 2 or 4");
+        if (value != 0 && value != 1 && value != 2) {
+          fail(QB_INVALID_ARGUMENT, "QB_OPT_LATENCY_NODES_PER_THREAD: 0, 1 or 2");
         }
         h->opt_latency_npt = value;
         break;
@@ -1806,6 +1788,8 @@ qb_status qb_set_option(qb_decoder* h, int option, int64_t value) {
   });
 }
 
+extern "C" {
+
 int64_t qb_get_option(const qb_decoder* h, int option) {
   if (!h) return -1;
   switch (option) {
@@ -1814,7 +1798,7 @@ int64_t qb_get_option(const qb_decoder* h, int option) {
     case QB_OPT_LATENCY_SHAPE: return h->opt_latency_shape;
     case QB_OPT_GROUP_THREADS: return h->lat.group_threads;
     case QB_OPT_BATCH_VARIANT: return h->bat.regular ? h->bat.npt : 0;
-    case QB_OPT_LATENCY_NODES_PER_THREAD: return h->lat.regular ? h->lat.npt : 0;
+    case QB_OPT_LATENCY_NODES_PER_THREAD: return h->opt_latency_npt;
     case QB_OPT_INFO_BATCH_CTAS_PER_SM: return h->bat.ctas_per_sm;
     case QB_OPT_INFO_BATCH_BLOCK: return h->bat.block;
     case QB_OPT_INFO_LATENCY_BLOCK: return h->lat_lean_kernel ? h->lat_lean_block : h->lat.block;
@@ -2154,7 +2138,7 @@ void campaign_enqueue(qb_decoder* h, uint64_t seed, double p, const double* prob
     if (soft) {
       launch_soft_measure(h, seed, mu, sigma, first_trial + done, n, h->b_syn, h->b_soft, h->c_err, st);
     }
-    run_batch_device(h, n, h->b_syn, h->b_est, nullptr, h->b_conv, h->b_iters, st, 0,
+    run_batch_device(h, n, h->b_syn, h->b_est, nullptr, h->b_conv, h->b_iters, st, -1,
                      soft ? h->b_soft : nullptr);
     launch_classify(h, n, h->c_err, h->b_est, h->b_syn, h->b_conv, h->b_iters, st);
   }
@@ -2471,7 +2455,7 @@ qb_status qb_decode_batch_soft_device(qb_decoder* h, uint64_t shots, const uint6
     run_batch_device(h, shots, reinterpret_cast<const uint32_t*>(d_syndromes),
                      reinterpret_cast<uint32_t*>(d_estimates),
                      reinterpret_cast<uint32_t*>(d_residuals), d_converged, d_iterations,
-                     static_cast<cudaStream_t>(stream), 0, d_soft);
+                     static_cast<cudaStream_t>(stream), -1, d_soft);
   });
 }
 

@@ -257,3 +257,27 @@ def test_single_shots_through_the_degree_padded_kernel(oracle, mode):
             for k in range(len(syn2)):
                 one = dec.decode_segments(syn2[k])
                 assert all(np.array_equal(a, b[k]) for a, b in zip(one, want)), k
+
+
+def test_rejected_option_does_not_stick(oracle):
+    """qb_set_option validates through the launch planner; a value it rejects must leave the
+    handle exactly as it was (the old value restored, plans rebuilt), so that later unrelated
+    options and decodes still work."""
+    from paper_2508_07879_b200 import codes
+    g = codes.build_tanner_graph(codes.toy_code_3x6())
+    cfg = DecoderConfig(max_iterations=10)
+    syn = gf2.pack_bits(np.array([[1, 0, 1], [0, 1, 1]], dtype=np.uint8))
+    with Decoder(g, cfg) as dec:
+        want = dec.decode_batch_segments(syn)
+        with pytest.raises(ValueError, match="regular kernel"):
+            dec.set_option(0, 2)  # QB_OPT_KERNEL = regular kernels on a (4,2) toy graph
+        assert dec.get_option(0) == 0
+        dec.set_option(7, 0)      # an unrelated plan-affecting option still goes through
+        dec.set_option(7, 1)
+        got = dec.decode_batch_segments(syn)
+        assert all(np.array_equal(a, b) for a, b in zip(got, want))
+    code = codes.make_code("bb72")
+    with Decoder(code, DecoderConfig()) as dec:
+        with pytest.raises(ValueError):
+            dec.set_option(5, 12)  # QB_OPT_BATCH_VARIANT out of range
+        assert dec.get_option(5) != 12
