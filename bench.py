@@ -501,6 +501,60 @@ def measure_variants(args, code, d_syn, d_est, d_conv, d_its, stream):
                     "p_data": pq, "p_meas": pq, "shots_per_launch": shots5,
                     "convergence_rate": float((d_conv[:shots5].min(dim=1).values == 1).double().mean().item()),
                     "mean_iterations": float(its.max(dim=1).values.double().mean().item())}
+    # ---- config 5 AS NAMED: soft (noisy) syndromes.  Data flips at p, every check measured
+    # through a Gaussian channel with flip probability Phi(-mu/sigma) ~ p; the reliabilities
+    # |LLR_m| are per-shot priors of the absorbed measurement variables (qb_decode_batch_soft).
+    import math
+    mu, sigma = 1.0, 0.39
+    q_eff = 0.5 * math.erfc(mu / sigma / math.sqrt(2))
+    for arith, dt in (("int8", torch.int8), ("float", torch.float32)):
+        e_soft = torch.zeros((shots5, ge.num_checks), dtype=dt, device=dev)
+        for label, iters, early in (("cap50_early", 50, True), ("fixed10", 10, False)):
+            cfg = DecoderConfig(max_iterations=iters, early_termination=early, arithmetic=arith,
+                                priors=[llr] * ge.num_vars)
+            with Decoder(ge, cfg, segments=segs) as dec:
+                dec.generate_soft_syndromes(args.seed, pq, mu, sigma, shots5, e_syn.data_ptr(),
+                                            e_soft.data_ptr(), None, stream=stream)
+                f = lambda: dec.decode_batch_soft_device(shots5, e_syn.data_ptr(), e_soft.data_ptr(),
+                                                         e_est.data_ptr(), None, d_conv.data_ptr(),
+                                                         d_its.data_ptr(), stream)
+                for _ in range(3):
+                    f()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(3):
+                    f()
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / 3
+                its = d_its[:shots5].to(torch.int64)
+                eu = float(its.sum().item()) * (ge.num_edges // 2)
+                out[f"config5_soft_{arith}_{label}"] = {
+                    "decodes_per_s": shots5 / ms * 1e3, "edge_updates_per_s": eu / ms * 1e3,
+                    "kernel": "decode_ell_h2_kernel<soft>" if dec.get_option(10) else "decode_ell_kernel<soft>",
+                    "p_data": pq, "mu": mu, "sigma": sigma, "p_meas_effective": q_eff,
+                    "shots_per_launch": shots5, "soft_bytes_per_shot": ge.num_checks * e_soft.element_size(),
+                    "convergence_rate": float((d_conv[:shots5].min(dim=1).values == 1).double().mean().item()),
+                    "mean_iterations": float(its.max(dim=1).values.double().mean().item())}
+    from paper_2508_07879_b200.campaign import PhenomenologicalCampaign
+    for arith in ("int8", "float"):
+        pc = PhenomenologicalCampaign(code, DecoderConfig(max_iterations=50, arithmetic=arith), pq, q_eff)
+        try:
+            tr = 1 << 18
+            for name, fn in (("config5_campaign_hard", lambda first: pc.run_range(args.seed, first, tr)),
+                             ("config5_campaign_soft", lambda first: pc.run_range_soft(args.seed, mu, sigma, first, tr))):
+                fn(0)
+                t0 = time.perf_counter()
+                for r in range(3):
+                    c = fn((r + 1) * tr)
+                dt = (time.perf_counter() - t0) / 3
+                out[f"{name}_{arith}"] = {
+                    "trials_per_s": tr / dt, "trials_per_call": tr, "p_data": pq, "p_meas": q_eff,
+                    "failures_last_call": int(c[2] + c[3] + c[4] + c[5]),
+                    "timer": "host perf_counter around the blocking campaign call, mean of 3"}
+        finally:
+            pc.close()
     # ---- BASELINE config 4's loop, entirely on the device: sample -> syndrome -> decode ->
     # classify through qb_campaign_run, with the reference-exact sampler and the skip sampler
     from paper_2508_07879_b200 import _lib
