@@ -543,6 +543,23 @@ class Ref:
                                             C.byref(nnz)))
         return int(rows.value), int(cols.value), buf[:int(nnz.value)].copy()
 
+    def have_css_json(self) -> bool:
+        return hasattr(self.lib, "ref_have_css_json") and bool(self.lib.ref_have_css_json())
+
+    def css_json_load(self, text: str, base_dir: str = "") -> RefCode:
+        """The reference's load_css_json (proj/src/css_json.cpp:84-150)."""
+        out = C.c_void_p()
+        self._check(self.lib.ref_css_json_load(text.encode(), base_dir.encode(), C.byref(out)))
+        return RefCode(self, out)
+
+    def css_json_save(self, code: RefCode) -> str:
+        """The reference's save_css_json(code): self-contained descriptor, inline alists."""
+        need = C.c_uint64()
+        self._check(self.lib.ref_css_json_save(code.ptr, None, C.c_uint64(0), C.byref(need)))
+        buf = C.create_string_buffer(int(need.value))
+        self._check(self.lib.ref_css_json_save(code.ptr, buf, need, C.byref(need)))
+        return buf.value.decode()
+
     def host_descriptor(self) -> str:
         buf = C.create_string_buffer(512)
         self._check(self.lib.ref_host_descriptor(buf, C.c_uint64(512)))

@@ -21,6 +21,9 @@
 #include "qldpc/alist.hpp"
 #include "qldpc/bench.hpp"
 #include "qldpc/css_code.hpp"
+#ifdef REF_HAVE_CSS_JSON
+#include "qldpc/css_json.hpp"
+#endif
 #include "qldpc/decoder.hpp"
 #include "qldpc/gf2.hpp"
 #include "qldpc/noise.hpp"
@@ -572,6 +575,42 @@ int ref_load_alist(const char* text, std::uint64_t* rows, std::uint64_t* cols,
       }
     }
   });
+}
+
+// CSS-JSON descriptors (proj/src/css_json.cpp), when the build found json.hpp.
+// ref_css_json_load: text -> CssCode handle (ref_code_free).  ref_css_json_save: the
+// self-contained descriptor (inline alist payloads) of a code into buf; returns the length
+// needed (call again with a larger buffer if it exceeds len).
+int ref_have_css_json() {
+#ifdef REF_HAVE_CSS_JSON
+  return 1;
+#else
+  return 0;
+#endif
+}
+
+int ref_css_json_load(const char* text, const char* base_dir, void** out) {
+#ifdef REF_HAVE_CSS_JSON
+  return guarded([&] { *out = new CssCode(load_css_json(text, base_dir ? base_dir : "")); });
+#else
+  (void)text; (void)base_dir; (void)out;
+  g_error = "css_json not built";
+  return 2;
+#endif
+}
+
+int ref_css_json_save(const void* code, char* buf, std::uint64_t len, std::uint64_t* needed) {
+#ifdef REF_HAVE_CSS_JSON
+  return guarded([&] {
+    const std::string s = save_css_json(*static_cast<const CssCode*>(code));
+    *needed = s.size() + 1;
+    if (buf && len >= s.size() + 1) std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+#else
+  (void)code; (void)buf; (void)len; (void)needed;
+  g_error = "css_json not built";
+  return 2;
+#endif
 }
 
 int ref_host_descriptor(char* buf, std::uint64_t len) {

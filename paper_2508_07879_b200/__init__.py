@@ -11,6 +11,7 @@ from .codes import (CssCode, SparseMatrix, TannerGraph, build_bb_code, build_tan
                     extended_graph, make_code, make_css_code, toy_code_3x6)
 from .decoder import (DecodeOutcome, Decoder, DecoderConfig, decode, decode_batch,  # noqa: F401
                       decode_css)
+from . import alist, css_json  # noqa: F401  on-disk code formats (alist, CSS-JSON descriptors)
 from .gf2 import concat_bits, num_words, pack_bits, to_hex, unpack_bits  # noqa: F401
 
 __all__ = [

@@ -281,3 +281,58 @@ def test_rejected_option_does_not_stick(oracle):
         with pytest.raises(ValueError):
             dec.set_option(5, 12)  # QB_OPT_BATCH_VARIANT out of range
         assert dec.get_option(5) != 12
+
+
+GOLD_CODES = __import__("os").path.join(__import__("os").path.dirname(__import__("os").path.abspath(__file__)),
+                                         "golden", "codes")
+
+
+@pytest.mark.parametrize("mode", ["float", "int8", "int16"])
+def test_codes_loaded_from_alist_and_json_files_decode_like_the_oracle(oracle, mode):
+    """user-supplied matrices reach the degree-padded kernels through the
+    on-disk formats.  Hand-written alist fixtures (the reference's own toy text, unpadded and
+    zero-padded: proj/tests/test_alist.cpp:27-60), a committed irregular 40 x 70 matrix, and
+    CSS-JSON descriptors (alist-file and bb constructions) are loaded, decoded in batch and
+    compared with the oracle bit for bit."""
+    import os
+    from paper_2508_07879_b200 import alist, css_json
+    rng = np.random.default_rng(17)
+    toy = alist.load(os.path.join(GOLD_CODES, "toy_3x6.alist"))
+    assert np.array_equal(toy.coo(), codes.toy_code_3x6().coo())
+    assert np.array_equal(alist.load(os.path.join(GOLD_CODES, "toy_3x6_padded.alist")).coo(), toy.coo())
+    irr = alist.load(os.path.join(GOLD_CODES, "irregular_40x70.alist"))
+    for h, shots, iters in ((toy, 8, 10), (irr, 500, 25)):
+        g = codes.build_tanner_graph(h)
+        syn = (gf2.pack_bits(np.array([[(i >> b) & 1 for b in range(3)] for i in range(8)], dtype=np.uint8))
+               if shots == 8 else random_syndromes(rng, shots, g.num_checks, 0.08))
+        cfg = DecoderConfig(max_iterations=iters, arithmetic=mode)
+        with Decoder(g, cfg) as dec:
+            assert dec.get_option(OPT_INFO_ELL) != 0, "served by the degree-padded kernel"
+            est, res, conv, its = dec.decode_batch_segments(syn)
+        oe, ores, oc, oi = oracle.decode_many(g, cfg, syn)
+        assert np.array_equal(est, oe) and np.array_equal(res, ores)
+        assert np.array_equal(conv, oc) and np.array_equal(its, oi)
+    # CSS codes from descriptors: files next to the JSON, and the bb construction
+    for fname, want in (("bb72_files.json", "bb72"), ("bb144_bb.json", "bb144")):
+        code = css_json.load(os.path.join(GOLD_CODES, fname))
+        ref_code = codes.make_code(want)
+        assert code.n == ref_code.n and code.k == ref_code.k
+        from tests.helpers import error_syndromes
+        _, _, syn = error_syndromes(code, rng, 200, 0.03)
+        cfg = DecoderConfig(max_iterations=20, arithmetic=mode)
+        with Decoder(code, cfg) as dec:
+            est, res, conv, its = dec.decode_batch_segments(syn)
+        oe, ores, oc, oi = oracle.decode_many(code.combined_graph, cfg, syn, code.segments)
+        assert np.array_equal(est, oe) and np.array_equal(res, ores)
+        assert np.array_equal(conv, oc) and np.array_equal(its, oi)
+    # ... and the extended graph of a descriptor-loaded code goes through the (7,3) kernel
+    code = css_json.load(os.path.join(GOLD_CODES, "bb72_files.json"))
+    hext, segs = codes.extended_graph(code)
+    ge = codes.build_tanner_graph(hext)
+    syn = random_syndromes(rng, 300, ge.num_checks, 0.05)
+    cfg = DecoderConfig(max_iterations=15, arithmetic=mode, priors=[3.0] * ge.num_vars)
+    with Decoder(ge, cfg, segments=segs) as dec:
+        assert dec.get_option(OPT_INFO_ELL) == 703
+        est, res, conv, its = dec.decode_batch_segments(syn)
+    oe, ores, oc, oi = oracle.decode_many(ge, cfg, syn, segs)
+    assert np.array_equal(est, oe) and np.array_equal(its, oi)
