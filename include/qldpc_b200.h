@@ -230,6 +230,19 @@ qb_status qb_decode_debug(qb_decoder* h, const uint64_t* syndrome,
                           float* q_f32, float* r_f32, int32_t* q_i32,
                           int32_t* r_i32);
 
+/* The same for the THROUGHPUT kernels: decodes `shots` syndromes (host memory) with the
+ * persistent batch kernel exactly as qb_decode_batch_device would - syndrome tiles, work
+ * queues, the first iteration evaluated from the syndrome on uniform-prior decoders - and
+ * additionally returns the final edge messages of shot `dump_shot`.  On the kernels that
+ * decode two shots per thread (half / int8 pairs) the messages are those at the moment the
+ * PAIR (dump_shot, dump_shot ^ 1) finished: the shot's own final messages when its partner did
+ * not run longer.  QB_INVALID_ARGUMENT when the generic kernel serves batches. */
+qb_status qb_decode_batch_debug(qb_decoder* h, uint64_t shots, const uint64_t* syndromes,
+                                uint64_t dump_shot, uint64_t* estimates,
+                                uint64_t* residuals /* may be NULL */, uint8_t* converged,
+                                uint32_t* iterations, float* q_f32, float* r_f32,
+                                int32_t* q_i32, int32_t* r_i32);
+
 /* Latency harness with the reference's run_bench protocol at batch 1
  * (proj/src/bench.cpp:182-337): decode pool[(b) % pool_size] for b in
  * [0, warmup + measure); for each measured decode record the host wall-clock

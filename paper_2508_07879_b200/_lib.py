@@ -68,6 +68,8 @@ SYMBOLS = {
                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "qb_decode_debug": (C.c_int, [C.c_void_p, u64p, u64p, u64p, u8p, u32p, f32p, f32p, i32p,
                                   i32p]),
+    "qb_decode_batch_debug": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
+                                        C.c_void_p, C.c_void_p, C.c_void_p, f32p, f32p, i32p, i32p]),
     "qb_generate_syndromes": (C.c_int, [C.c_void_p, C.c_uint64, C.c_double, f64p, C.c_int,
                                         C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
                                         C.c_void_p]),

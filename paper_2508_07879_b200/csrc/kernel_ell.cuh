@@ -307,12 +307,29 @@ __device__ __forceinline__ int32_t load_soft<ArithI32>(const ShotIO& io, uint64_
                              : static_cast<int32_t>(static_cast<const int16_t*>(io.soft)[idx]);
 }
 
+// Parity hook of the batch kernels (qb_decode_batch_debug): final messages of one shot in
+// reference edge order (padded slots are not edges and are skipped).
+template <class Store>
+__device__ __noinline__ void ell_dump_messages(const DecodeParams& P, const SegmentDev seg,
+                                               const unsigned char* msgs, uint32_t stride,
+                                               uint32_t slot_bytes, uint32_t roff, uint32_t lane_off,
+                                               Store store) {
+  for (uint32_t m = seg.c0 + threadIdx.x; m < seg.c1; m += blockDim.x) {
+    const uint32_t e0 = P.check_off[m], e1 = P.check_off[m + 1];
+    for (uint32_t e = e0; e < e1; ++e) {
+      const unsigned char* q = msgs + (m - seg.c0) * stride + (e - e0) * slot_bytes + lane_off;
+      store(e, q, q + roff);
+    }
+  }
+}
+
 // ---- the kernel -------------------------------------------------------------------
 // Work item = (shot, segment); a CTA serves one segment for its whole life and
 // draws shots from that segment's ticket queue (as decode_lean_kernel).
 // kSoft: the absorbed variables' priors come per shot from ShotIO::soft.
 
-template <class A, int DC, int DV, int CPT, int VPT, int MAXT, int MINB, bool kSoft = false>
+template <class A, int DC, int DV, int CPT, int VPT, int MAXT, int MINB, bool kSoft = false,
+          bool kDump = false>
 __global__ void __launch_bounds__(MAXT, MINB)
 decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant__ ShotIO io) {
   static_assert(DV <= DC, "padded variable slots live in the q half of the zero block");
@@ -587,6 +604,18 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
     if (tid == 0) {
       io.conv[shot * nseg + s] = still_unsat ? 0 : 1;
       io.iters[shot * nseg + s] = iter;
+    }
+    if constexpr (kDump) if (io.q_dump != nullptr && shot == io.dump_shot) {
+      ell_dump_messages(P, seg, msgs, kStride, kMsg, DC * kMsg, 0u,
+                        [&](uint32_t e, const unsigned char* q, const unsigned char* r) {
+                          if constexpr (A::kInt) {
+                            static_cast<int32_t*>(io.q_dump)[e] = *reinterpret_cast<const Msg*>(q);
+                            static_cast<int32_t*>(io.r_dump)[e] = *reinterpret_cast<const Msg*>(r);
+                          } else {
+                            static_cast<float*>(io.q_dump)[e] = static_cast<float>(*reinterpret_cast<const Msg*>(q));
+                            static_cast<float*>(io.r_dump)[e] = static_cast<float>(*reinterpret_cast<const Msg*>(r));
+                          }
+                        });
     }
     shot = next == kNoShot ? ~0ull : static_cast<uint64_t>(next);
     ipar ^= 1u;

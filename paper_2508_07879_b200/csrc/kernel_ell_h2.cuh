@@ -90,7 +90,8 @@ __device__ __forceinline__ uint32_t vn_ell_h2(unsigned char* base, const uint32_
   return h22u(total) & 0x80008000u;
 }
 
-template <int DC, int DV, int CPT, int VPT, int MAXT, int MINB, bool kI8, bool kSoft = false>
+template <int DC, int DV, int CPT, int VPT, int MAXT, int MINB, bool kI8, bool kSoft = false,
+          bool kDump = false>
 __global__ void __launch_bounds__(MAXT, MINB)
 decode_ell_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_constant__ ShotIO io) {
   static_assert(DV <= DC, "padded variable slots live in the q half of the zero block");
@@ -450,6 +451,20 @@ decode_ell_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_consta
     };
     write_out(shot_a, par_a, fin_a, afin_a, conv_a, iter_a);
     if (has_b) write_out(shot_b, par_b, fin_b, afin_b, conv_b, iter_b);
+    if constexpr (kDump) if (io.q_dump != nullptr && (io.dump_shot >> 1) == pair) {  // parity hook: the messages when the PAIR finished
+      ell_dump_messages(P, seg, msgs, kStride, kMsg, DC * kMsg, (io.dump_shot & 1u) ? 2u : 0u,
+                        [&](uint32_t e, const unsigned char* q, const unsigned char* r) {
+                          const float qv = __half2float(*reinterpret_cast<const __half*>(q));
+                          const float rv = __half2float(*reinterpret_cast<const __half*>(r));
+                          if constexpr (kI8) {
+                            static_cast<int32_t*>(io.q_dump)[e] = static_cast<int32_t>(qv);
+                            static_cast<int32_t*>(io.r_dump)[e] = static_cast<int32_t>(rv);
+                          } else {
+                            static_cast<float*>(io.q_dump)[e] = qv;
+                            static_cast<float*>(io.r_dump)[e] = rv;
+                          }
+                        });
+    }
     pair = next == kNoShot ? ~0ull : static_cast<uint64_t>(next);
     ipar ^= 1u;
   }

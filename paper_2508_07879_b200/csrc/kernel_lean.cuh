@@ -60,6 +60,11 @@ template <> struct Lay<ArithF32> { static constexpr uint32_t kStride = 56, kROff
 template <> struct Lay<ArithF16> { static constexpr uint32_t kStride = 28, kROff = 12; };
 template <> struct Lay<ArithI16> { static constexpr uint32_t kStride = 28, kROff = 12; };
 template <> struct Lay<ArithI8> { static constexpr uint32_t kStride = 24, kROff = 8; };
+// Integer modes with one 32-bit word per message (the fp32 layout): the batch kernel of the
+// int16 mode.  The sub-word layouts above cost a sign extension per value read and a pack per
+// value written, on the ALU pipe that bounds the integer kernels; with whole words a message
+// is an operand as loaded and the saturation bound is a kernel constant (DecodeParams::kmax).
+template <> struct Lay<ArithI32> { static constexpr uint32_t kStride = 56, kROff = 24; };
 
 __host__ __device__ inline uint32_t lean_stride(int arith) {
   return arith == 0 ? 56u : arith == 1 ? 24u : 28u;
@@ -182,6 +187,22 @@ __device__ __forceinline__ void cn6_block(const DecodeParams& P, ArithI16, unsig
   }
 }
 
+__device__ __forceinline__ void cn6_block(const DecodeParams& P, ArithI32, unsigned char* blk,
+                                          uint32_t syn_bit) {
+  const int2* qp = reinterpret_cast<const int2*>(blk);
+  int32_t v[6], o[6];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const int2 p = qp[j];
+    v[2 * j] = p.x;
+    v[2 * j + 1] = p.y;
+  }
+  cn6_finish_int(P, v, o, syn_bit);
+  int2* rp = reinterpret_cast<int2*>(blk + Lay<ArithI32>::kROff);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) rp[j] = make_int2(o[2 * j], o[2 * j + 1]);
+}
+
 __device__ __forceinline__ void cn6_block(const DecodeParams& P, ArithI8, unsigned char* blk,
                                           uint32_t syn_bit) {
   const uint2 w = *reinterpret_cast<const uint2*>(blk);  // 6 message bytes + 2 unused
@@ -267,6 +288,11 @@ __device__ __forceinline__ uint32_t vn3_off(const DecodeParams& P, ArithI16, uns
                                             const uint32_t (&eo)[3], int32_t gamma) {
   return vn3_off_int<kFast, ArithI16>(P, base, eo, gamma);
 }
+template <bool kFast>
+__device__ __forceinline__ uint32_t vn3_off(const DecodeParams& P, ArithI32, unsigned char* base,
+                                            const uint32_t (&eo)[3], int32_t gamma) {
+  return vn3_off_int<kFast, ArithI32>(P, base, eo, gamma);
+}
 
 // ---- first iteration with a uniform prior --------------------------------------
 // Every q equals gamma before the first check stage, so check m sends
@@ -346,6 +372,10 @@ __device__ __forceinline__ uint32_t vn3_first(const DecodeParams& P, ArithI16, u
                                               const uint32_t (&eo)[3], const uint32_t* par) {
   return vn3_first_int<ArithI16>(P, base, eo, par);
 }
+__device__ __forceinline__ uint32_t vn3_first(const DecodeParams& P, ArithI32, unsigned char* base,
+                                              const uint32_t (&eo)[3], const uint32_t* par) {
+  return vn3_first_int<ArithI32>(P, base, eo, par);
+}
 
 // ---- the kernel ---------------------------------------------------------------
 
@@ -380,7 +410,29 @@ __device__ __noinline__ void lean_issue_tile(const uint32_t* syn, uint64_t nshot
   }
 }
 
-template <class A, int CPT, int VPT, bool kFast, int MAXT, int MINB>
+// Parity hook of the batch kernels (qb_decode_batch_debug): the final messages of ONE shot of
+// the batch, written back in reference edge order from the kernel that decodes the whole
+// batch - shortcut of the first iteration, tiles and queues all active.  Compiled into the
+// kDump instantiations only (the same source with this one call added): as a run-time test in
+// the production kernels it cost 2 % (fp32) to 7 % (packed pairs) through register
+// allocation around the call.  `first_only`: the segment
+// stopped after the first iteration of the uniform-prior path, whose check stage is implicit
+// (every r is +-S by the syndrome bit, see vn3_first) and never reached the r slots.
+template <class A, class Store>
+__device__ __noinline__ void lean_dump_messages(const DecodeParams& P, const ShotIO& io,
+                                                const SegmentDev seg, const unsigned char* msgs,
+                                                const uint32_t* syn0, bool first_only, uint32_t slot_bytes,
+                                                uint32_t stride, uint32_t roff, uint32_t lane_off,
+                                                Store store) {
+  for (uint32_t e = threadIdx.x; e < seg.e1 - seg.e0; e += blockDim.x) {
+    const uint32_t m = e / kDC;
+    const unsigned char* src = msgs + m * stride + P.edge_slot[seg.e0 + e] * slot_bytes + lane_off;
+    const uint32_t flip = ((syn0[m >> 5] >> (m & 31u)) & 1u) ^ P.it1_neg;
+    store(seg.e0 + e, src, src + roff, first_only, flip);
+  }
+}
+
+template <class A, int CPT, int VPT, bool kFast, int MAXT, int MINB, bool kDump = false>
 __global__ void __launch_bounds__(MAXT, MINB)
 decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant__ ShotIO io) {
   using Msg = typename A::Msg;
@@ -614,6 +666,26 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
     if (tid == 0) {
       io.conv[shot * nseg + s] = still_unsat ? 0 : 1;
       io.iters[shot * nseg + s] = iter;
+    }
+    if constexpr (kDump) if (io.q_dump != nullptr && shot == io.dump_shot) {
+      lean_dump_messages<A>(
+          P, io, seg, msgs, syn0, kFast && iter == 1u, static_cast<uint32_t>(sizeof(Msg)), kStride,
+          Lay<A>::kROff, 0u,
+          [&](uint32_t e, const unsigned char* q, const unsigned char* r, bool first_only, uint32_t flip) {
+            if constexpr (A::kInt) {
+              static_cast<int32_t*>(io.q_dump)[e] = *reinterpret_cast<const Msg*>(q);
+              static_cast<int32_t*>(io.r_dump)[e] =
+                  first_only ? (flip ? -P.it1_i : P.it1_i) : static_cast<int32_t>(*reinterpret_cast<const Msg*>(r));
+            } else if constexpr (sizeof(Msg) == 2) {
+              const __half s1 = __ushort_as_half(static_cast<unsigned short>(P.it1_h ^ (flip << 15)));
+              static_cast<float*>(io.q_dump)[e] = __half2float(*reinterpret_cast<const __half*>(q));
+              static_cast<float*>(io.r_dump)[e] = __half2float(first_only ? s1 : *reinterpret_cast<const __half*>(r));
+            } else {
+              const float s1 = static_cast<float>(flip ? -P.it1_d : P.it1_d);
+              static_cast<float*>(io.q_dump)[e] = *reinterpret_cast<const float*>(q);
+              static_cast<float*>(io.r_dump)[e] = first_only ? s1 : *reinterpret_cast<const float*>(r);
+            }
+          });
     }
     shot = next == kNoShot ? ~0ull : static_cast<uint64_t>(next);
     ipar ^= 1u;

@@ -178,7 +178,7 @@ __device__ __forceinline__ __half h2_prior(float g) {
   }
 }
 
-template <int CPT, int VPT, bool kFast, int MAXT, int MINB, bool kI8 = false>
+template <int CPT, int VPT, bool kFast, int MAXT, int MINB, bool kI8 = false, bool kDump = false>
 __global__ void __launch_bounds__(MAXT, MINB)
 decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_constant__ ShotIO io) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -469,6 +469,27 @@ decode_lean_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_const
     };
     write_out(shot_a, par_a, fin_a, conv_a, iter_a);
     if (has_b) write_out(shot_b, par_b, fin_b, conv_b, iter_b);
+    if constexpr (kDump) if (io.q_dump != nullptr && (io.dump_shot >> 1) == pair) {
+      // parity hook (see lean_dump_messages).  A lane that stopped earlier than its partner has
+      // had its r slots rewritten by the partner's later check stages (a frozen lane's q no
+      // longer changes, so they were recomputed from the same inputs: still its final r).
+      const bool hi = (io.dump_shot & 1u) != 0;
+      const bool both_first = kFast && iter == 1u;
+      lean_dump_messages<ArithF16>(
+          P, io, seg, msgs, hi ? syn_b : syn_a, both_first, 4u, kH2Stride, kH2ROff, hi ? 2u : 0u,
+          [&](uint32_t e, const unsigned char* q, const unsigned char* r, bool first_only, uint32_t flip) {
+            const __half s1 = __ushort_as_half(static_cast<unsigned short>(P.it1_h ^ (flip << 15)));
+            const float qv = __half2float(*reinterpret_cast<const __half*>(q));
+            const float rv = __half2float(first_only ? s1 : *reinterpret_cast<const __half*>(r));
+            if constexpr (kI8) {
+              static_cast<int32_t*>(io.q_dump)[e] = static_cast<int32_t>(qv);
+              static_cast<int32_t*>(io.r_dump)[e] = static_cast<int32_t>(rv);
+            } else {
+              static_cast<float*>(io.q_dump)[e] = qv;
+              static_cast<float*>(io.r_dump)[e] = rv;
+            }
+          });
+    }
     pair = next == kNoShot ? ~0ull : static_cast<uint64_t>(next);
     ipar ^= 1u;
   }

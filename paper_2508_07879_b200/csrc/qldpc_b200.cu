@@ -101,6 +101,7 @@ constexpr int kSchedSlots = 1 + kPipeSlots + kSchedRing;
 struct LaunchPlan {
   KernelFn kernel = nullptr;
   KernelFn kernel_soft = nullptr;  // same shape, per-shot priors of the absorbed variables
+  KernelFn kernel_dump = nullptr;  // same shape + the message dump of qb_decode_batch_debug
   const char* name = "";
   bool regular = false;
   bool cluster = false;
@@ -391,10 +392,65 @@ KernelFn lean_kernel(int arith, int variant, bool fast) {
       return fast ? lean_kernel_tf<ArithF32, true>(variant) : lean_kernel_tf<ArithF32, false>(variant);
     case QB_ARITH_INT8:
       return fast ? lean_kernel_tf<ArithI8, true>(variant) : lean_kernel_tf<ArithI8, false>(variant);
-    case QB_ARITH_INT16:
-      return fast ? lean_kernel_tf<ArithI16, true>(variant) : lean_kernel_tf<ArithI16, false>(variant);
+    case QB_ARITH_INT16:  // whole-word messages (Lay<ArithI32>): the fp32 layout and shared-memory size
+      return fast ? lean_kernel_tf<ArithI32, true>(variant) : lean_kernel_tf<ArithI32, false>(variant);
     default:
       return fast ? lean_kernel_tf<ArithF16, true>(variant) : lean_kernel_tf<ArithF16, false>(variant);
+  }
+}
+
+// kDump instantiations (qb_decode_batch_debug) exist for the shapes the loader picks by itself
+template <class A, bool kFast>
+KernelFn lean_dump_kernel_tf(int variant) {
+  switch (variant) {
+    case 4: return decode_lean_kernel<A, 3, 5, kFast, 192, 5, true>;
+    case 11: return decode_lean_kernel<A, 3, 5, kFast, 160, 8, true>;
+    default: return nullptr;
+  }
+}
+KernelFn lean_dump_kernel(int arith, int variant, bool fast) {
+  switch (arith) {
+    case QB_ARITH_FLOAT:
+      return fast ? lean_dump_kernel_tf<ArithF32, true>(variant) : lean_dump_kernel_tf<ArithF32, false>(variant);
+    case QB_ARITH_INT16:
+      return fast ? lean_dump_kernel_tf<ArithI32, true>(variant) : lean_dump_kernel_tf<ArithI32, false>(variant);
+    default: return nullptr;
+  }
+}
+KernelFn lean_h2_dump_kernel(bool i8, int variant, bool fast) {
+  if (variant != 8) return nullptr;
+  if (i8) {
+    return fast ? decode_lean_h2_kernel<3, 5, true, 160, 4, true, true>
+                : decode_lean_h2_kernel<3, 5, false, 160, 4, true, true>;
+  }
+  return fast ? decode_lean_h2_kernel<3, 5, true, 160, 4, false, true>
+              : decode_lean_h2_kernel<3, 5, false, 160, 4, false, true>;
+}
+template <class A>
+KernelFn ell_dump_kernel_t(int idx) {
+  switch (idx) {
+    case 0: return decode_ell_kernel<A, 4, 2, 1, 2, 1024, 1, false, true>;
+    case 1: return decode_ell_kernel<A, 7, 3, 3, 5, 192, 5, false, true>;
+    case 2: return decode_ell_kernel<A, 7, 3, 3, 5, 320, 3, false, true>;
+    default: return nullptr;
+  }
+}
+KernelFn ell_dump_kernel(int arith, int idx, bool pair) {
+  if (pair) {
+    const bool i8 = arith == QB_ARITH_INT8;
+    switch (idx) {
+      case 1: return i8 ? decode_ell_h2_kernel<7, 3, 3, 5, 160, 4, true, false, true>
+                        : decode_ell_h2_kernel<7, 3, 3, 5, 160, 4, false, false, true>;
+      case 2: return i8 ? decode_ell_h2_kernel<7, 3, 3, 5, 320, 2, true, false, true>
+                        : decode_ell_h2_kernel<7, 3, 3, 5, 320, 2, false, false, true>;
+      default: return nullptr;
+    }
+  }
+  switch (arith) {
+    case QB_ARITH_FLOAT: return ell_dump_kernel_t<ArithF32>(idx);
+    case QB_ARITH_INT8:
+    case QB_ARITH_INT16: return ell_dump_kernel_t<ArithI32>(idx);
+    default: return ell_dump_kernel_t<ArithF16>(idx);
   }
 }
 
@@ -558,9 +614,11 @@ void finish_plan(qb_decoder* h, LaunchPlan& pl) {
                       : h->smem_bytes;
   CUDA_TRY(cudaFuncSetAttribute(pl.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(pl.smem)));
-  if (pl.kernel_soft) {
-    CUDA_TRY(cudaFuncSetAttribute(pl.kernel_soft, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(pl.smem)));
+  for (KernelFn extra : {pl.kernel_soft, pl.kernel_dump}) {
+    if (extra) {
+      CUDA_TRY(cudaFuncSetAttribute(extra, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(pl.smem)));
+    }
   }
   if (pl.cluster) {
     pl.ctas_per_sm = 1;
@@ -710,6 +768,7 @@ void choose_plans(qb_decoder* h) {
         pl.kernel = !pair                       ? ell_kernel(h->arith, idx)
                     : h->arith == QB_ARITH_INT8 ? ell_h2_kernel_t<true>(idx)
                                                 : ell_h2_kernel_t<false>(idx);
+        pl.kernel_dump = ell_dump_kernel(h->arith, idx, pair);
         pl.kernel_soft = !pair                       ? ell_soft_kernel(h->arith, idx)
                          : h->arith == QB_ARITH_INT8 ? ell_h2_kernel_t<true, true>(idx)
                                                      : ell_h2_kernel_t<false, true>(idx);
@@ -809,6 +868,7 @@ void choose_plans(qb_decoder* h) {
         pl.npt = variant;
         pl.pair = pair;
         pl.kernel = !pl.pair ? lean_kernel(h->arith, variant, fast) : i8 ? i8_pair : h2_pair;
+        pl.kernel_dump = pl.pair ? lean_h2_dump_kernel(i8, variant, fast) : lean_dump_kernel(h->arith, variant, fast);
         pl.name = pl.pair ? "decode_lean_h2_kernel" : "decode_lean_kernel";
         pl.ngroups = 1;
         pl.group_threads = T;
@@ -846,6 +906,13 @@ void launch_plan(qb_decoder* h, const LaunchPlan& pl, const ShotIO& io, unsigned
   if (io.soft) {
     if (!pl.kernel_soft) fail(QB_RUNTIME_ERROR, "launch plan has no per-shot-prior kernel");
     kernel = pl.kernel_soft;
+  }
+  if (io.q_dump && pl.items) {
+    if (!pl.kernel_dump) {
+      fail(QB_INVALID_ARGUMENT, "decode_batch_debug: this batch kernel shape has no message-dump "
+                                "instantiation (the loader's own choices have one)");
+    }
+    kernel = pl.kernel_dump;
   }
   CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, P, io));
   ++h->launches;
@@ -919,13 +986,18 @@ void require_soft(qb_decoder* h, const char* who) {
 
 void run_batch_device(qb_decoder* h, uint64_t shots, const uint32_t* d_syn, uint32_t* d_est,
                       uint32_t* d_res, uint8_t* d_conv, uint32_t* d_iters, cudaStream_t stream,
-                      int sched_slot = -1, const void* d_soft = nullptr) {
+                      int sched_slot = -1, const void* d_soft = nullptr, int64_t dump_shot = -1) {
   if (shots == 0) return;
   if (sched_slot < 0) sched_slot = 1 + kPipeSlots + static_cast<int>(h->sched_next++ % kSchedRing);
   if (shots > 0x7fff0000ull) fail(QB_INVALID_ARGUMENT, "too many shots for one launch");
   ShotIO io{};
   io.soft = d_soft;
   io.soft_bytes = h->soft_bytes;
+  if (dump_shot >= 0) {  // parity hook: messages of one shot of the batch
+    io.q_dump = h->d_qdump;
+    io.r_dump = h->d_rdump;
+    io.dump_shot = static_cast<uint32_t>(dump_shot);
+  }
   io.nshots = shots;
   io.syn = d_syn;
   io.est = d_est;
@@ -1491,7 +1563,10 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
       P.seg_mmax = std::max(P.seg_mmax, P.segs[k].c1 - P.segs[k].c0);
       P.seg_nmax = std::max(P.seg_nmax, P.segs[k].v1 - P.segs[k].v0);
     }
-    h->smem_lean = lean_smem_bytes(P.seg_mmax, arith == QB_ARITH_HALF ? 3 : arith, P.syn_w32);
+    h->smem_lean = lean_smem_bytes(P.seg_mmax, arith == QB_ARITH_HALF    ? 3
+                                               : arith == QB_ARITH_INT16 ? 0  // whole-word messages
+                                                                         : arith,
+                                   P.syn_w32);
     if (h->smem_bytes > static_cast<size_t>(h->max_smem_optin)) {
       fail(QB_INVALID_ARGUMENT, "graph needs " + std::to_string(h->smem_bytes) +
                                     " bytes of shared memory per shot; the device offers " +
@@ -2426,6 +2501,46 @@ qb_status qb_decode_batch(qb_decoder* h, uint64_t shots, const uint64_t* syndrom
   if (!h) return QB_INVALID_ARGUMENT;
   return guarded(h, [&] {
     decode_batch_host(h, shots, syndromes, nullptr, estimates, residuals, converged, iterations);
+  });
+}
+
+qb_status qb_decode_batch_debug(qb_decoder* h, uint64_t shots, const uint64_t* syndromes,
+                                uint64_t dump_shot, uint64_t* estimates, uint64_t* residuals,
+                                uint8_t* converged, uint32_t* iterations, float* q_f32,
+                                float* r_f32, int32_t* q_i32, int32_t* r_i32) {
+  if (!h) return QB_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    if (shots == 0) return;
+    if (!syndromes || !estimates || !converged || !iterations) {
+      fail(QB_INVALID_ARGUMENT, "decode_batch_debug: NULL buffer");
+    }
+    if (dump_shot >= shots) fail(QB_INVALID_ARGUMENT, "decode_batch_debug: dump_shot out of range");
+    if (!h->bat.items) {
+      fail(QB_INVALID_ARGUMENT, "decode_batch_debug: the batch kernel in use has no message dump "
+                                "(generic kernel: use qb_decode_debug)");
+    }
+    const DecodeParams& P = h->P;
+    const bool packed_i8 = h->bat.pair && h->arith == QB_ARITH_INT8;
+    const bool is_int = h->arith == QB_ARITH_INT8 || h->arith == QB_ARITH_INT16;
+    (void)packed_i8;
+    void* qdst = is_int ? static_cast<void*>(q_i32) : static_cast<void*>(q_f32);
+    void* rdst = is_int ? static_cast<void*>(r_i32) : static_cast<void*>(r_f32);
+    if (!qdst || !rdst) fail(QB_INVALID_ARGUMENT, "decode_batch_debug: message buffers of the wrong type");
+    ensure_batch(h, shots, true);
+    cudaStream_t st = h->stream;
+    CUDA_TRY(cudaMemcpyAsync(h->b_syn, syndromes, shots * P.syn_w32 * 4, cudaMemcpyHostToDevice, st));
+    run_batch_device(h, shots, h->b_syn, h->b_est, h->b_res, h->b_conv, h->b_iters, st, -1, nullptr,
+                     static_cast<int64_t>(dump_shot));
+    CUDA_TRY(cudaMemcpyAsync(estimates, h->b_est, shots * P.est_w32 * 4, cudaMemcpyDeviceToHost, st));
+    if (residuals) {
+      CUDA_TRY(cudaMemcpyAsync(residuals, h->b_res, shots * P.syn_w32 * 4, cudaMemcpyDeviceToHost, st));
+    }
+    CUDA_TRY(cudaMemcpyAsync(converged, h->b_conv, shots * P.nseg, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(iterations, h->b_iters, shots * P.nseg * 4, cudaMemcpyDeviceToHost, st));
+    const size_t bytes = static_cast<size_t>(P.E) * 4;
+    CUDA_TRY(cudaMemcpyAsync(qdst, h->d_qdump, bytes, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(rdst, h->d_rdump, bytes, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
   });
 }
 

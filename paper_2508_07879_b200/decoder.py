@@ -238,6 +238,29 @@ class Decoder:
             _raise(st, self._h)
         return est, res, conv, its, q, r
 
+    def decode_batch_debug(self, syndromes: np.ndarray, dump_shot: int):
+        """qb_decode_batch_debug: the batch kernel's outcomes plus the final edge messages
+        (q, r) of shot `dump_shot`, in reference edge order."""
+        syndromes = np.ascontiguousarray(syndromes, dtype=np.uint64)
+        if syndromes.ndim != 2 or syndromes.shape[1] != self._sw:
+            raise ValueError(f"decode_batch: syndromes must be (shots, {self._sw}) uint64 words")
+        shots, e = syndromes.shape[0], self._graph.num_edges
+        est = np.zeros((shots, self._ew), dtype=np.uint64)
+        res = np.zeros((shots, self._sw), dtype=np.uint64)
+        conv = np.zeros((shots, self.num_segments), dtype=np.uint8)
+        its = np.zeros((shots, self.num_segments), dtype=np.uint32)
+        is_int = self._cfg.arithmetic in ("int8", "int16")
+        q = np.zeros(e, dtype=np.int32 if is_int else np.float32)
+        r = np.zeros(e, dtype=np.int32 if is_int else np.float32)
+        args = ((None, None, _ptr(q, _lib.i32p), _ptr(r, _lib.i32p)) if is_int
+                else (_ptr(q, _lib.f32p), _ptr(r, _lib.f32p), None, None))
+        st = self._lib.qb_decode_batch_debug(self._h, shots, syndromes.ctypes.data, int(dump_shot),
+                                             est.ctypes.data, res.ctypes.data, conv.ctypes.data,
+                                             its.ctypes.data, *args)
+        if st != _lib.QB_OK:
+            _raise(st, self._h)
+        return est, res, conv, its, q, r
+
     def decode_batch_segments(self, syndromes: np.ndarray, want_residual: bool = True):
         """qb_decode_batch on (shots, ceil(M/64)) host words: (estimates, residuals | None,
         converged[shots, nseg], iterations[shots, nseg])."""

@@ -569,3 +569,87 @@ def test_memcpy_protocol_graph_and_event_timing(oracle):
         dec.set_option(OPT_LATENCY_EVENTS, 0)
         _, kern, _ = dec.latency_run(syn.view(np.uint64), 5, 50)
         assert np.median(kern) < np.median(ev)
+
+
+# ---- per-edge messages of the THROUGHPUT kernels ----------------------------------------
+
+def _bits(a):
+    return a.view(np.uint32) if a.dtype == np.float32 else a
+
+
+@pytest.mark.parametrize("mode", REF_MODES)
+@pytest.mark.parametrize("p", [0.01, 0.03])
+def test_batch_kernel_messages_match_oracle_bitwise(oracle, mode, p):
+    """north star: "per-edge messages within 1e-5 relative" - checked where the time is
+    spent: the persistent batch kernels (decode_lean_kernel for float / int16,
+    decode_lean_h2_kernel for int8) decoding a whole bb784 batch with syndrome tiles, work
+    queues and the first-iteration-from-the-syndrome shortcut ACTIVE, dump the final q and r
+    of selected shots; they equal the oracle's (reference semantics
+    proj/src/decoder.cpp:245-335) bit for bit, which is stronger than the stated tolerance.
+    Every syndrome appears twice in a row so that, on the two-shots-per-thread kernel, both
+    lanes of a pair stop together."""
+    code = codes.make_code("bb784")
+    g = code.combined_graph
+    rng = np.random.default_rng(31)
+    _, _, syn1 = error_syndromes(code, rng, 96, p)
+    syn = np.repeat(syn1, 2, axis=0)
+    for cfg in (DecoderConfig(max_iterations=50, arithmetic=mode),
+                DecoderConfig(max_iterations=10, early_termination=False, arithmetic=mode)):
+        oe, ores, oc, oi = oracle.decode_many(g, cfg, syn1, code.segments)
+        # shots covering the spread of iteration counts, incl. one-iteration segments (r is
+        # implicit there) and non-converged ones
+        order = np.argsort(oi.max(axis=1), kind="stable")
+        picks = sorted({int(order[0]), int(order[len(order) // 3]), int(order[len(order) // 2]),
+                        int(order[-2]), int(order[-1])})
+        if cfg.early_termination:
+            assert oi.min() == 1, "the sample must contain one-iteration segments"
+        with Decoder(code, cfg) as dec:
+            assert dec.get_option(104) == 1
+            for k in picks:
+                for lane in ((0, 1) if k == picks[0] else (k & 1,)):
+                    est, res, conv, its, q, r = dec.decode_batch_debug(syn, 2 * k + lane)
+                    assert np.array_equal(est[::2], oe) and np.array_equal(est[1::2], oe)
+                    assert np.array_equal(its[::2], oi) and np.array_equal(conv[1::2], oc)
+                    _, _, _, _, oq, orr = oracle.decode(g, cfg, syn1[k], code.segments)
+                    assert np.array_equal(_bits(q), _bits(oq)), ("q", k, oi[k])
+                    assert np.array_equal(_bits(r), _bits(orr)), ("r", k, oi[k])
+
+
+def test_batch_kernel_messages_half_mode_equal_the_single_shot_kernel():
+    """fp16 messages have no oracle; the packed batch kernel's messages must equal the
+    single-shot half kernel's (same arithmetic, lane by lane)."""
+    code = codes.make_code("bb144")
+    rng = np.random.default_rng(32)
+    _, _, syn1 = error_syndromes(code, rng, 40, 0.03)
+    syn = np.repeat(syn1, 2, axis=0)
+    cfg = DecoderConfig(max_iterations=30, arithmetic="half")
+    with Decoder(code, cfg) as dec:
+        for k in (0, 7, 21, 39):
+            est, res, conv, its, q, r = dec.decode_batch_debug(syn, 2 * k + 1)
+            e1, r1, c1, i1, q1, rr1 = dec.decode_debug(syn1[k])
+            assert np.array_equal(est[2 * k], e1) and np.array_equal(its[2 * k + 1], i1)
+            assert np.array_equal(_bits(q), _bits(q1)) and np.array_equal(_bits(r), _bits(rr1))
+
+
+@pytest.mark.parametrize("mode", REF_MODES)
+def test_degree_padded_batch_kernel_messages_match_oracle_bitwise(oracle, mode):
+    """The same for decode_ell_kernel / decode_ell_h2_kernel on the extended graph
+    diag([Hz | I], [Hx | I]) of BASELINE config 5 (absorbed measurement variables included:
+    their q stays the prior, decoder.cpp:324-329)."""
+    code = codes.make_code("bb144")
+    h, segs = codes.extended_graph(code)
+    g = codes.build_tanner_graph(h)
+    rng = np.random.default_rng(33)
+    err = (rng.random((48, g.num_vars)) < 0.02).astype(np.uint8)
+    syn1 = gf2.pack_bits(h.mat_vec(err))
+    syn = np.repeat(syn1, 2, axis=0)
+    cfg = DecoderConfig(max_iterations=30, arithmetic=mode, priors=[3.9] * g.num_vars)
+    oe, ores, oc, oi = oracle.decode_many(g, cfg, syn1, segs)
+    with Decoder(g, cfg, segments=segs) as dec:
+        assert dec.get_option(107) == 703
+        for k in (0, 11, 30, 47):
+            est, res, conv, its, q, r = dec.decode_batch_debug(syn, 2 * k)
+            assert np.array_equal(est[::2], oe) and np.array_equal(its[1::2], oi)
+            _, _, _, _, oq, orr = oracle.decode(g, cfg, syn1[k], segs)
+            assert np.array_equal(_bits(q), _bits(oq)), ("q", k)
+            assert np.array_equal(_bits(r), _bits(orr)), ("r", k)
