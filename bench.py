@@ -564,8 +564,11 @@ def measure_variants(args, code, d_syn, d_est, d_conv, d_its, stream):
                                         early_termination=not args.no_early_stop,
                                         arithmetic=args.arithmetic))
     try:
-        for name, sampler in (("campaign_reference_stream", 0), ("campaign_skip_sampler", 1)):
+        for name, sampler, fused in (("campaign_reference_stream", 0, 1),
+                                     ("campaign_reference_stream_three_kernels", 0, 0),
+                                     ("campaign_skip_sampler", 1, 0)):
             camp.decoder.set_option(_lib.OPT_SAMPLER, sampler)
+            camp.decoder.set_option(17, fused)  # QB_OPT_CAMPAIGN_FUSED
             camp.run_range(args.p, args.seed, 0, trials)  # warm-up (buffers, module load)
             t0 = time.perf_counter()
             reps = 3
@@ -573,6 +576,8 @@ def measure_variants(args, code, d_syn, d_est, d_conv, d_its, stream):
                 c = camp.run_range(args.p, args.seed, r * trials, trials)
             dt = (time.perf_counter() - t0) / reps
             out[name] = {"trials_per_s": trials / dt, "trials_per_call": trials, "p": args.p,
+                         "kernels": ("decode_lean_campaign_kernel + campaign_count_kernel" if fused and sampler == 0
+                                     else "sampler + decode_lean_kernel + classify_kernel"),
                          "timer": "host perf_counter around qb_campaign_run (blocking), mean of 3",
                          "non_converged_last_call": int(c[5])}
     finally:

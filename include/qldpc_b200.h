@@ -154,6 +154,13 @@ typedef enum {
    * same way, for campaigns that need the statistics but not the reference's trials
    * ("device RNG need not reproduce SplitMix64 bit-streams"). */
   QB_OPT_SAMPLER = 16,
+  /* qb_campaign_run / qb_campaign_run_multi on (6,3)-regular CSS codes in float / int16 mode:
+   * 1 (default) = the whole trial loop in ONE kernel (kernel_campaign.cuh: every thread
+   * samples the error bits of its own variables with the reference's SplitMix64 stream, the
+   * syndrome is built in shared memory, the residual is classified from registers; 10 bytes
+   * per trial reach HBM); 0 = sampler, decode and classifier as three kernels per round.
+   * Counters are identical either way (and identical to the reference's run_campaign). */
+  QB_OPT_CAMPAIGN_FUSED = 17,
   /* Read-only (qb_get_option): the launch plans actually in use. */
   QB_OPT_INFO_BATCH_CTAS_PER_SM = 100,
   QB_OPT_INFO_BATCH_BLOCK = 101,

@@ -31,6 +31,7 @@
 #include "kernel_noise.cuh"
 #include "kernel_bw.cuh"
 #include "kernel_classify.cuh"
+#include "kernel_campaign.cuh"
 
 using namespace qb;
 
@@ -160,6 +161,8 @@ struct qb_decoder {
   double quant_scale = 0.0;              // integer modes: the scale priors were quantised with
   std::vector<uint32_t> soft_var;        // [M] variable whose prior soft[m] replaces, or ~0u
   uint32_t* d_aux_mask = nullptr;        // [est_w32] non-data variables (qb_set_auxiliary_vars)
+  uint64_t* d_tcol = nullptr;            // [N] logical-test column per variable (fused campaign kernel)
+  int64_t opt_campaign_fused = 1;        // QB_OPT_CAMPAIGN_FUSED
 
   // options
   int64_t opt_kernel = 0, opt_latency_io = 0, opt_latency_shape = 0, opt_group_threads = 0,
@@ -255,6 +258,7 @@ void destroy(qb_decoder* h) {
   cudaFree(h->d_tests_z);
   cudaFree(h->d_counters);
   cudaFree(h->d_aux_mask);
+  cudaFree(h->d_tcol);
   if (h->h_db) cudaFreeHost(h->h_db);
   if (h->h_rec) cudaFreeHost(h->h_rec);
   cudaFree(h->d_rec_dev);
@@ -1801,6 +1805,10 @@ qb_status set_option_unchecked(qb_decoder* h, int option, int64_t value) {
         if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_SAMPLER: 0 or 1");
         h->opt_sampler = value;
         return;
+      case QB_OPT_CAMPAIGN_FUSED:
+        if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_CAMPAIGN_FUSED: 0 or 1");
+        h->opt_campaign_fused = value;
+        return;
       case QB_OPT_BATCH_CHUNK:
         if (value < 0) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_CHUNK: >= 0");
         h->opt_batch_chunk = value;
@@ -1891,6 +1899,7 @@ int64_t qb_get_option(const qb_decoder* h, int option) {
     case QB_OPT_BATCH_TILE: return h->opt_batch_tile;
     case QB_OPT_BATCH_CHUNK: return h->opt_batch_chunk;
     case QB_OPT_SAMPLER: return h->opt_sampler;
+    case QB_OPT_CAMPAIGN_FUSED: return h->opt_campaign_fused;
     case QB_OPT_SLOT_SPREAD: return h->opt_slot_spread;
     case QB_OPT_INFO_LAST_EVENT_NS: return static_cast<int64_t>(h->last_event_ns);
     case QB_OPT_BATCH_CTAS_PER_SM: return h->opt_batch_ctas;
@@ -2091,6 +2100,23 @@ qb_status qb_set_logicals(qb_decoder* h, const uint64_t* x_tests, uint32_t n_x,
     upload(z_tests, n_z, h->d_tests_z);
     h->n_tests_x = n_x;
     h->n_tests_z = n_z;
+    // transposed form for the fused campaign kernel: bit j of tcol[v] = "test j of v's own
+    // component contains v" (at most 64 tests per component, else that kernel is not used)
+    cudaFree(h->d_tcol);
+    h->d_tcol = nullptr;
+    if (n_x <= 64 && n_z <= 64) {
+      std::vector<uint64_t> tcol(P.N, 0);
+      const uint32_t w64 = P.est_w32 / 2;
+      for (uint32_t v = 0; v < P.N; ++v) {
+        const bool in_x = v >= P.segs[0].v0 && v < P.segs[0].v1;
+        const uint64_t* tests = in_x ? x_tests : z_tests;
+        const uint32_t nt = in_x ? n_x : n_z;
+        for (uint32_t j = 0; j < nt; ++j) {
+          if ((tests[static_cast<size_t>(j) * w64 + (v >> 6)] >> (v & 63u)) & 1ull) tcol[v] |= 1ull << j;
+        }
+      }
+      h->d_tcol = dev_upload(tcol);
+    }
   });
 }
 
@@ -2174,6 +2200,64 @@ void check_soft_channel(double mu, double sigma) {
   }
 }
 
+// The fused campaign kernel (kernel_campaign.cuh) serves plain CSS campaigns on (6,3)-regular
+// codes in the modes whose batch kernel decodes one shot per thread (float, int16): the
+// shapes the loader picks for the decode-only batch kernel.
+using CampKernelFn = void (*)(DecodeParams, CampaignIO);
+template <class A>
+CampKernelFn campaign_kernel_t(bool fast, bool early) {
+  if (early) {
+    return fast ? decode_lean_campaign_kernel<A, 3, 5, true, 192, 5>
+                : decode_lean_campaign_kernel<A, 3, 5, false, 192, 5>;
+  }
+  return fast ? decode_lean_campaign_kernel<A, 3, 5, true, 160, 8>
+              : decode_lean_campaign_kernel<A, 3, 5, false, 160, 8>;
+}
+
+bool campaign_fusable(const qb_decoder* h, const double* probs, bool soft) {
+  const DecodeParams& P = h->P;
+  return h->opt_campaign_fused != 0 && !soft && !probs && !h->d_aux_mask && h->d_tcol != nullptr &&
+         h->opt_sampler == 0 && h->regular63 && h->opt_kernel != 1 && h->opt_batch_shape != 1 &&
+         (h->arith == QB_ARITH_FLOAT || h->arith == QB_ARITH_INT16) && P.nseg == 2 &&
+         P.segs[0].v1 * 2 == P.N && P.segs[0].c1 - P.segs[0].c0 <= 576 &&
+         P.segs[1].c1 - P.segs[1].c0 <= 576 && P.segs[0].v1 <= 960;
+}
+
+void launch_campaign_fused(qb_decoder* h, uint64_t seed, double p, uint64_t first_trial, uint64_t n,
+                           cudaStream_t st) {
+  const DecodeParams& P0 = h->P;
+  const bool fast = h->fast_ok && h->opt_fast != 0;
+  CampKernelFn kern = h->arith == QB_ARITH_FLOAT ? campaign_kernel_t<ArithF32>(fast, P0.early != 0)
+                                                 : campaign_kernel_t<ArithI32>(fast, P0.early != 0);
+  const uint32_t T = regular_group_threads(P0, 3, 5);
+  const size_t smem = campaign_smem_bytes(P0.seg_mmax, 0);
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, static_cast<int>(T), smem));
+  if (per_sm < 1) fail(QB_RUNTIME_ERROR, "campaign kernel does not fit on an SM");
+  const uint64_t resident = static_cast<uint64_t>(per_sm) * h->sm_count;
+  const uint64_t per_seg = std::max<uint64_t>(1, std::min<uint64_t>(resident / P0.nseg, n));
+  DecodeParams P = P0;
+  P.ngroups = 1;
+  P.group_threads = T;
+  CampaignIO io{};
+  io.ntrials = n;
+  io.first_trial = first_trial;
+  io.seed = seed;
+  io.thr = noise_threshold(p);
+  io.tcol = h->d_tcol;
+  io.flags = h->b_conv;
+  io.iters = h->b_iters;
+  io.sched = h->d_sched + (1 + kPipeSlots + static_cast<int>(h->sched_next++ % kSchedRing)) * kSchedWords;
+  kern<<<static_cast<unsigned>(per_seg * P0.nseg), T, smem, st>>>(P, io);
+  CUDA_TRY(cudaGetLastError());
+  ++h->launches;
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(h->sm_count) * 8));
+  campaign_count_kernel<<<grid, 256, 0, st>>>(n, h->b_conv, h->b_iters, h->d_counters);
+  CUDA_TRY(cudaGetLastError());
+  ++h->launches;
+}
+
 // One campaign: sample -> (soft measurement) -> decode -> classify in rounds of `chunk`
 // trials, ENQUEUED on the handle's stream; the ten counters stay in h->d_counters.
 void campaign_enqueue(qb_decoder* h, uint64_t seed, double p, const double* probs, bool soft, double mu,
@@ -2203,6 +2287,14 @@ void campaign_enqueue(qb_decoder* h, uint64_t seed, double p, const double* prob
   if (soft) {
     dprobs = data_only_probs(h, p, probs);
     probs = dprobs.data();
+  }
+  if (campaign_fusable(h, probs, soft)) {
+    // the whole loop inside one kernel per round
+    for (uint64_t done = 0; done < trials; done += chunk) {
+      const uint64_t n = std::min<uint64_t>(chunk, trials - done);
+      launch_campaign_fused(h, seed, p, first_trial + done, n, st);
+    }
+    return;
   }
   for (uint64_t done = 0; done < trials; done += chunk) {
     const uint64_t n = std::min<uint64_t>(chunk, trials - done);

@@ -167,3 +167,32 @@ def test_multi_gpu_entry_point_on_the_gpus_present(ref):
     finally:
         for c in camps:
             c.close()
+
+
+@pytest.mark.parametrize("mode", ["float", "int16"])
+def test_fused_campaign_kernel_equals_the_three_kernel_pipeline(ref, mode):
+    """QB_OPT_CAMPAIGN_FUSED: sample + syndrome + decode + classify in one kernel
+    (kernel_campaign.cuh) against sampler -> decode -> classifier as separate kernels and
+    against the reference's run_campaign: all ten counters identical, at an early-stop and a
+    fixed-iteration configuration, for whole ranges and odd splits."""
+    code = codes.make_code("bb144")
+    rc = ref.code("bb144")
+    for cfg, p, trials in ((DecoderConfig(max_iterations=30, arithmetic=mode), 0.03, 6001),
+                           (DecoderConfig(max_iterations=8, early_termination=False, arithmetic=mode), 0.05, 3000),
+                           (DecoderConfig(max_iterations=1, arithmetic=mode), 0.01, 2000)):
+        camp = Campaign(code, cfg)
+        try:
+            assert camp.decoder.get_option(17) == 1
+            fused = camp.run_range(p, 77, 0, trials)
+            split = camp.run_range(p, 77, 0, 1234) + camp.run_range(p, 77, 1234, trials - 1234)
+            camp.decoder.set_option(15, 257)  # many rounds inside one call
+            rounds = camp.run_range(p, 77, 0, trials)
+            camp.decoder.set_option(15, 0)
+            camp.decoder.set_option(17, 0)
+            plain = camp.run_range(p, 77, 0, trials)
+        finally:
+            camp.close()
+        assert np.array_equal(fused, plain), (fused, plain)
+        assert np.array_equal(fused, split) and np.array_equal(fused, rounds)
+        _same(CampaignResult.from_counters(fused), ref.run_campaign(rc, 0, p, 77, trials, cfg, workers=0))
+    assert fused[6] > 0  # the identity-decoder baseline is exercised too
