@@ -57,6 +57,14 @@ struct DecodeParams {
   double it1_d;     // fp32 mode: (double)float(alpha * |gamma|)
   int32_t it1_i;    // int modes: scale_q16(|gamma|)
   uint32_t it1_neg; // 1 when gamma < 0 (its sign multiplies every first message)
+  // ... as a TABLE (fp32 / whole-word integer batch kernels): with a uniform prior the message
+  // a variable sends after the first iteration depends only on how many of its OTHER two
+  // checks have syndrome bit 1 (it1_tq[0..2], raw message words), and its decision only on
+  // how many of its three checks do (bit 4k of it1_dec4, k = 0..3).  The loader computes the
+  // entries with the reference's own operation sequence for all eight syndrome patterns and
+  // only enables the FAST instantiations of those kernels if every pattern agrees.
+  uint32_t it1_tq[3];
+  uint32_t it1_dec4;
   // CSR tables (device global memory, read-only)
   const uint32_t* check_off;   // [M + 1]
   const uint32_t* var_off;     // [N + 1]

@@ -57,8 +57,9 @@ constexpr uint32_t kCampAccWords = 8;   // {flag bits, res lo, res hi, err lo, e
 
 __host__ __device__ inline size_t campaign_smem_bytes(uint32_t seg_mmax, int arith) {
   const size_t msg = (static_cast<size_t>(seg_mmax + 1) * lean_stride(arith) + 15) & ~size_t(15);
-  // messages | [2] parity bitmaps | [2] syndrome copies | [2] unsat | [2] tickets | [2] accumulators
-  return msg + 4 * (4 * static_cast<size_t>(lean_pw(seg_mmax)) + 4 + 2 * kCampAccWords);
+  // table | messages | [2] parity bitmaps | [2] syndrome copies | [2] rotated copies | [2] unsat |
+  // [2] tickets | [2] accumulators
+  return kLeanTabBytes + msg + 4 * (6 * static_cast<size_t>(lean_pw(seg_mmax)) + 4 + 2 * kCampAccWords);
 }
 
 template <class A, int CPT, int VPT, bool kFast, int MAXT, int MINB>
@@ -78,14 +79,16 @@ decode_lean_campaign_kernel(const __grid_constant__ DecodeParams P, const __grid
   const uint32_t Ms = seg.c1 - seg.c0;
   const uint32_t pw = lean_pw(P.seg_mmax);
 
-  unsigned char* const msgs = smem_raw;
+  static_assert(sizeof(Msg) == 4, "whole-word messages (fp32 / ArithI32): first iteration by table");
+  unsigned char* const msgs = smem_raw + kLeanTabBytes;
   const size_t msg_bytes = (static_cast<size_t>(P.seg_mmax + 1) * kStride + 15) & ~size_t(15);
-  uint32_t* const bits = reinterpret_cast<uint32_t*>(smem_raw + msg_bytes);
+  uint32_t* const bits = reinterpret_cast<uint32_t*>(msgs + msg_bytes);
   uint32_t* const par_buf = bits;              // [2][pw] live parity bitmaps
   uint32_t* const syn_buf = bits + 2 * pw;     // [2][pw] the syndromes themselves, never toggled
-  uint32_t* const unsat_ctr = bits + 4 * pw;   // [2]
-  uint32_t* const ticket = bits + 4 * pw + 2;  // [2]
-  uint32_t* const acc_buf = bits + 4 * pw + 4; // [2][kCampAccWords]
+  uint32_t* const rot_buf = bits + 4 * pw;     // [2][pw] ... every word rotated left by two
+  uint32_t* const unsat_ctr = bits + 6 * pw;   // [2]
+  uint32_t* const ticket = bits + 6 * pw + 2;  // [2]
+  uint32_t* const acc_buf = bits + 6 * pw + 4; // [2][kCampAccWords]
 
   // ---- per-thread tables (as decode_lean_kernel; no slot permutation needed for parity)
   uint32_t eo[VPT][kDV], co[CPT], cl[CPT], valid = 0;
@@ -115,7 +118,8 @@ decode_lean_campaign_kernel(const __grid_constant__ DecodeParams P, const __grid
     }
   }
   for (uint32_t b = tid; b < kStride; b += T) msgs[P.seg_mmax * kStride + b] = 0;  // dummy block
-  for (uint32_t w = tid; w < 4 * pw + 4 + 2 * kCampAccWords; w += T) bits[w] = 0u;
+  for (uint32_t w = tid; w < 6 * pw + 4 + 2 * kCampAccWords; w += T) bits[w] = 0u;
+  if (tid < 3) reinterpret_cast<uint32_t*>(smem_raw)[tid] = P.it1_tq[tid];
 
   uint64_t shot = peer;
   uint32_t ipar = 0;
@@ -127,6 +131,7 @@ decode_lean_campaign_kernel(const __grid_constant__ DecodeParams P, const __grid
   while (shot < io.ntrials) {
     uint32_t* const par = par_buf + ipar * pw;
     uint32_t* const syn0 = syn_buf + ipar * pw;
+    uint32_t* const syn2 = rot_buf + ipar * pw;
     volatile uint32_t* const unsat = unsat_ctr + ipar;
     uint32_t* const acc = acc_buf + ipar * kCampAccWords;
     // ---------------- prologue: sample, syndrome ----------------
@@ -159,6 +164,7 @@ decode_lean_campaign_kernel(const __grid_constant__ DecodeParams P, const __grid
             const uint32_t bit = 1u << (lm & 31u);
             const uint32_t old = atomicXor(&par[lm >> 5], bit);
             atomicXor(&syn0[lm >> 5], bit);
+            if constexpr (kFast) atomicXor(&syn2[lm >> 5], __funnelshift_l(bit, bit, 2));
             delta += (old & bit) ? -1 : 1;
           }
           tc ^= io.tcol[seg.v0 + tid + k * T];
@@ -193,9 +199,11 @@ decode_lean_campaign_kernel(const __grid_constant__ DecodeParams P, const __grid
         __syncwarp();
         uint32_t* const opar = par_buf + (ipar ^ 1u) * pw;
         uint32_t* const osyn = syn_buf + (ipar ^ 1u) * pw;
+        uint32_t* const orot = rot_buf + (ipar ^ 1u) * pw;
         for (uint32_t w = lane; w < pw; w += 32u) {
           opar[w] = 0u;
           osyn[w] = 0u;
+          orot[w] = 0u;
         }
         if (lane == 0) unsat_ctr[ipar ^ 1u] = 0u;
       }
@@ -221,7 +229,7 @@ decode_lean_campaign_kernel(const __grid_constant__ DecodeParams P, const __grid
       uint32_t eb = 0;
       if (kFast && iter == 1u) {
 #pragma unroll
-        for (int k = 0; k < VPT; ++k) eb |= vn3_first(P, A{}, msgs, eo[k], syn0) << k;
+        for (int k = 0; k < VPT; ++k) eb |= vn3_first_tab<kStride>(P, msgs, smem_raw, eo[k], syn2) << k;
       } else {
 #pragma unroll
         for (int k = 0; k < CPT; ++k) cn6_block(P, A{}, msgs + co[k], (synbits >> k) & 1u);

@@ -75,12 +75,13 @@ __host__ __device__ inline uint32_t lean_pw(uint32_t seg_mmax) { return (seg_mma
 // flight per CTA.
 constexpr uint32_t kMaxTile = 16;
 __host__ __device__ inline size_t lean_bits_words(uint32_t seg_mmax) {
-  return (4 * static_cast<size_t>(lean_pw(seg_mmax)) + 8 + 3) & ~size_t(3);  // keeps 16-byte alignment
+  return (6 * static_cast<size_t>(lean_pw(seg_mmax)) + 8 + 3) & ~size_t(3);  // keeps 16-byte alignment
 }
+constexpr uint32_t kLeanTabBytes = 16;  // first-iteration table at shared-memory offset 0
 __host__ __device__ inline size_t lean_smem_bytes(uint32_t seg_mmax, int arith, uint32_t syn_w32) {
   const size_t msg = (static_cast<size_t>(seg_mmax + 1) * lean_stride(arith) + 15) & ~size_t(15);
-  // messages | bitmaps, counters, tickets | 2 syndrome tiles | 2 mbarriers | tile info [2][2]
-  return msg + 4 * lean_bits_words(seg_mmax) + 2 * kMaxTile * syn_w32 * 4 + 16 + 16 + 16;
+  // table | messages | bitmaps, counters, tickets | 2 syndrome tiles | 2 mbarriers | tile info [2][2]
+  return kLeanTabBytes + msg + 4 * lean_bits_words(seg_mmax) + 2 * kMaxTile * syn_w32 * 4 + 16 + 16 + 16;
 }
 
 // ---- check update on one message block ---------------------------------------
@@ -309,6 +310,32 @@ __device__ __forceinline__ uint32_t syn_bit_of_edge(const uint32_t* par, uint32_
   return (par[lm >> 5] >> (lm & 31u)) & 1u;
 }
 
+// First iteration by TABLE (uniform prior; fp32 and whole-word integer messages): the message
+// on edge i is it1_tq[number of the OTHER two checks with syndrome bit 1], the decision bit 4k
+// of it1_dec4 (DecodeParams; verified by the loader against the reference's operation sequence
+// for all eight patterns).  `tab` = the three table words at the start of shared memory,
+// `syn2` = the syndrome bitmap with every word ROTATED LEFT BY TWO, so that
+// rotate_right(word, position) & 4 is the byte offset of a table step: three gathers, one add, and per edge subtract / load / store -
+// no widening, no fp64 sums, no conversions.
+template <uint32_t kStrideT>
+__device__ __forceinline__ uint32_t vn3_first_tab(const DecodeParams& P, unsigned char* base,
+                                                  const unsigned char* tab, const uint32_t (&eo)[3],
+                                                  const uint32_t* syn2) {
+  uint32_t b4[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const uint32_t lm = eo[i] / kStrideT;
+    const uint32_t w = syn2[lm >> 5];
+    b4[i] = __funnelshift_r(w, w, lm) & 4u;  // rotate right by lm mod 32: bit lm of the syndrome at position 2
+  }
+  const uint32_t k4 = b4[0] + b4[1] + b4[2];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    *reinterpret_cast<uint32_t*>(base + eo[i]) = *reinterpret_cast<const uint32_t*>(tab + (k4 - b4[i]));
+  }
+  return (P.it1_dec4 >> k4) & 1u;
+}
+
 __device__ __forceinline__ uint32_t vn3_first(const DecodeParams& P, ArithF32, unsigned char* base,
                                               const uint32_t (&eo)[3], const uint32_t* par) {
   const uint32_t hi0 = static_cast<uint32_t>(__double2hiint(P.it1_d));
@@ -456,12 +483,15 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
   const uint32_t vw0 = seg.v0 >> 5, vspan = ((v1z - 1) >> 5) - vw0 + 1;
   const uint32_t gspan_out = ((c1z - 1) >> 5) - gw0 + 1;
 
-  unsigned char* const msgs = smem_raw;
+  // uniform prior on fp32 / whole-word integer messages: first iteration by table
+  constexpr bool kTab = kFast && (sizeof(Msg) == 4);
+  unsigned char* const msgs = smem_raw + kLeanTabBytes;
   const size_t msg_bytes = (static_cast<size_t>(P.seg_mmax + 1) * kStride + 15) & ~size_t(15);
-  uint32_t* const bits = reinterpret_cast<uint32_t*>(smem_raw + msg_bytes);
+  uint32_t* const bits = reinterpret_cast<uint32_t*>(msgs + msg_bytes);
   uint32_t* const unsat_ctr = bits + 2 * pw;  // [2]
   uint32_t* const ticket = bits + 2 * pw + 2;  // [2]
   uint32_t* const syn_copy = bits + 2 * pw + 8;  // [2][pw] the syndrome itself, never toggled
+  uint32_t* const syn_rot = bits + 4 * pw + 8;   // [2][pw] ... rotated left by two (vn3_first_tab)
   uint32_t* const tilebuf = bits + lean_bits_words(P.seg_mmax);  // [2][kMaxTile][syn_w32]
   uint64_t* const mbar = reinterpret_cast<uint64_t*>(tilebuf + 2 * kMaxTile * P.syn_w32);  // [2]
   uint32_t* const tinfo = reinterpret_cast<uint32_t*>(mbar + 2);  // [2]{first shot, shots}
@@ -498,6 +528,7 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
     }
   }
   for (uint32_t b = tid; b < kStride; b += T) msgs[P.seg_mmax * kStride + b] = 0;  // dummy block
+  if (tid < 3) reinterpret_cast<uint32_t*>(smem_raw)[tid] = P.it1_tq[tid];
 
   auto issue_tile = [&](uint64_t t, uint32_t b) {
     lean_issue_tile(io.syn, io.nshots, P.syn_w32, K, t, tilebuf + b * tile_words, &mbar[b],
@@ -518,6 +549,7 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
   while (shot < io.nshots) {
     uint32_t* const par = bits + ipar * pw;
     uint32_t* const syn0 = syn_copy + ipar * pw;
+    uint32_t* const syn2 = syn_rot + ipar * pw;
     volatile uint32_t* const unsat = unsat_ctr + ipar;
     // ---------------- prologue ----------------
     if (warp == 0) {
@@ -550,6 +582,7 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
       if (lane < pw) {
         par[lane] = loc;
         syn0[lane] = loc;
+        if constexpr (kTab) syn2[lane] = __funnelshift_l(loc, loc, 2);
       }
       const uint32_t cnt = __reduce_add_sync(0xffffffffu, __popc(loc));
       if (lane == 0) {
@@ -597,10 +630,16 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
       ++iter;
       uint32_t eb = 0;
       if (kFast && iter == 1u) {
-#pragma unroll
         // syndrome bits come from the untouched copy, so toggles of the live bitmap by
         // faster threads need no barrier here
-        for (int k = 0; k < VPT; ++k) eb |= vn3_first(P, A{}, msgs, eo[k], syn0) << k;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+          if constexpr (kTab) {
+            eb |= vn3_first_tab<kStride>(P, msgs, smem_raw, eo[k], syn2) << k;
+          } else {
+            eb |= vn3_first(P, A{}, msgs, eo[k], syn0) << k;
+          }
+        }
       } else {
 #pragma unroll
         for (int k = 0; k < CPT; ++k) cn6_block(P, A{}, msgs + co[k], (synbits >> k) & 1u);

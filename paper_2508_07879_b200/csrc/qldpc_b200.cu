@@ -199,6 +199,7 @@ struct qb_decoder {
   std::vector<uint32_t> h_var_edges, h_check_off;  // host copies for the slot optimiser
   bool i8_pair_ok = false;  // int8 mode: the Q16 scaling has an exact fp16 form (kernel_lean_h2.cuh)
   bool fast_ok = false;    // uniform prior (and, for fp32, provably clamp-free)
+  bool tab_ok = false;     // ... and its first iteration is a function of syndrome-bit counts (it1_tq)
   int64_t opt_fast = 1;
   LaunchPlan lat, bat;
   LaunchPlan lat_ell;  // single shots on irregular graphs: degree-padded kernel (kernel == nullptr: none)
@@ -832,7 +833,8 @@ void choose_plans(qb_decoder* h) {
     }
   }
   bool bat_done = false;
-  const bool fast = h->fast_ok && h->opt_fast != 0;
+  const bool word_msgs = h->arith == QB_ARITH_FLOAT || h->arith == QB_ARITH_INT16;
+  const bool fast = h->fast_ok && h->opt_fast != 0 && (!word_msgs || h->tab_ok);
   if (h->opt_batch_shape != 1 && P.seg_mmax <= 960) {
     // work item = (shot, segment): lean item kernel; first variant whose CTA fits
     // (measured on [[784,24,24]]: the packed fp16 kernel prefers the spill-free
@@ -1623,11 +1625,60 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
         const __half ah = __float2half_rn(static_cast<float>(config->alpha));
         P.gamma_hb = __half_as_ushort(gh);
         P.it1_h = __half_as_ushort(__hmul(ah, __habs(gh)));
+        // first iteration as a table (kernel_lean.cuh vn3_first_tab): evaluate the reference's
+        // variable stage (decoder.cpp:313-335: fp64 sum in edge order, one rounding per stored
+        // message) for all eight syndrome patterns of a degree-3 variable and check that the
+        // message on edge i only depends on how many OTHER checks are unsatisfied and the
+        // decision on how many of all three are
+        if (arith == QB_ARITH_FLOAT) {
+          const double gd = static_cast<double>(g0);
+          const double sd = (g0 < 0.0f ? -1.0 : 1.0) * P.it1_d;  // r of a satisfied check
+          uint32_t tq[3] = {0, 0, 0}, dec4 = 0;
+          bool seen_q[3] = {false, false, false}, seen_d[4] = {false, false, false, false}, ok = true;
+          for (int pat = 0; pat < 8 && ok; ++pat) {
+            double r[3], total = gd;
+            for (int i = 0; i < 3; ++i) {
+              r[i] = ((pat >> i) & 1) ? -sd : sd;
+              total += r[i];
+            }
+            const int k = (pat & 1) + ((pat >> 1) & 1) + ((pat >> 2) & 1);
+            const uint32_t d = total < 0.0 ? 1u : 0u;
+            if (seen_d[k] && ((dec4 >> (4 * k)) & 1u) != d) ok = false;
+            seen_d[k] = true;
+            dec4 |= d << (4 * k);
+            for (int i = 0; i < 3; ++i) {
+              float x = static_cast<float>(total - r[i]);
+              x = std::fmin(std::fmax(x, -1e30f), 1e30f);
+              uint32_t bits;
+              std::memcpy(&bits, &x, 4);
+              const int ko = k - ((pat >> i) & 1);
+              if (seen_q[ko] && tq[ko] != bits) ok = false;
+              seen_q[ko] = true;
+              tq[ko] = bits;
+            }
+          }
+          h->tab_ok = ok;
+          for (int j = 0; j < 3; ++j) P.it1_tq[j] = tq[j];
+          P.it1_dec4 = dec4;
+        }
       } else {
         const int32_t g0 = gamma_i[0];
         P.it1_neg = g0 < 0 ? 1u : 0u;
         P.it1_i = static_cast<int32_t>(
             (static_cast<int64_t>(g0 < 0 ? -g0 : g0) * alpha_fx + 32768) >> 16);
+        {
+          // the same table for the integer modes (exact sums: the order cannot matter)
+          const int32_t sgn = g0 < 0 ? -1 : 1;
+          for (int ko = 0; ko < 3; ++ko) {
+            const int32_t v = g0 + sgn * (2 - 2 * ko) * P.it1_i;
+            P.it1_tq[ko] = static_cast<uint32_t>(std::max(-kmax, std::min(kmax, v)));
+          }
+          P.it1_dec4 = 0;
+          for (int k = 0; k < 4; ++k) {
+            if (g0 + sgn * (3 - 2 * k) * P.it1_i < 0) P.it1_dec4 |= 1u << (4 * k);
+          }
+          h->tab_ok = true;
+        }
         if (arith == QB_ARITH_INT8) {
           // int8 on the packed fp16 kernel: find an fp16 constant c with
           // round-to-nearest-even(mag * c) == (mag * alpha_fx + 32768) >> 16 for every
@@ -2226,7 +2277,7 @@ bool campaign_fusable(const qb_decoder* h, const double* probs, bool soft) {
 void launch_campaign_fused(qb_decoder* h, uint64_t seed, double p, uint64_t first_trial, uint64_t n,
                            cudaStream_t st) {
   const DecodeParams& P0 = h->P;
-  const bool fast = h->fast_ok && h->opt_fast != 0;
+  const bool fast = h->fast_ok && h->opt_fast != 0 && h->tab_ok;
   CampKernelFn kern = h->arith == QB_ARITH_FLOAT ? campaign_kernel_t<ArithF32>(fast, P0.early != 0)
                                                  : campaign_kernel_t<ArithI32>(fast, P0.early != 0);
   const uint32_t T = regular_group_threads(P0, 3, 5);
