@@ -197,7 +197,11 @@ __device__ __forceinline__ void cn_ell(const DecodeParams& P, ArithI32, unsigned
 
 // ---- hard decision of an absorbed degree-1 variable: gamma + r < 0 in the mode's arithmetic
 __device__ __forceinline__ uint32_t absorbed_decision(ArithF32, float q, float r) {
-  return (static_cast<double>(q) + static_cast<double>(r)) < 0.0 ? 1u : 0u;  // decoder.cpp:319-323
+  // decoder.cpp:319-323 decides on the sign of the fp64 sum gamma + r, which is EXACT for two
+  // fp32 terms; the fp32 sum is its correctly rounded image and rounding cannot change a sign
+  // (a non-zero sum of two floats is at least 2^-149 in magnitude, so it cannot flush to zero
+  // either): one FADD instead of two widening conversions and a DADD.
+  return (q + r) < 0.0f ? 1u : 0u;
 }
 __device__ __forceinline__ uint32_t absorbed_decision(ArithF16, __half q, __half r) {
   return h_neg(__hadd(q, r)) ? 1u : 0u;
