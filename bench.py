@@ -379,6 +379,13 @@ def run_ours(args):
                 and tr.get("workload") == workload_name(args)):
             roofline["traffic"] = tr["dram_bytes_per_launch"]
             roofline["traffic_source"] = tr.get("source")
+            # the hardware's own view of the same launch, to set beside `frac` (which counts
+            # ALGORITHMIC bytes, incl. the first iteration that the kernel evaluates from a table
+            # without touching r): shared-memory wavefronts as a fraction of their peak rate
+            if tr.get("smem_wavefronts_pct_of_peak") is not None:
+                roofline["ncu_smem_wavefront_frac"] = tr["smem_wavefronts_pct_of_peak"] / 100.0
+                roofline["ncu_pipes_pct"] = {"issue": tr.get("issue_active_pct"), "alu": tr.get("alu_pipe_pct"),
+                                             "xu": tr.get("xu_pipe_pct")}
             roofline["hbm"]["traffic"] = tr["dram_bytes_per_launch"]
             roofline["hbm"]["algorithmic_bytes_per_launch"] = shots * hbm_bytes_per_shot
     except (OSError, ValueError, KeyError):
@@ -682,14 +689,16 @@ def measure_latency(args, code, lib, d_syn):
         cfg = DecoderConfig(max_iterations=10, early_termination=False, arithmetic=arith,
                             priors=[float(np.log((1 - pq) / pq))] * gx.num_vars)
         with Decoder(gx, cfg, segments=segs) as dec:
-            wall, kern, digest = dec.latency_run(pool5, 300, args.latency_shots)
-            wall = np.sort(wall.astype(np.float64) * 1e-3)
-            kern = np.sort(kern.astype(np.float64) * 1e-3)
-            out[f"config5_ext_{arith}_fixed10"] = {
-                "p50": nearest_rank(wall, 50), "p99": nearest_rank(wall, 99),
-                "mean": float(np.mean(wall)), "kernel_p50": nearest_rank(kern, 50),
-                "kernel_p99": nearest_rank(kern, 99), "shots": args.latency_shots,
-                "kernel": "decode_ell_kernel" if dec.get_option(107) else "decode_generic_kernel"}
+            for io_mode, io_name in ((2, "doorbell"), (0, "mapped"), (1, "memcpy")):
+                dec.set_option(1, io_mode)
+                wall, kern, digest = dec.latency_run(pool5, 300, args.latency_shots)
+                wall = np.sort(wall.astype(np.float64) * 1e-3)
+                kern = np.sort(kern.astype(np.float64) * 1e-3)
+                out[f"config5_ext_{arith}_fixed10_{io_name}"] = {
+                    "p50": nearest_rank(wall, 50), "p99": nearest_rank(wall, 99),
+                    "mean": float(np.mean(wall)), "kernel_p50": nearest_rank(kern, 50),
+                    "kernel_p99": nearest_rank(kern, 99), "shots": args.latency_shots,
+                    "kernel": "decode_ell_latency_kernel" if dec.get_option(106) else "decode_generic_kernel"}
     out["note"] = ("wall = host steady_clock around the whole qb_decode (copy-in, launch, "
                    "completion, copy-out) inside qb_latency_run; kernel = in-kernel %globaltimer "
                    "span; doorbell = persistent cluster polling mapped host memory (no launch per "
@@ -720,9 +729,14 @@ def compact_latency(table: dict) -> dict:
                 row[proto].update(cuda_event_p50=r["cuda_event_p50"], cuda_event_p99=r["cuda_event_p99"])
         code[label] = row
     out["bb784_float"] = code
-    for key in ("config5_ext_int8_fixed10", "config5_ext_float_fixed10"):
-        if key in table:
-            out[key] = {"p50": table[key]["p50"], "p99": table[key]["p99"]}
+    for arith in ("int8", "float"):
+        row = {}
+        for proto in ("memcpy", "mapped", "doorbell"):
+            r = table.get(f"config5_ext_{arith}_fixed10_{proto}")
+            if r:
+                row[proto] = {"p50": r["p50"], "p99": r["p99"]}
+        if row:
+            out[f"config5_ext784_{arith}"] = {"fixed10": row}
     return out
 
 

@@ -51,8 +51,9 @@ struct DecodeParams {
   int32_t deg1_i;     // scale_q16(kmax)             (decoder.cpp:253)
   // uniform-prior fast path (every gamma equal; fp32 additionally proven clamp-free)
   double gamma_d;     // (double)float(gamma)
-  float gamma_f;
+  float gamma_f;      // integer modes: float(gamma_i) (ArithI16F kernels)
   int32_t gamma_i;
+  float kmax_f;       // float(kmax)
   // first-iteration constants of the uniform-prior path: every check sends +-S
   double it1_d;     // fp32 mode: (double)float(alpha * |gamma|)
   int32_t it1_i;    // int modes: scale_q16(|gamma|)
@@ -209,6 +210,20 @@ struct ArithI32 {
   using Msg = int32_t;
   using Gam = int32_t;
   static constexpr bool kInt = true;
+};
+
+// The reference's INT16 mode on fp32 INSTRUCTIONS (lean batch kernels): every quantity of that
+// mode is an integer of magnitude <= 4 * 32767 < 2^24, which fp32 represents exactly, so sums
+// (FADD), saturation and the minimum network (FMNMX) and comparisons are exact in fp32
+// arithmetic - and the additions run on the FMA pipe instead of the ALU pipe that bounds the
+// integer kernels.  Messages are stored as fp32 integers.  The Q16 scaling stays an integer
+// multiply: adding 2^23 puts the magnitude into the low mantissa bits, one IMAD evaluates
+// (mag * alpha_fx + 32768) on the bit pattern (the exponent's contribution is folded into the
+// addend, arithmetic mod 2^32), a shift and the same trick backwards return the float.
+struct ArithI16F {
+  using Msg = float;
+  using Gam = float;
+  static constexpr bool kInt = true;  // reference semantics: integer mode (dumps are int32)
 };
 
 // Q16 scaling of a non-negative magnitude (decoder.cpp:226-229).  mag <= 32767

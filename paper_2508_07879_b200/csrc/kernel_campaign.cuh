@@ -94,7 +94,6 @@ decode_lean_campaign_kernel(const __grid_constant__ DecodeParams P, const __grid
   uint32_t eo[VPT][kDV], co[CPT], cl[CPT], valid = 0;
   Gam gam[kFast ? 1 : VPT];
   {
-    const Gam* __restrict__ gamma = static_cast<const Gam*>(P.gamma);
     const uint32_t dummy = P.seg_mmax * kStride;
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
@@ -108,7 +107,7 @@ decode_lean_campaign_kernel(const __grid_constant__ DecodeParams P, const __grid
         eo[k][i] = ok ? (e / kDC) * kStride + P.edge_slot[eg] * static_cast<uint32_t>(sizeof(Msg))
                       : dummy + i * static_cast<uint32_t>(sizeof(Msg));
       }
-      if constexpr (!kFast) gam[k] = ok ? gamma[n] : static_cast<Gam>(1);
+      if constexpr (!kFast) gam[k] = ok ? load_prior<A>(P, n) : static_cast<Gam>(1);
     }
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {

@@ -13,12 +13,12 @@
 //    is 64 (resp. kmax in the integer modes), which makes the ordinary update
 //    emit the reference's special value alpha * sigma * 64 (decoder.cpp:251-258)
 //    without a special case;
-//  * a variable of degree d < DV points its slots d..DV-1 at a ZERO block whose r
-//    half is never written: the padded terms add +0 to the posterior (exact in
-//    every arithmetic mode) and the padded q stores land in a scratch area.  A
-//    degree-1 variable keeps q = gamma (decoder.cpp:324-329): its single store is
-//    predicated off in the floating-point modes, where (gamma + r) - r need not
-//    equal gamma;
+//  * a variable of degree d < DV points its slots d..DV-1 at a DUMMY block behind the real
+//    ones whose r half is never written: the padded terms add +0 to the posterior (exact in
+//    every arithmetic mode) and the padded q stores land in a word only that thread writes
+//    (ell_dummy_blocks).  A degree-1 variable keeps q = gamma (decoder.cpp:324-329): its single
+//    store is predicated off in the floating-point modes, where (gamma + r) - r need not equal
+//    gamma;
 //  * a degree-1 variable whose check has no other one is ABSORBED by that check: its
 //    message q = gamma never changes (it sits in the check's block for the life of the
 //    CTA), and its posterior gamma + r and hard decision are evaluated by the check's
@@ -51,10 +51,23 @@ __host__ __device__ inline uint32_t ell_stride_bytes(uint32_t msg_bytes, uint32_
   return 4u * w;
 }
 __host__ __device__ inline uint32_t ell_pw(uint32_t seg_mmax) { return ((seg_mmax + 2u) >> 5) + 1u; }
-__host__ __device__ inline size_t ell_smem_bytes(uint32_t seg_mmax, uint32_t msg_bytes, uint32_t dc) {
-  const size_t msg =
-      (static_cast<size_t>(seg_mmax + 2) * ell_stride_bytes(msg_bytes, dc) + 15) & ~size_t(15);
-  return msg + 4 * (2 * static_cast<size_t>(ell_pw(seg_mmax)) + 8);
+// Dummy blocks behind the real ones.  A padded variable slot (degree below the bound, or an
+// idle thread) must load r = 0 and store its q somewhere harmless: thread t owns slot t % DC of
+// dummy block t / DC - its q word is written by that thread only, the r half of every dummy
+// block is never written and stays zero.  (One shared scratch block would do for the results,
+// but racecheck rightly reports its q words as write-after-write hazards between threads.)
+__host__ __device__ inline uint32_t ell_dummy_blocks(uint32_t threads, uint32_t dc) {
+  return (threads + dc - 1u) / dc;
+}
+__host__ __device__ inline size_t ell_msg_region_bytes(uint32_t seg_mmax, uint32_t stride,
+                                                       uint32_t threads, uint32_t dc) {
+  // ... plus one block that thread slots WITHOUT a check run their (branch-free) update on
+  return (static_cast<size_t>(seg_mmax + ell_dummy_blocks(threads, dc) + 1u) * stride + 15) & ~size_t(15);
+}
+__host__ __device__ inline size_t ell_smem_bytes(uint32_t seg_mmax, uint32_t msg_bytes, uint32_t dc,
+                                                 uint32_t threads) {
+  return ell_msg_region_bytes(seg_mmax, ell_stride_bytes(msg_bytes, dc), threads, dc) +
+         4 * (2 * static_cast<size_t>(ell_pw(seg_mmax)) + 8);
 }
 
 // min1 / min2 of N keys, branch-free (3 operations per key after the first two).
@@ -362,16 +375,17 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
   const uint32_t gspan_out = c1z > seg.c0 ? ((c1z - 1) >> 5) - gw0 + 1 : 0u;
 
   unsigned char* const msgs = smem_raw;
-  const size_t msg_bytes = (static_cast<size_t>(P.seg_mmax + 2) * kStride + 15) & ~size_t(15);
+  const size_t msg_bytes = ell_msg_region_bytes(P.seg_mmax, kStride, T, DC);
   uint32_t* const bits = reinterpret_cast<uint32_t*>(smem_raw + msg_bytes);
   uint32_t* const unsat_ctr = bits + 2 * pw;   // [2]
   uint32_t* const ticket = bits + 2 * pw + 2;  // [2]
-  const uint32_t scratch_off = P.seg_mmax * kStride;     // block of the padding threads
-  const uint32_t zero_off = (P.seg_mmax + 1) * kStride;  // r half stays zero for ever
+  const uint32_t scratch_off = P.seg_mmax * kStride;  // first dummy block (see ell_dummy_blocks)
+  const uint32_t pad_off = scratch_off + (tid / DC) * kStride + (tid % DC) * kMsg;  // this thread's slot
+  const uint32_t scribble_off = scratch_off + ell_dummy_blocks(T, DC) * kStride;  // thread slots without a check
 
-  // both dummy blocks start out as zeros (before any sentinel / q store)
+  // the dummy blocks start out as zeros (before any q store)
   const uint64_t t_entry = io.kernel_ns ? globaltimer_ns() : 0ull;  // single-shot use only
-  for (uint32_t b = tid; b < 2 * kStride; b += T) msgs[scratch_off + b] = 0;
+  for (uint32_t b = tid; b < (ell_dummy_blocks(T, DC) + 1u) * kStride; b += T) msgs[scratch_off + b] = 0;
 
   // ---- per-thread tables
   uint32_t eo[VPT][DV], co[CPT], cl[CPT], valid = 0, keep0 = 0;
@@ -392,7 +406,7 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
       keep0 |= (deg == 1u ? 1u : 0u) << k;
 #pragma unroll
       for (int i = 0; i < DV; ++i) {
-        uint32_t off = (ok ? zero_off : scratch_off) + i * kMsg;
+        uint32_t off = pad_off;
         if (static_cast<uint32_t>(i) < deg) {
           const uint32_t e = P.var_edges[b + i];
           const uint32_t m = P.edge_check[e];
@@ -406,8 +420,8 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
     for (int k = 0; k < CPT; ++k) {
       const uint32_t m = tid + k * T;
       const bool ok = m < Ms;
-      cl[k] = ok ? m : Ms;  // dummy check: bit Ms of the bitmap, always 0
-      co[k] = (ok ? m : P.seg_mmax) * kStride;
+      cl[k] = ok ? m : Ms;  // no check: bit Ms of the bitmap (always 0) and the scribble block
+      co[k] = ok ? m * kStride : scribble_off;
       uint32_t aslot = kNoAbsorb;
       if (ok) {  // sentinels of the padded slots: written once, never overwritten
         const uint32_t e0 = P.check_off[seg.c0 + m];

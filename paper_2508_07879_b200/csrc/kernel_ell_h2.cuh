@@ -23,9 +23,9 @@
 
 namespace qb {
 
-__host__ __device__ inline size_t ell_h2_smem_bytes(uint32_t seg_mmax, uint32_t dc) {
-  const size_t msg = (static_cast<size_t>(seg_mmax + 2) * ell_stride_bytes(4u, dc) + 15) & ~size_t(15);
-  return msg + 4 * (8 * static_cast<size_t>(ell_pw(seg_mmax)) + 16);
+__host__ __device__ inline size_t ell_h2_smem_bytes(uint32_t seg_mmax, uint32_t dc, uint32_t threads) {
+  return ell_msg_region_bytes(seg_mmax, ell_stride_bytes(4u, dc), threads, dc) +
+         4 * (8 * static_cast<size_t>(ell_pw(seg_mmax)) + 16);
 }
 
 // check update over one padded block of half2 slots: per-edge minimum of the OTHER
@@ -119,16 +119,17 @@ decode_ell_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_consta
   const uint64_t npairs = (io.nshots + 1) / 2;
 
   unsigned char* const msgs = smem_raw;
-  const size_t msg_bytes = (static_cast<size_t>(P.seg_mmax + 2) * kStride + 15) & ~size_t(15);
+  const size_t msg_bytes = ell_msg_region_bytes(P.seg_mmax, kStride, T, DC);
   uint32_t* const bits = reinterpret_cast<uint32_t*>(smem_raw + msg_bytes);
   // [item parity][shot lane][pw] live bitmaps, counters, tickets, untouched syndrome copies
   uint32_t* const unsat_ctr = bits + 4 * pw;       // [2][2]
   uint32_t* const ticket = bits + 4 * pw + 4;      // [2]
   uint32_t* const syn_copy = bits + 4 * pw + 16;   // [2][2][pw]
-  const uint32_t scratch_off = P.seg_mmax * kStride;     // block of the padding threads
-  const uint32_t zero_off = (P.seg_mmax + 1) * kStride;  // r half stays zero for ever
+  const uint32_t scratch_off = P.seg_mmax * kStride;  // first dummy block (see ell_dummy_blocks)
+  const uint32_t pad_off = scratch_off + (tid / DC) * kStride + (tid % DC) * kMsg;  // this thread's slot
+  const uint32_t scribble_off = scratch_off + ell_dummy_blocks(T, DC) * kStride;  // thread slots without a check
 
-  for (uint32_t b = tid; b < 2 * kStride; b += T) msgs[scratch_off + b] = 0;
+  for (uint32_t b = tid; b < (ell_dummy_blocks(T, DC) + 1u) * kStride; b += T) msgs[scratch_off + b] = 0;
 
   // ---- per-thread tables (as decode_ell_kernel)
   uint32_t eo[VPT][DV], co[CPT], cl[CPT], valid = 0, keep0 = 0, absorb = 0;
@@ -153,7 +154,7 @@ decode_ell_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_consta
       keep0 |= (deg == 1u ? 1u : 0u) << k;
 #pragma unroll
       for (int i = 0; i < DV; ++i) {
-        uint32_t off = (ok ? zero_off : scratch_off) + i * kMsg;
+        uint32_t off = pad_off;
         if (static_cast<uint32_t>(i) < deg) {
           const uint32_t e = P.var_edges[b + i];
           const uint32_t m = P.edge_check[e];
@@ -169,8 +170,8 @@ decode_ell_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_consta
     for (int k = 0; k < CPT; ++k) {
       const uint32_t m = tid + k * T;
       const bool ok = m < Ms;
-      cl[k] = ok ? m : Ms;
-      co[k] = (ok ? m : P.seg_mmax) * kStride;
+      cl[k] = ok ? m : Ms;  // no check: the scribble block
+      co[k] = ok ? m * kStride : scribble_off;
       uint32_t aslot = kNoAbsorb;
       if (ok) {
         const uint32_t e0 = P.check_off[seg.c0 + m];

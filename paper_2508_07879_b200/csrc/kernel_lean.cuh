@@ -65,6 +65,17 @@ template <> struct Lay<ArithI8> { static constexpr uint32_t kStride = 24, kROff 
 // value written, on the ALU pipe that bounds the integer kernels; with whole words a message
 // is an operand as loaded and the saturation bound is a kernel constant (DecodeParams::kmax).
 template <> struct Lay<ArithI32> { static constexpr uint32_t kStride = 56, kROff = 24; };
+template <> struct Lay<ArithI16F> { static constexpr uint32_t kStride = 56, kROff = 24; };
+
+// prior of variable n in the kernel's own representation
+template <class A>
+__device__ __forceinline__ typename A::Gam load_prior(const DecodeParams& P, uint32_t n) {
+  return static_cast<const typename A::Gam*>(P.gamma)[n];
+}
+template <>
+__device__ __forceinline__ float load_prior<ArithI16F>(const DecodeParams& P, uint32_t n) {
+  return static_cast<float>(static_cast<const int32_t*>(P.gamma)[n]);  // |gamma| <= 32767: exact
+}
 
 __host__ __device__ inline uint32_t lean_stride(int arith) {
   return arith == 0 ? 56u : arith == 1 ? 24u : 28u;
@@ -204,6 +215,46 @@ __device__ __forceinline__ void cn6_block(const DecodeParams& P, ArithI32, unsig
   for (int j = 0; j < 3; ++j) rp[j] = make_int2(o[2 * j], o[2 * j + 1]);
 }
 
+// scale_q16 of a non-negative integer-valued float below 2^15 (see ArithI16F)
+__device__ __forceinline__ float scale_q16_f(float mag, uint32_t alpha_fx, uint32_t addend) {
+  const uint32_t b = __float_as_uint(mag + 8388608.0f);  // 0x4B000000 + mag
+  const uint32_t u = b * alpha_fx + addend;              // mag * alpha_fx + 32768  (mod 2^32: exact)
+  return __uint_as_float((u >> 16) | 0x4B000000u) - 8388608.0f;
+}
+
+__device__ __forceinline__ void cn6_block(const DecodeParams& P, ArithI16F, unsigned char* blk,
+                                          uint32_t syn_bit) {
+  const float2* qp = reinterpret_cast<const float2*>(blk);
+  float v[6];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const float2 p = qp[j];
+    v[2 * j] = p.x;
+    v[2 * j + 1] = p.y;
+  }
+  const float l0 = fminf(fabsf(v[0]), fabsf(v[1])), h0 = fmaxf(fabsf(v[0]), fabsf(v[1]));
+  const float l1 = fminf(fabsf(v[2]), fabsf(v[3])), h1 = fmaxf(fabsf(v[2]), fabsf(v[3]));
+  const float l2 = fminf(fabsf(v[4]), fabsf(v[5])), h2 = fmaxf(fabsf(v[4]), fabsf(v[5]));
+  const float m1 = fminf(fminf(l0, l1), l2);
+  const float med = fmaxf(fminf(l0, l1), fminf(fmaxf(l0, l1), l2));
+  const float m2 = fminf(med, fminf(fminf(h0, h1), h2));
+  uint32_t sx = syn_bit << 31;
+#pragma unroll
+  for (int j = 0; j < 6; ++j) sx ^= __float_as_uint(v[j]);
+  sx &= 0x80000000u;
+  const uint32_t addend = 32768u - 0x4B000000u * P.alpha_fx;
+  const uint32_t s1 = __float_as_uint(scale_q16_f(m1, P.alpha_fx, addend)) ^ sx;
+  const uint32_t s2 = __float_as_uint(scale_q16_f(m2, P.alpha_fx, addend)) ^ sx;
+  float2* rp = reinterpret_cast<float2*>(blk + Lay<ArithI16F>::kROff);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const uint32_t ox = (fabsf(v[2 * j]) == m1 ? s2 : s1) ^ (__float_as_uint(v[2 * j]) & 0x80000000u);
+    const uint32_t oy =
+        (fabsf(v[2 * j + 1]) == m1 ? s2 : s1) ^ (__float_as_uint(v[2 * j + 1]) & 0x80000000u);
+    rp[j] = make_float2(__uint_as_float(ox), __uint_as_float(oy));
+  }
+}
+
 __device__ __forceinline__ void cn6_block(const DecodeParams& P, ArithI8, unsigned char* blk,
                                           uint32_t syn_bit) {
   const uint2 w = *reinterpret_cast<const uint2*>(blk);  // 6 message bytes + 2 unused
@@ -293,6 +344,20 @@ template <bool kFast>
 __device__ __forceinline__ uint32_t vn3_off(const DecodeParams& P, ArithI32, unsigned char* base,
                                             const uint32_t (&eo)[3], int32_t gamma) {
   return vn3_off_int<kFast, ArithI32>(P, base, eo, gamma);
+}
+// int16 semantics on fp32 instructions: exact integer sums, saturation at +-kmax
+template <bool kFast>
+__device__ __forceinline__ uint32_t vn3_off(const DecodeParams& P, ArithI16F, unsigned char* base,
+                                            const uint32_t (&eo)[3], float gamma) {
+  constexpr uint32_t R = Lay<ArithI16F>::kROff;
+  const float r0 = *reinterpret_cast<const float*>(base + eo[0] + R);
+  const float r1 = *reinterpret_cast<const float*>(base + eo[1] + R);
+  const float r2 = *reinterpret_cast<const float*>(base + eo[2] + R);
+  const float total = (kFast ? P.gamma_f : gamma) + r0 + r1 + r2;
+  *reinterpret_cast<float*>(base + eo[0]) = fmaxf(-P.kmax_f, fminf(P.kmax_f, total - r0));
+  *reinterpret_cast<float*>(base + eo[1]) = fmaxf(-P.kmax_f, fminf(P.kmax_f, total - r1));
+  *reinterpret_cast<float*>(base + eo[2]) = fmaxf(-P.kmax_f, fminf(P.kmax_f, total - r2));
+  return total < 0.0f ? 1u : 0u;
 }
 
 // ---- first iteration with a uniform prior --------------------------------------
@@ -403,6 +468,21 @@ __device__ __forceinline__ uint32_t vn3_first(const DecodeParams& P, ArithI32, u
                                               const uint32_t (&eo)[3], const uint32_t* par) {
   return vn3_first_int<ArithI32>(P, base, eo, par);
 }
+__device__ __forceinline__ uint32_t vn3_first(const DecodeParams& P, ArithI16F, unsigned char* base,
+                                              const uint32_t (&eo)[3], const uint32_t* par) {
+  float r[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const uint32_t flip = syn_bit_of_edge(par, eo[i], Lay<ArithI16F>::kStride) ^ P.it1_neg;
+    r[i] = static_cast<float>(flip ? -P.it1_i : P.it1_i);
+  }
+  const float total = P.gamma_f + r[0] + r[1] + r[2];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    *reinterpret_cast<float*>(base + eo[i]) = fmaxf(-P.kmax_f, fminf(P.kmax_f, total - r[i]));
+  }
+  return total < 0.0f ? 1u : 0u;
+}
 
 // ---- the kernel ---------------------------------------------------------------
 
@@ -504,7 +584,6 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
   uint32_t eo[VPT][kDV], co[CPT], cl[CPT], valid = 0;
   Gam gam[kFast ? 1 : VPT];
   {
-    const Gam* __restrict__ gamma = static_cast<const Gam*>(P.gamma);
     const uint32_t dummy = P.seg_mmax * kStride;
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
@@ -518,7 +597,7 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
         eo[k][i] = ok ? (e / kDC) * kStride + P.edge_slot[eg] * static_cast<uint32_t>(sizeof(Msg))
                       : dummy + i * static_cast<uint32_t>(sizeof(Msg));
       }
-      if constexpr (!kFast) gam[k] = ok ? gamma[n] : static_cast<Gam>(1);
+      if constexpr (!kFast) gam[k] = ok ? load_prior<A>(P, n) : static_cast<Gam>(1);
     }
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
@@ -711,8 +790,8 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
           P, io, seg, msgs, syn0, kFast && iter == 1u, static_cast<uint32_t>(sizeof(Msg)), kStride,
           Lay<A>::kROff, 0u,
           [&](uint32_t e, const unsigned char* q, const unsigned char* r, bool first_only, uint32_t flip) {
-            if constexpr (A::kInt) {
-              static_cast<int32_t*>(io.q_dump)[e] = *reinterpret_cast<const Msg*>(q);
+            if constexpr (A::kInt) {  // (ArithI16F: integer-valued floats, converted exactly)
+              static_cast<int32_t*>(io.q_dump)[e] = static_cast<int32_t>(*reinterpret_cast<const Msg*>(q));
               static_cast<int32_t*>(io.r_dump)[e] =
                   first_only ? (flip ? -P.it1_i : P.it1_i) : static_cast<int32_t>(*reinterpret_cast<const Msg*>(r));
             } else if constexpr (sizeof(Msg) == 2) {
@@ -1051,6 +1130,11 @@ decode_lean_latency_kernel(const __grid_constant__ DecodeParams P,
     t_idle0 = globaltimer_ns();
     last = cmd;
     if (ctl.mode != 2u) break;
+    // The next prologue overwrites the bitmap this record was read from.  The host only rings
+    // the next doorbell after it has seen the whole record, i.e. after every read above - an
+    // ordering no tool can see; the barrier states it (the record is already out: the host's
+    // latency does not include it).
+    __syncthreads();
   }
   if (ctl.mode == 2u) {
     if (s == 0 && tid == 0 && ctl.alive) {

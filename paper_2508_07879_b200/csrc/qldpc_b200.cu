@@ -28,6 +28,7 @@
 #include "kernel_lean_h2.cuh"
 #include "kernel_ell.cuh"
 #include "kernel_ell_h2.cuh"
+#include "kernel_ell_latency.cuh"
 #include "kernel_noise.cuh"
 #include "kernel_bw.cuh"
 #include "kernel_classify.cuh"
@@ -191,7 +192,6 @@ struct qb_decoder {
   int64_t opt_slot_spread = 1;  // lean batch kernels: bank-spreading slot permutation
   int64_t opt_latency_graph = 1;
   cudaGraphExec_t lat_graph[2] = {nullptr, nullptr};
-  cudaGraphExec_t ell_graph = nullptr;  // degree-padded single shot: H2D, kernel, D2H
   uint32_t lat_graph_flip = 0;
   bool regular63 = false;  // every check degree 6, every variable degree 3
   uint32_t max_dc = 0, max_dv = 0;  // largest check / variable degree of the graph
@@ -202,7 +202,6 @@ struct qb_decoder {
   bool tab_ok = false;     // ... and its first iteration is a function of syndrome-bit counts (it1_tq)
   int64_t opt_fast = 1;
   LaunchPlan lat, bat;
-  LaunchPlan lat_ell;  // single shots on irregular graphs: degree-padded kernel (kernel == nullptr: none)
 
   uint64_t launches = 0;
   std::string err;
@@ -217,8 +216,6 @@ void drop_latency_graphs(qb_decoder* h) {
     if (g) cudaGraphExecDestroy(g);
     g = nullptr;
   }
-  if (h->ell_graph) cudaGraphExecDestroy(h->ell_graph);
-  h->ell_graph = nullptr;
 }
 
 void free_batch(qb_decoder* h) {
@@ -397,8 +394,8 @@ KernelFn lean_kernel(int arith, int variant, bool fast) {
       return fast ? lean_kernel_tf<ArithF32, true>(variant) : lean_kernel_tf<ArithF32, false>(variant);
     case QB_ARITH_INT8:
       return fast ? lean_kernel_tf<ArithI8, true>(variant) : lean_kernel_tf<ArithI8, false>(variant);
-    case QB_ARITH_INT16:  // whole-word messages (Lay<ArithI32>): the fp32 layout and shared-memory size
-      return fast ? lean_kernel_tf<ArithI32, true>(variant) : lean_kernel_tf<ArithI32, false>(variant);
+    case QB_ARITH_INT16:  // integers in fp32 words (ArithI16F): the fp32 layout and shared-memory size
+      return fast ? lean_kernel_tf<ArithI16F, true>(variant) : lean_kernel_tf<ArithI16F, false>(variant);
     default:
       return fast ? lean_kernel_tf<ArithF16, true>(variant) : lean_kernel_tf<ArithF16, false>(variant);
   }
@@ -418,7 +415,7 @@ KernelFn lean_dump_kernel(int arith, int variant, bool fast) {
     case QB_ARITH_FLOAT:
       return fast ? lean_dump_kernel_tf<ArithF32, true>(variant) : lean_dump_kernel_tf<ArithF32, false>(variant);
     case QB_ARITH_INT16:
-      return fast ? lean_dump_kernel_tf<ArithI32, true>(variant) : lean_dump_kernel_tf<ArithI32, false>(variant);
+      return fast ? lean_dump_kernel_tf<ArithI16F, true>(variant) : lean_dump_kernel_tf<ArithI16F, false>(variant);
     default: return nullptr;
   }
 }
@@ -533,22 +530,22 @@ KernelFn ell_kernel_t(int idx) {
   }
 }
 
-// Single shots on irregular graphs: the same kernel with one check and two variables per
-// thread (more threads per segment, shorter phases); one CTA per segment, one shot.
+// Single shots on irregular graphs: decode_ell_latency_kernel (kernel_ell_latency.cuh), one
+// check and two variables per thread, a cluster with one CTA per segment.
 constexpr EllVariant kEllLatVariants[] = {
     {4, 2, 1, 2, 1024},
-    {7, 3, 1, 2, 448},
+    {7, 3, 1, 2, 1024},
     {8, 4, 1, 2, 1024},
     {12, 6, 1, 2, 1024},
 };
 constexpr int kNumEllLatVariants = sizeof(kEllLatVariants) / sizeof(kEllLatVariants[0]);
 template <class A>
-KernelFn ell_lat_kernel_t(int idx) {
+LatKernelFn ell_lat_kernel_t(int idx) {
   switch (idx) {
-    case 0: return decode_ell_kernel<A, 4, 2, 1, 2, 1024, 1>;
-    case 1: return decode_ell_kernel<A, 7, 3, 1, 2, 448, 1>;
-    case 2: return decode_ell_kernel<A, 8, 4, 1, 2, 1024, 1>;
-    default: return decode_ell_kernel<A, 12, 6, 1, 2, 1024, 1>;
+    case 0: return decode_ell_latency_kernel<A, 4, 2>;
+    case 1: return decode_ell_latency_kernel<A, 7, 3>;
+    case 2: return decode_ell_latency_kernel<A, 8, 4>;
+    default: return decode_ell_latency_kernel<A, 12, 6>;
   }
 }
 
@@ -570,7 +567,7 @@ KernelFn ell_soft_kernel(int arith, int idx) {
     default: return ell_kernel_t<ArithF16, true>(idx);
   }
 }
-KernelFn ell_lat_kernel(int arith, int idx) {
+LatKernelFn ell_lat_kernel(int arith, int idx) {
   switch (arith) {
     case QB_ARITH_FLOAT: return ell_lat_kernel_t<ArithF32>(idx);
     case QB_ARITH_INT8:
@@ -611,9 +608,9 @@ uint32_t regular_group_threads(const DecodeParams& P, uint32_t cpt, uint32_t vpt
 void finish_plan(qb_decoder* h, LaunchPlan& pl) {
   pl.block = pl.cluster ? pl.group_threads : pl.ngroups * pl.group_threads;
   if (pl.items) pl.block = pl.group_threads;
-  pl.smem = pl.ell && pl.pair ? ell_h2_smem_bytes(h->P.seg_mmax, static_cast<uint32_t>(pl.ell / 100))
+  pl.smem = pl.ell && pl.pair ? ell_h2_smem_bytes(h->P.seg_mmax, static_cast<uint32_t>(pl.ell / 100), pl.block)
             : pl.ell  ? ell_smem_bytes(h->P.seg_mmax, ell_msg_bytes(h->arith),
-                                       static_cast<uint32_t>(pl.ell / 100))
+                                       static_cast<uint32_t>(pl.ell / 100), pl.block)
             : pl.pair ? lean_h2_smem_bytes(h->P.seg_mmax, h->P.syn_w32)
             : pl.lean ? h->smem_lean
                       : h->smem_bytes;
@@ -743,7 +740,6 @@ void choose_plans(qb_decoder* h) {
   if (h->opt_kernel == 2 && !h->regular63) {
     fail(QB_INVALID_ARGUMENT, "the (6,3)-regular kernels need a (6,3)-regular graph with at most 8 segments");
   }
-  h->lat_ell = LaunchPlan{};
   if (!use_regular) {
     h->lat = h->bat = generic_plan(h);
     // batch: degree-padded item kernel when the degrees fit an instantiated bound
@@ -761,9 +757,9 @@ void choose_plans(qb_decoder* h) {
         const bool pair = (h->arith == QB_ARITH_HALF || (h->arith == QB_ARITH_INT8 && h->i8_pair_ok)) &&
                           h->opt_batch_pair != 0 && T <= static_cast<uint32_t>(kEllH2MaxT[idx]);
         if (T > static_cast<uint32_t>(ev.maxt)) continue;
-        const size_t smem = pair ? ell_h2_smem_bytes(P.seg_mmax, static_cast<uint32_t>(ev.dc))
+        const size_t smem = pair ? ell_h2_smem_bytes(P.seg_mmax, static_cast<uint32_t>(ev.dc), T)
                                  : ell_smem_bytes(P.seg_mmax, ell_msg_bytes(h->arith),
-                                                  static_cast<uint32_t>(ev.dc));
+                                                  static_cast<uint32_t>(ev.dc), T);
         if (smem > static_cast<size_t>(h->max_smem_optin)) continue;
         LaunchPlan pl{};
         pl.items = true;
@@ -784,27 +780,28 @@ void choose_plans(qb_decoder* h) {
         h->bat = pl;
         break;
       }
-      for (int idx = 0; idx < kNumEllLatVariants; ++idx) {  // single shots: one check per thread
+    }
+    // single shots: the degree-padded cluster kernel (mapped / doorbell / memcpy protocols)
+    h->lat_lean_kernel = nullptr;
+    if (h->opt_kernel != 1 && h->opt_latency_shape != 1 && P.syn_w32 <= kInlineSynWords &&
+        P.nseg <= kMaxSegments) {
+      for (int idx = 0; idx < kNumEllLatVariants; ++idx) {
         const EllVariant& ev = kEllLatVariants[idx];
         if (h->max_dc > static_cast<uint32_t>(ev.dc) || h->max_dv > static_cast<uint32_t>(ev.dv)) continue;
         uint32_t want = 32;
         for (uint32_t k = 0; k < P.nseg; ++k) {
           const uint32_t ms = P.segs[k].c1 - P.segs[k].c0;
-          want = std::max(want, std::max((ms + ev.cpt - 1) / ev.cpt,
-                                         (P.ell_nvars[k] + ev.vpt - 1) / ev.vpt));
+          want = std::max(want, std::max(ms, (P.ell_nvars[k] + 1) / 2));
         }
         const uint32_t T = round_up32(want);
-        if (T > static_cast<uint32_t>(ev.maxt)) continue;
-        LaunchPlan pl{};
-        pl.items = true;
-        pl.lean = true;
-        pl.ell = 100 * ev.dc + ev.dv;
-        pl.kernel = ell_lat_kernel(h->arith, idx);
-        pl.name = "decode_ell_kernel";
-        pl.ngroups = 1;
-        pl.group_threads = T;
-        finish_plan(h, pl);
-        h->lat_ell = pl;
+        const size_t smem = ell_latency_smem_bytes(P.seg_mmax, P.seg_nmax, ell_msg_bytes(h->arith),
+                                                   static_cast<uint32_t>(ev.dc), T);
+        if (T > 1024 || smem > static_cast<size_t>(h->max_smem_optin)) continue;
+        h->lat_lean_kernel = ell_lat_kernel(h->arith, idx);
+        h->lat_lean_block = T;
+        h->lat_lean_smem = smem;
+        CUDA_TRY(cudaFuncSetAttribute(h->lat_lean_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
         break;
       }
     }
@@ -1259,13 +1256,10 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
     return;
   }
 
-  // ---- graphs the lean kernel does not cover: degree-padded / generic / regular kernels
-  // The degree-padded kernel merges the segments' bit vectors with device atomics, so its
-  // single shots always take the copy protocol (device buffers, H2D / kernel / D2H).
-  const bool ell_shot = h->lat_ell.kernel != nullptr && !debug;
-  const bool use_mapped = mapped && !ell_shot;
+  // ---- graphs neither cluster kernel covers (or QB_OPT_KERNEL = 1 / QB_OPT_LATENCY_SHAPE = 1):
+  // the generic CSR kernel, one CTA, results to mapped memory + flag or by memcpy
   volatile uint32_t* h_flag = reinterpret_cast<volatile uint32_t*>(h->h_out + h->off_flag);
-  unsigned char* out = use_mapped ? h->d_out_map : h->d_out_dev;
+  unsigned char* out = mapped ? h->d_out_map : h->d_out_dev;
   io.est = reinterpret_cast<uint32_t*>(out);
   io.resid = reinterpret_cast<uint32_t*>(out + h->off_res);
   io.conv = out + h->off_conv;
@@ -1273,46 +1267,14 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
   io.kernel_ns = reinterpret_cast<uint64_t*>(out + h->off_ns);
   io.flag = reinterpret_cast<volatile uint32_t*>(out + h->off_flag);
   std::memcpy(h->h_in, syndrome, P.syn_w32 * 4);
-  io.syn = use_mapped ? h->d_in_map : h->d_in_dev;
-  if (use_mapped) {
-    launch_plan(h, h->lat, io, h->lat.cluster ? h->P.nseg : 1, h->stream);
+  io.syn = mapped ? h->d_in_map : h->d_in_dev;
+  if (mapped) {
+    launch_plan(h, h->lat, io, 1, h->stream);
     spin_until(h, [&] { return *h_flag == seq; }, false);
   } else {
-    auto enqueue = [&] {
-      CUDA_TRY(cudaMemcpyAsync(h->d_in_dev, h->h_in, P.syn_w32 * 4, cudaMemcpyHostToDevice,
-                               h->stream));
-      if (ell_shot) {
-        io.tile = 1;
-        launch_plan(h, h->lat_ell, io, h->P.nseg, h->stream);  // one CTA per segment
-      } else {
-        launch_plan(h, h->lat, io, h->lat.cluster ? h->P.nseg : 1, h->stream);
-      }
-      CUDA_TRY(cudaMemcpyAsync(h->h_out, h->d_out_dev, h->out_bytes, cudaMemcpyDeviceToHost,
-                               h->stream));
-    };
-    if (ell_shot && h->opt_latency_graph != 0) {
-      // nothing in the three operations depends on the shot: one graph, captured once
-      if (!h->ell_graph) {
-        cudaGraph_t graph = nullptr;
-        CUDA_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-        try {
-          enqueue();
-        } catch (...) {
-          cudaStreamEndCapture(h->stream, &graph);
-          if (graph) cudaGraphDestroy(graph);
-          throw;
-        }
-        CUDA_TRY(cudaStreamEndCapture(h->stream, &graph));
-        const cudaError_t ie = cudaGraphInstantiate(&h->ell_graph, graph, 0);
-        cudaGraphDestroy(graph);
-        CUDA_TRY(ie);
-        --h->launches;
-      }
-      CUDA_TRY(cudaGraphLaunch(h->ell_graph, h->stream));
-      ++h->launches;
-    } else {
-      enqueue();
-    }
+    CUDA_TRY(cudaMemcpyAsync(h->d_in_dev, h->h_in, P.syn_w32 * 4, cudaMemcpyHostToDevice, h->stream));
+    launch_plan(h, h->lat, io, 1, h->stream);
+    CUDA_TRY(cudaMemcpyAsync(h->h_out, h->d_out_dev, h->out_bytes, cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
   }
   std::memcpy(estimate, h->h_out, P.est_w32 * 4);
@@ -1534,6 +1496,7 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
     P.clamp_f = static_cast<float>(1e30);
     P.alpha_fx = alpha_fx;
     P.kmax = kmax;
+    P.kmax_f = static_cast<float>(kmax);
     P.deg1_i = kmax ? static_cast<int32_t>((static_cast<int64_t>(kmax) * alpha_fx + 32768) >> 16) : 0;
     for (size_t s = 0; s < segs.size(); ++s) {
       P.segs[s] = {segs[s].check_begin, segs[s].check_end, segs[s].var_begin, segs[s].var_end,
@@ -1669,9 +1632,15 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
         {
           // the same table for the integer modes (exact sums: the order cannot matter)
           const int32_t sgn = g0 < 0 ? -1 : 1;
+          P.gamma_f = static_cast<float>(g0);
           for (int ko = 0; ko < 3; ++ko) {
-            const int32_t v = g0 + sgn * (2 - 2 * ko) * P.it1_i;
-            P.it1_tq[ko] = static_cast<uint32_t>(std::max(-kmax, std::min(kmax, v)));
+            const int32_t v = std::max(-kmax, std::min(kmax, g0 + sgn * (2 - 2 * ko) * P.it1_i));
+            if (arith == QB_ARITH_INT16) {  // the int16 batch kernels keep integers in fp32 words
+              const float vf = static_cast<float>(v);
+              std::memcpy(&P.it1_tq[ko], &vf, 4);
+            } else {
+              P.it1_tq[ko] = static_cast<uint32_t>(v);
+            }
           }
           P.it1_dec4 = 0;
           for (int k = 0; k < 4; ++k) {
@@ -2279,7 +2248,7 @@ void launch_campaign_fused(qb_decoder* h, uint64_t seed, double p, uint64_t firs
   const DecodeParams& P0 = h->P;
   const bool fast = h->fast_ok && h->opt_fast != 0 && h->tab_ok;
   CampKernelFn kern = h->arith == QB_ARITH_FLOAT ? campaign_kernel_t<ArithF32>(fast, P0.early != 0)
-                                                 : campaign_kernel_t<ArithI32>(fast, P0.early != 0);
+                                                 : campaign_kernel_t<ArithI16F>(fast, P0.early != 0);
   const uint32_t T = regular_group_threads(P0, 3, 5);
   const size_t smem = campaign_smem_bytes(P0.seg_mmax, 0);
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));

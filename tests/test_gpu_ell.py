@@ -222,9 +222,12 @@ def test_packed_pairs_on_irregular_graphs(oracle, mode):
 
 @pytest.mark.parametrize("mode", REF_MODES)
 def test_single_shots_through_the_degree_padded_kernel(oracle, mode):
-    """qb_decode on irregular graphs runs the degree-padded kernel with one check per thread
-    and one CTA per segment (copy protocol): every outcome, per segment, equals the oracle's,
-    in both single-shot I/O settings, interleaved with batches on the same handle."""
+    """qb_decode on irregular graphs runs decode_ell_latency_kernel - the degree-padded node
+    updates inside the single-shot cluster protocol (one CTA per segment, one check per
+    thread): every outcome, per segment, equals the oracle's in all three I/O settings
+    (syndrome in the kernel parameters + mapped records, memcpy protocol, persistent
+    doorbell without a launch per shot), interleaved with batches on the same handle; the
+    final edge messages (qb_decode_debug) match bit for bit."""
     OPT_LATENCY_IO = 1
     code = codes.make_code("bb144")
     h, segs = codes.extended_graph(code)
@@ -239,13 +242,24 @@ def test_single_shots_through_the_degree_padded_kernel(oracle, mode):
                             priors=priors.tolist())
         want = oracle.decode_many(g, cfg, syn, segs)
         with Decoder(g, cfg, segments=segs) as dec:
-            for io_mode in (0, 1):
+            assert dec.get_option(106) == 1 and dec.get_option(103) == 1  # cluster kernel in use
+            for io_mode in (0, 1, 2):
                 dec.set_option(OPT_LATENCY_IO, io_mode)
+                launches = dec.launch_count()
                 for k in range(len(syn)):
                     one = dec.decode_segments(syn[k])
                     assert all(np.array_equal(a, b[k]) for a, b in zip(one, want)), (io_mode, k)
                     assert dec.last_kernel_ns() > 0
+                if io_mode == 2:
+                    assert dec.launch_count() - launches <= 2, "doorbell mode must not launch per shot"
                 assert _same(_batch(dec, syn), want)
+            dec.set_option(OPT_LATENCY_IO, 0)
+            for k in (0, 17, 59):
+                est, res, conv, its, q, r = dec.decode_debug(syn[k])
+                _, _, _, oi, oq, orr = oracle.decode(g, cfg, syn[k], segs)
+                assert np.array_equal(its, oi)
+                assert np.array_equal(q.view(np.uint32), oq.view(np.uint32))
+                assert np.array_equal(r.view(np.uint32), orr.view(np.uint32))
     # irregular single-segment graphs with degree-0 / degree-1 nodes
     for g2 in (codes.build_tanner_graph(_degree_zero_graph()),
                codes.build_tanner_graph(random_ldpc_matrix(rng, 25, 60))):
@@ -254,9 +268,11 @@ def test_single_shots_through_the_degree_padded_kernel(oracle, mode):
         syn2 = random_syndromes(rng, 40, g2.num_checks, 0.3)
         want = oracle.decode_many(g2, cfg, syn2, None)
         with Decoder(g2, cfg) as dec:
-            for k in range(len(syn2)):
-                one = dec.decode_segments(syn2[k])
-                assert all(np.array_equal(a, b[k]) for a, b in zip(one, want)), k
+            for io_mode in (0, 2):
+                dec.set_option(OPT_LATENCY_IO, io_mode)
+                for k in range(len(syn2)):
+                    one = dec.decode_segments(syn2[k])
+                    assert all(np.array_equal(a, b[k]) for a, b in zip(one, want)), (io_mode, k)
 
 
 def test_rejected_option_does_not_stick(oracle):

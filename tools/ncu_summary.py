@@ -87,8 +87,19 @@ def traffic_json(path, out, shots, arithmetic, workload):
     for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         i = hdr.index(name)
         tot[name] = float(vals[i].replace(",", "")) * scale[units[i]]
+    def pct(name):
+        try:
+            return float(vals[hdr.index(name)].replace(",", ""))
+        except (ValueError, IndexError):
+            return None
+
     with open(out, "w") as f:
         json.dump({"kernel": vals[hdr.index("Kernel Name")], "shots_per_launch": int(shots),
+                   "smem_wavefronts_pct_of_peak": pct(
+                       "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+                   "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                   "alu_pipe_pct": pct("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                   "xu_pipe_pct": pct("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
                    "arithmetic": arithmetic, "workload": workload,
                    "dram_bytes_read": tot["dram__bytes_read.sum"],
                    "dram_bytes_write": tot["dram__bytes_write.sum"],

@@ -6,9 +6,9 @@
 set -u
 R=${1:-r1}
 PARTS=${2:-"other parity"}
-SMALL='toy or bb72 or zero_syndrome or irregular or unit_degrees or degree_zero or tma_tiles or regular_and_cluster or packed_fp16 or generator_reproduces or independent_of_the_partition or skip_sampler'
+SMALL='toy or bb72 or zero_syndrome or irregular or unit_degrees or degree_zero or tma_tiles or regular_and_cluster or packed_fp16 or generator_reproduces or independent_of_the_partition or skip_sampler or fused_campaign or messages_half or degree_padded_batch_kernel_messages or soft_requires or device_campaigns_on_the_extended or alist'
 for part in $PARTS; do
-  if [ "$part" = parity ]; then sel="tests/test_gpu_parity.py"; else sel="tests/test_gpu_ell.py tests/test_gpu_noise.py tests/test_gpu_campaign.py"; fi
+  if [ "$part" = parity ]; then sel="tests/test_gpu_parity.py"; else sel="tests/test_gpu_ell.py tests/test_gpu_noise.py tests/test_gpu_campaign.py tests/test_gpu_soft.py"; fi
   log=/tmp/racecheck_${part}.log
   timeout ${SANITIZE_TIMEOUT:-1200} compute-sanitizer --tool racecheck --racecheck-report all --show-backtrace no \
       --print-limit 2000000 --target-processes all --log-file $log \

@@ -12,8 +12,8 @@ R=${1:-r1}
 TOOLS=${2:-"memcheck racecheck synccheck initcheck"}
 mkdir -p gpurun_out
 SKIP="--deselect tests/test_alist_csv.py::test_gpu_bench_rows_validate_and_digest_matches_reference"
-SUBSET="tests/test_gpu_parity.py tests/test_gpu_ell.py tests/test_gpu_noise.py tests/test_gpu_campaign.py"
-SMALL='toy or bb72 or zero_syndrome or irregular or unit_degrees or degree_zero or tma_tiles or regular_and_cluster or memcpy_protocol or packed_fp16 or generator_reproduces or independent_of_the_partition'
+SUBSET="tests/test_gpu_parity.py tests/test_gpu_ell.py tests/test_gpu_noise.py tests/test_gpu_campaign.py tests/test_gpu_soft.py"
+SMALL='toy or bb72 or zero_syndrome or irregular or unit_degrees or degree_zero or tma_tiles or regular_and_cluster or memcpy_protocol or packed_fp16 or generator_reproduces or independent_of_the_partition or fused_campaign or messages_half or degree_padded_batch_kernel_messages or soft_requires or device_campaigns_on_the_extended or rejected_option or alist'
 for tool in $TOOLS; do
   log=gpurun_out/${R}_${tool}.log
   if [ "$tool" = memcheck ]; then
