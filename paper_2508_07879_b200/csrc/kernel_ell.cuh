@@ -125,8 +125,13 @@ __device__ __forceinline__ void cn_ell(const DecodeParams& P, ArithF32, unsigned
     m1 = fminf(m1, a[j]);
   }
   // float(alpha * |min|): fp64 product, one rounding (decoder.cpp:302-307)
-  const uint32_t s1 = __float_as_uint(static_cast<float>(P.alpha * static_cast<double>(m1)));
-  const uint32_t s2 = __float_as_uint(static_cast<float>(P.alpha * static_cast<double>(m2)));
+  uint32_t s1 = __float_as_uint(static_cast<float>(P.alpha * static_cast<double>(m1)));
+  uint32_t s2 = __float_as_uint(static_cast<float>(P.alpha * static_cast<double>(m2)));
+  // keep the two products where they are: left alone, the compiler turns "select one of two
+  // products" into "product of the selected minimum" PER EDGE - DC widenings, multiplies and
+  // narrowings per check instead of two (14 of the 77 conversions per thread and iteration
+  // on the (7,3) graphs, with the conversion pipe at 71 %)
+  asm volatile("" : "+r"(s1), "+r"(s2));
   uint32_t sx = syn_bit << 31;
 #pragma unroll
   for (int j = 0; j < DC; ++j) sx ^= __float_as_uint(v[j]);
@@ -152,10 +157,11 @@ __device__ __forceinline__ void cn_ell(const DecodeParams& P, ArithF16, unsigned
   int32_t m1, m2;
   two_smallest_n<DC>(a, m1, m2);
   const __half alpha = __ushort_as_half(P.alpha_h);
-  const uint32_t s1 =
+  uint32_t s1 =
       __half_as_ushort(__hmul(alpha, __ushort_as_half(static_cast<unsigned short>(m1))));
-  const uint32_t s2 =
+  uint32_t s2 =
       __half_as_ushort(__hmul(alpha, __ushort_as_half(static_cast<unsigned short>(m2))));
+  asm volatile("" : "+r"(s1), "+r"(s2));  // two products per check, not one per edge (see ArithF32)
   uint32_t sx = syn_bit << 15;
 #pragma unroll
   for (int j = 0; j < DC; ++j) sx ^= u[j];
@@ -179,8 +185,9 @@ __device__ __forceinline__ void cn_ell_int(const DecodeParams& P, unsigned char*
   }
   int32_t m1, m2;
   two_smallest_n<DC>(a, m1, m2);
-  const int32_t s1 = scale_q16(static_cast<uint32_t>(m1), P.alpha_fx);
-  const int32_t s2 = scale_q16(static_cast<uint32_t>(m2), P.alpha_fx);
+  int32_t s1 = scale_q16(static_cast<uint32_t>(m1), P.alpha_fx);
+  int32_t s2 = scale_q16(static_cast<uint32_t>(m2), P.alpha_fx);
+  asm volatile("" : "+r"(s1), "+r"(s2));  // two scalings per check, not one per edge (see ArithF32)
   int32_t sx = static_cast<int32_t>(syn_bit << 31);
 #pragma unroll
   for (int j = 0; j < DC; ++j) sx ^= v[j];
