@@ -741,10 +741,12 @@ def compact_latency(table: dict) -> dict:
 
 
 def measure_latency_bb144(args) -> dict:
-    """BASELINE config 2: [[144,12,12]] single shots, fp32, ONE CTA per shot (both segments in
-    one CTA, QB_OPT_LATENCY_SHAPE = 1) and, beside it, the 2-CTA cluster the loader would pick;
-    pool = trials 0..255 of sample_error(p, seed) exactly as run_bench builds it
-    (proj/src/bench.cpp:203-211), generated by the bit-exact device sampler."""
+    """BASELINE config 2: [[144,12,12]] single shots, fp32, ONE CTA per shot - a decoder built
+    from the combined Tanner graph (the reference's `Decoder(graph, cfg)` constructor: one
+    segment, decoder.cpp:406-413), which the cluster kernel runs as a cluster of one CTA - and,
+    beside it, the CssCode decoder (two segments) as a 2-CTA cluster; pool = trials 0..255 of
+    sample_error(p, seed) exactly as run_bench builds it (proj/src/bench.cpp:203-211),
+    generated by the bit-exact device sampler."""
     import torch
     from paper_2508_07879_b200 import Decoder, DecoderConfig, codes, gf2
     code = codes.make_code("bb144")
@@ -753,31 +755,33 @@ def measure_latency_bb144(args) -> dict:
     out = {}
     for label, iters, early in (("fixed10", 10, False), ("cap50_early", 50, True)):
         cfg = DecoderConfig(max_iterations=iters, early_termination=early, arithmetic=args.arithmetic)
-        with Decoder(code, cfg) as dec:
-            dec.generate_syndromes(args.seed, args.p, 256, d_pool.data_ptr(), None,
+        row = {}
+        with Decoder(code, cfg) as gen:
+            gen.generate_syndromes(args.seed, args.p, 256, d_pool.data_ptr(), None,
                                    stream=torch.cuda.current_stream().cuda_stream)
             torch.cuda.synchronize()
-            pool = d_pool.cpu().numpy().astype(np.uint64)
-            row = {}
-            for shape, shape_name in ((1, "one_cta_per_shot"), (0, "cluster")):
-                dec.set_option(2, shape)
+        pool = d_pool.cpu().numpy().astype(np.uint64)
+        for shape_name, target in (("one_cta_per_shot", g), ("cluster", code)):
+            with Decoder(target, cfg) as dec:
+                assert dec.get_option(106) == 1, "cluster kernel expected"
                 for io_mode, io_name in ((1, "memcpy"), (0, "mapped"), (2, "doorbell")):
-                    if shape == 1 and io_mode == 2:
-                        continue  # the doorbell belongs to the cluster kernel
                     dec.set_option(1, io_mode)
                     wall, kern, _ = dec.latency_run(pool, 300, args.latency_shots)
                     wall = np.sort(wall.astype(np.float64) * 1e-3)
                     kern = np.sort(kern.astype(np.float64) * 1e-3)
                     r = {"p50": nearest_rank(wall, 50), "p99": nearest_rank(wall, 99),
                          "kernel_p50": nearest_rank(kern, 50), "kernel_p99": nearest_rank(kern, 99)}
-                    if io_mode == 1 and dec.get_option(106):  # CUDA events: the lean cluster path
+                    if io_mode == 1:  # the same protocol timed by CUDA events on the stream
                         dec.set_option(11, 1)
                         _, ev, _ = dec.latency_run(pool, 300, args.latency_shots)
                         dec.set_option(11, 0)
                         ev = np.sort(ev.astype(np.float64) * 1e-3)
                         r.update(cuda_event_p50=nearest_rank(ev, 50), cuda_event_p99=nearest_rank(ev, 99))
                     row[f"{shape_name}_{io_name}"] = r
-            out[label] = row
+        out[label] = row
+    out["shapes"] = ("one_cta_per_shot = Decoder(combined graph): one segment, X and Z stop together "
+                     "(identical outcomes at a fixed iteration count); cluster = Decoder(CssCode): "
+                     "one CTA per segment, segments stop independently")
     return {"bb144_%s" % args.arithmetic: out}
 
 
