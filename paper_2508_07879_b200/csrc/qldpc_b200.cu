@@ -843,7 +843,9 @@ void choose_plans(qb_decoder* h) {
     // CTAs per SM hides the dependent chains better (24.8 vs 23.5 M/s)
     const int order_f32[] = {4, 3, 6, 1, 1, 1, 1}, order_h2[] = {8, 3, 6, 1, 1, 1, 1},
               order_fixed[] = {11, 4, 3, 6, 1, 1, 1};
-    const int* order_auto = pair_wanted ? order_h2 : P.early ? order_f32 : order_fixed;
+    // (int16 on fp32 instructions has no conversion chains to hide: 64 registers, no spills, win
+    // at a fixed count too: 25.0 vs 23.5 M/s)
+    const int* order_auto = pair_wanted ? order_h2 : (P.early || h->arith == QB_ARITH_INT16) ? order_f32 : order_fixed;
     for (int idx = 0; idx < 7 && !bat_done; ++idx) {
       const int variant = h->opt_batch_npt ? static_cast<int>(h->opt_batch_npt) : order_auto[idx];
       const LeanVariant& lv = kLeanVariants[variant - 1];
@@ -2247,9 +2249,10 @@ void launch_campaign_fused(qb_decoder* h, uint64_t seed, double p, uint64_t firs
                            cudaStream_t st) {
   const DecodeParams& P0 = h->P;
   const bool fast = h->fast_ok && h->opt_fast != 0 && h->tab_ok;
-  CampKernelFn kern = h->arith == QB_ARITH_FLOAT ? campaign_kernel_t<ArithF32>(fast, P0.early != 0)
-                                                 : campaign_kernel_t<ArithI16F>(fast, P0.early != 0);
   const uint32_t T = regular_group_threads(P0, 3, 5);
+  // the 48-register shape (fixed iteration counts, fp32) is built for CTAs of up to 160 threads
+  CampKernelFn kern = h->arith == QB_ARITH_FLOAT ? campaign_kernel_t<ArithF32>(fast, P0.early != 0 || T > 160)
+                                                 : campaign_kernel_t<ArithI16F>(fast, true);
   const size_t smem = campaign_smem_bytes(P0.seg_mmax, 0);
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
