@@ -89,10 +89,14 @@ __host__ __device__ inline size_t lean_bits_words(uint32_t seg_mmax) {
   return (6 * static_cast<size_t>(lean_pw(seg_mmax)) + 8 + 3) & ~size_t(3);  // keeps 16-byte alignment
 }
 constexpr uint32_t kLeanTabBytes = 16;  // first-iteration table at shared-memory offset 0
+// per-item constants of the two single-warp prologue jobs, computed once per CTA: the bit masks
+// of the (up to 64) estimate words a segment owns, and of the 32 local syndrome words
+constexpr uint32_t kLeanLaneTabWords = 96;
 __host__ __device__ inline size_t lean_smem_bytes(uint32_t seg_mmax, int arith, uint32_t syn_w32) {
   const size_t msg = (static_cast<size_t>(seg_mmax + 1) * lean_stride(arith) + 15) & ~size_t(15);
   // table | messages | bitmaps, counters, tickets | 2 syndrome tiles | 2 mbarriers | tile info [2][2]
-  return kLeanTabBytes + msg + 4 * lean_bits_words(seg_mmax) + 2 * kMaxTile * syn_w32 * 4 + 16 + 16 + 16;
+  return kLeanTabBytes + msg + 4 * lean_bits_words(seg_mmax) + 2 * kMaxTile * syn_w32 * 4 + 16 + 16 + 16 +
+         4 * kLeanLaneTabWords;
 }
 
 // ---- check update on one message block ---------------------------------------
@@ -578,7 +582,13 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
   // warp 0's tile cursor lives in shared memory (it is touched once per item, and registers
   // are what this kernel is short of): buffer in use, item within it, mbarrier phase bits
   uint32_t* const tstate = tinfo + 4;  // {tb, ti, tphase}
+  uint32_t* const zmask = tstate + 4;  // [64] mask of this segment's bits in estimate word vw0 + w
+  uint32_t* const cmask = zmask + 64;  // [32] valid bits of local syndrome word w
   const uint32_t K = io.tile, tile_words = kMaxTile * P.syn_w32;
+  for (uint32_t w = tid; w < 64u; w += T) zmask[w] = w < vspan ? range_mask(vw0 + w, seg.v0, v1z) : 0u;
+  if (tid < 32u) {
+    cmask[tid] = tid >= pws ? 0u : (Ms - tid * 32u < 32u ? (1u << (Ms - tid * 32u)) - 1u : 0xffffffffu);
+  }
 
   // ---- per-thread tables: byte offsets of the q side of every edge / check block
   uint32_t eo[VPT][kDV], co[CPT], cl[CPT], valid = 0;
@@ -652,12 +662,7 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
           lane < gspan ? tilebuf[tb * tile_words + ti * P.syn_w32 + gw0 + lane] : 0u;
       uint32_t nb = __shfl_down_sync(0xffffffffu, raw_next, 1);
       if (lane + 1 >= gspan) nb = 0;
-      uint32_t loc = cshift ? __funnelshift_r(raw_next, nb, cshift) : raw_next;
-      if (lane >= pws) {
-        loc = 0;
-      } else if (Ms - lane * 32u < 32u) {
-        loc &= (1u << (Ms - lane * 32u)) - 1u;
-      }
+      const uint32_t loc = (cshift ? __funnelshift_r(raw_next, nb, cshift) : raw_next) & cmask[lane];
       if (lane < pw) {
         par[lane] = loc;
         syn0[lane] = loc;
@@ -676,7 +681,7 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
     if (warp == nwarps - 1) {  // zero this segment's bits of the shot's estimate
       uint32_t* est_g = io.est + shot * P.est_w32 + vw0;
       for (uint32_t w = lane; w < vspan; w += 32u) {
-        const uint32_t mask = range_mask(vw0 + w, seg.v0, v1z);
+        const uint32_t mask = w < 64u ? zmask[w] : range_mask(vw0 + w, seg.v0, v1z);
         if (mask == 0xffffffffu) {
           est_g[w] = 0u;
         } else {
@@ -771,14 +776,11 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
         }
       }
     }
-    if (eprev) {
+    if (eprev) {  // few variables decide 1: walk the set bits instead of testing all VPT
       uint32_t* est_g = io.est + shot * P.est_w32;
-#pragma unroll
-      for (int k = 0; k < VPT; ++k) {
-        if ((eprev >> k) & 1u) {
-          const uint32_t n = seg.v0 + tid + k * T;
-          atomicOr(&est_g[n >> 5], 1u << (n & 31u));
-        }
+      for (uint32_t bits = eprev; bits; bits &= bits - 1u) {
+        const uint32_t n = seg.v0 + tid + (__ffs(bits) - 1) * T;
+        atomicOr(&est_g[n >> 5], 1u << (n & 31u));
       }
     }
     if (tid == 0) {
