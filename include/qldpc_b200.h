@@ -104,7 +104,7 @@ typedef enum {
   /* CTAs per SM for the persistent batch kernel (0 = auto). */
   QB_OPT_BATCH_CTAS_PER_SM = 4,
   /* Batch item kernel variant (checks x variables per thread, CTAs per SM):
-   * 0 = auto, else one of the instantiations 1, 3, 4, 6, 8, 11 (see kLeanVariants). */
+   * 0 = auto, else one of the instantiations 1, 2, 3, 4, 6, 8, 11 (see kLeanVariants). */
   QB_OPT_BATCH_VARIANT = 5,
   /* Single-shot cluster kernel: 1 or 2 checks (and twice as many variables)
    * per thread; 0 = auto. */

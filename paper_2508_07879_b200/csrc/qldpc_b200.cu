@@ -359,11 +359,12 @@ KernelFn generic_kernel(int arith) {
 struct LeanVariant {
   int cpt, vpt, maxt, minb;
 };
-// Variant numbers are stable identifiers (QB_OPT_BATCH_VARIANT); 2, 5, 7, 9 and 10 were
+// Variant numbers are stable identifiers (QB_OPT_BATCH_VARIANT); 5, 7, 9 and 10 were
 // measured, never selected by the loader and retired (maxt = 0).
 constexpr LeanVariant kLeanVariants[] = {
     {1, 2, 1024, 1},  // 1: widest CTA, any segment size up to 960 checks
-    {0, 0, 0, 0},     // 2: retired
+    {3, 5, 160, 7},   // 2: 56 registers, seven 5-warp CTAs per SM: the fp32 / int16 choice since the
+                      //    first iteration is a table (no spills left at 56: 127.3 vs 123.9 M/s)
     {2, 4, 256, 3},   // 3
     {3, 5, 192, 5},   // 4: 64 registers, six CTAs per SM on [[784,24,24]]: the early-stop choice
     {0, 0, 0, 0},     // 5: retired
@@ -380,6 +381,7 @@ template <class A, bool kFast>
 KernelFn lean_kernel_tf(int variant) {
   switch (variant) {
     case 1: return decode_lean_kernel<A, 1, 2, kFast, 1024, 1>;
+    case 2: return decode_lean_kernel<A, 3, 5, kFast, 160, 7>;
     case 3: return decode_lean_kernel<A, 2, 4, kFast, 256, 3>;
     case 4: return decode_lean_kernel<A, 3, 5, kFast, 192, 5>;
     case 8: return decode_lean_kernel<A, 3, 5, kFast, 160, 4>;
@@ -405,8 +407,8 @@ KernelFn lean_kernel(int arith, int variant, bool fast) {
 template <class A, bool kFast>
 KernelFn lean_dump_kernel_tf(int variant) {
   switch (variant) {
+    case 2: return decode_lean_kernel<A, 3, 5, kFast, 160, 7, true>;
     case 4: return decode_lean_kernel<A, 3, 5, kFast, 192, 5, true>;
-    case 11: return decode_lean_kernel<A, 3, 5, kFast, 160, 8, true>;
     default: return nullptr;
   }
 }
@@ -841,8 +843,8 @@ void choose_plans(qb_decoder* h) {
     // measured on [[784,24,24]] (fp32): with early stop the 64-register build at six CTAs per
     // SM wins (107.9 vs 101.1 M/s); at a fixed iteration count the 48-register build at eight
     // CTAs per SM hides the dependent chains better (24.8 vs 23.5 M/s)
-    const int order_f32[] = {4, 3, 6, 1, 1, 1, 1}, order_h2[] = {8, 3, 6, 1, 1, 1, 1},
-              order_fixed[] = {11, 4, 3, 6, 1, 1, 1};
+    const int order_f32[] = {2, 4, 3, 6, 1, 1, 1}, order_h2[] = {8, 3, 6, 1, 1, 1, 1},
+              order_fixed[] = {2, 11, 4, 3, 6, 1, 1};
     // (int16 on fp32 instructions has no conversion chains to hide: 64 registers, no spills, win
     // at a fixed count too: 25.0 vs 23.5 M/s)
     const int* order_auto = pair_wanted ? order_h2 : (P.early || h->arith == QB_ARITH_INT16) ? order_f32 : order_fixed;
@@ -850,7 +852,7 @@ void choose_plans(qb_decoder* h) {
       const int variant = h->opt_batch_npt ? static_cast<int>(h->opt_batch_npt) : order_auto[idx];
       const LeanVariant& lv = kLeanVariants[variant - 1];
       if (lv.maxt == 0) {
-        if (h->opt_batch_npt) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_VARIANT: that variant is retired (1, 3, 4, 6, 8, 11 exist)");
+        if (h->opt_batch_npt) fail(QB_INVALID_ARGUMENT, "QB_OPT_BATCH_VARIANT: that variant is retired (1, 2, 3, 4, 6, 8, 11 exist)");
         continue;
       }
       const uint32_t T = regular_group_threads(P, lv.cpt, lv.vpt);
@@ -2228,12 +2230,12 @@ void check_soft_channel(double mu, double sigma) {
 using CampKernelFn = void (*)(DecodeParams, CampaignIO);
 template <class A>
 CampKernelFn campaign_kernel_t(bool fast, bool early) {
-  if (early) {
+  if (early) {  // `early` here: CTAs of more than 160 threads
     return fast ? decode_lean_campaign_kernel<A, 3, 5, true, 192, 5>
                 : decode_lean_campaign_kernel<A, 3, 5, false, 192, 5>;
   }
-  return fast ? decode_lean_campaign_kernel<A, 3, 5, true, 160, 8>
-              : decode_lean_campaign_kernel<A, 3, 5, false, 160, 8>;
+  return fast ? decode_lean_campaign_kernel<A, 3, 5, true, 160, 7>
+              : decode_lean_campaign_kernel<A, 3, 5, false, 160, 7>;
 }
 
 bool campaign_fusable(const qb_decoder* h, const double* probs, bool soft) {
@@ -2250,9 +2252,9 @@ void launch_campaign_fused(qb_decoder* h, uint64_t seed, double p, uint64_t firs
   const DecodeParams& P0 = h->P;
   const bool fast = h->fast_ok && h->opt_fast != 0 && h->tab_ok;
   const uint32_t T = regular_group_threads(P0, 3, 5);
-  // the 48-register shape (fixed iteration counts, fp32) is built for CTAs of up to 160 threads
-  CampKernelFn kern = h->arith == QB_ARITH_FLOAT ? campaign_kernel_t<ArithF32>(fast, P0.early != 0 || T > 160)
-                                                 : campaign_kernel_t<ArithI16F>(fast, true);
+  // seven CTAs per SM at 56 registers for CTAs of up to 160 threads, else the 192-thread shape
+  CampKernelFn kern = h->arith == QB_ARITH_FLOAT ? campaign_kernel_t<ArithF32>(fast, T > 160)
+                                                 : campaign_kernel_t<ArithI16F>(fast, T > 160);
   const size_t smem = campaign_smem_bytes(P0.seg_mmax, 0);
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;

@@ -348,7 +348,7 @@ def test_regular_and_cluster_kernels_match_oracle(oracle, name, mode):
             for bshape in (1, 2):  # CTA per shot / CTA per (shot, segment) work item
                 dec.set_option(OPT_BATCH_SHAPE, bshape)
                 assert dec.get_option(OPT_BATCH_SHAPE) == bshape
-                for npt in ((0,) if bshape == 1 else (1, 3, 4, 6, 8, 11)):
+                for npt in ((0,) if bshape == 1 else (1, 2, 3, 4, 6, 8, 11)):
                     dec.set_option(OPT_BATCH_NPT, npt)
                     for fast in (1, 0):
                         dec.set_option(OPT_FAST_PATH, fast)
