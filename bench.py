@@ -699,6 +699,28 @@ def measure_latency(args, code, lib, d_syn):
                     "mean": float(np.mean(wall)), "kernel_p50": nearest_rank(kern, 50),
                     "kernel_p99": nearest_rank(kern, 99), "shots": args.latency_shots,
                     "kernel": "decode_ell_latency_kernel" if dec.get_option(106) else "decode_generic_kernel"}
+    # ... and config 5 as named (soft syndromes): every single shot carries its own priors of the
+    # measurement-error variables (qb_decode_soft); l_m = (1 - 2 s_m) mu + N(0, sigma^2)
+    mu, sigma = 1.0, 0.39
+    s0 = hx.mat_vec((rng.random((256, gx.num_vars)) < pq).astype(np.uint8) * data_mask(code, gx)[None, :])
+    lm = (1.0 - 2.0 * s0) * mu + sigma * rng.standard_normal(s0.shape)
+    pool5s, llr5 = gf2.pack_bits((lm < 0).astype(np.uint8)), 2.0 * mu * np.abs(lm) / sigma ** 2
+    for arith in ("int8", "float"):
+        cfg = DecoderConfig(max_iterations=10, early_termination=False, arithmetic=arith,
+                            priors=[float(np.log((1 - pq) / pq))] * gx.num_vars)
+        with Decoder(gx, cfg, segments=segs) as dec:
+            soft5 = dec.quantize_soft(llr5)
+            for io_mode, io_name in ((2, "doorbell"), (0, "mapped"), (1, "memcpy")):
+                dec.set_option(1, io_mode)
+                wall, kern, digest = dec.latency_run(pool5s, 300, args.latency_shots, soft_pool=soft5)
+                wall = np.sort(wall.astype(np.float64) * 1e-3)
+                kern = np.sort(kern.astype(np.float64) * 1e-3)
+                out[f"config5_soft_{arith}_fixed10_{io_name}"] = {
+                    "p50": nearest_rank(wall, 50), "p99": nearest_rank(wall, 99),
+                    "mean": float(np.mean(wall)), "kernel_p50": nearest_rank(kern, 50),
+                    "kernel_p99": nearest_rank(kern, 99), "shots": args.latency_shots,
+                    "soft_bytes_per_shot": int(soft5.shape[1] * soft5.itemsize), "mu": mu, "sigma": sigma,
+                    "api": "qb_decode_soft", "kernel": "decode_ell_latency_kernel"}
     out["note"] = ("wall = host steady_clock around the whole qb_decode (copy-in, launch, "
                    "completion, copy-out) inside qb_latency_run; kernel = in-kernel %globaltimer "
                    "span; doorbell = persistent cluster polling mapped host memory (no launch per "
@@ -708,6 +730,16 @@ def measure_latency(args, code, lib, d_syn):
                    "launch per decode (memcpy_nograph: three separate stream operations); cuda_event = "
                    "cudaEventRecord before the H2D copy and after the D2H copy of that protocol")
     return out
+
+
+def data_mask(code, gx) -> np.ndarray:
+    """1 for the data-qubit variables of the extended graph [Hz | I] (+) [Hx | I], 0 for the
+    measurement-error variables."""
+    n, mz = code.n, code.hz.rows
+    m = np.zeros(gx.num_vars, dtype=np.uint8)
+    m[:n] = 1
+    m[n + mz:2 * n + mz] = 1
+    return m
 
 
 def compact_latency(table: dict) -> dict:
@@ -737,6 +769,13 @@ def compact_latency(table: dict) -> dict:
                 row[proto] = {"p50": r["p50"], "p99": r["p99"]}
         if row:
             out[f"config5_ext784_{arith}"] = {"fixed10": row}
+        row = {}
+        for proto in ("memcpy", "mapped", "doorbell"):
+            r = table.get(f"config5_soft_{arith}_fixed10_{proto}")
+            if r:
+                row[proto] = {"p50": r["p50"], "p99": r["p99"]}
+        if row:
+            out[f"config5_soft784_{arith}"] = {"fixed10": row}
     return out
 
 

@@ -264,6 +264,13 @@ qb_status qb_latency_run(qb_decoder* h, const uint64_t* pool,
                          uint64_t* wall_ns, uint64_t* kernel_ns,
                          uint64_t* digest);
 
+/* ... the same with per-shot priors: soft_pool = [pool_size][num_checks] values in the
+ * layout of qb_decode_batch_soft (NULL = qb_latency_run); every decode is a qb_decode_soft. */
+qb_status qb_latency_run_soft(qb_decoder* h, const uint64_t* pool, const void* soft_pool,
+                              uint64_t pool_size, uint64_t warmup, uint64_t measure,
+                              uint64_t* wall_ns, uint64_t* kernel_ns,
+                              uint64_t* digest);
+
 /* Decoder::last_kernel_ns (decoder.cpp:593-596): device-side %globaltimer
  * span of the most recent qb_decode (first instruction to last store). */
 uint64_t qb_last_kernel_ns(const qb_decoder* h);
@@ -357,6 +364,11 @@ qb_status qb_classify_batch_device(qb_decoder* h, uint64_t shots,
  * `priors[qb_soft_vars()[m]] = soft[shot][m]` (de-quantised: value / quant_scale).
  * QB_INVALID_ARGUMENT when the decoder's batch kernel is not the degree-padded one. */
 qb_status qb_soft_vars(const qb_decoder* h, uint32_t* vars /* [num_checks] out */);
+/* ... for ONE shot, latency path (qb_decode with `soft` = [num_checks] values, host memory);
+ * all three single-shot I/O protocols (QB_OPT_LATENCY_IO). */
+qb_status qb_decode_soft(qb_decoder* h, const uint64_t* syndrome, const void* soft,
+                         uint64_t* estimate, uint64_t* residual /* may be NULL */,
+                         uint8_t* converged, uint32_t* iterations);
 qb_status qb_decode_batch_soft(qb_decoder* h, uint64_t shots, const uint64_t* syndromes,
                                const void* soft, uint64_t* estimates,
                                uint64_t* residuals /* may be NULL */, uint8_t* converged,

@@ -75,6 +75,8 @@ SYMBOLS = {
                                         C.c_void_p]),
     "qb_latency_run": (C.c_int, [C.c_void_p, u64p, C.c_uint64, C.c_uint64, C.c_uint64, u64p,
                                  u64p, u64p]),
+    "qb_latency_run_soft": (C.c_int, [C.c_void_p, u64p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
+                                      u64p, u64p, u64p]),
     "qb_set_logicals": (C.c_int, [C.c_void_p, u64p, C.c_uint32, u64p, C.c_uint32]),
     "qb_campaign_run": (C.c_int, [C.c_void_p, C.c_uint64, C.c_double, f64p, C.c_uint64,
                                   C.c_uint64, u64p]),
@@ -83,6 +85,7 @@ SYMBOLS = {
     "qb_classify_batch_device": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
                                            C.c_void_p, C.c_void_p, C.c_void_p, u64p, C.c_void_p]),
     "qb_soft_vars": (C.c_int, [C.c_void_p, u32p]),
+    "qb_decode_soft": (C.c_int, [C.c_void_p, u64p, C.c_void_p, u64p, u64p, u8p, u32p]),
     "qb_decode_batch_soft": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.c_void_p, C.c_void_p, C.c_void_p]),
     "qb_decode_batch_soft_device": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,

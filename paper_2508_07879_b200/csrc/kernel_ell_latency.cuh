@@ -175,6 +175,25 @@ decode_ell_latency_kernel(const __grid_constant__ DecodeParams P, const __grid_c
     t_begin = static_cast<uint64_t>(cmd_word[1]) | (static_cast<uint64_t>(cmd_word[2]) << 32);
     // (the first toggles of the bitmap come after the first iteration's mid barrier)
     const uint32_t synbit = (par[cl >> 5] >> (cl & 31u)) & 1u;
+    if (ctl.soft != nullptr && aslot != kNoAbsorb) {
+      // soft syndromes: this shot's prior of the absorbed variable (read after the doorbell was
+      // seen; volatile: the values live in mapped host memory or were just copied in).  The
+      // slot belongs to this thread's own check block, so no barrier is needed before its use.
+      // Integer modes: soft_bytes = 4 when the host staged the values widened to int32 (mapped
+      // host memory: one full 128-byte request per warp), else the caller's int8 / int16.
+      const uint32_t m = seg.c0 + tid;
+      Msg v;
+      if constexpr (sizeof(Msg) == 2) {
+        v = prior_as_msg<ArithF16>(*(static_cast<const volatile float*>(ctl.soft) + m));
+      } else if constexpr (A::kInt) {
+        v = ctl.soft_bytes == 4u   ? static_cast<Msg>(*(static_cast<const volatile int32_t*>(ctl.soft) + m))
+            : ctl.soft_bytes == 1u ? static_cast<Msg>(*(static_cast<const volatile int8_t*>(ctl.soft) + m))
+                                   : static_cast<Msg>(*(static_cast<const volatile int16_t*>(ctl.soft) + m));
+      } else {
+        v = *(static_cast<const volatile float*>(ctl.soft) + m) + 0.0f;
+      }
+      *reinterpret_cast<Msg*>(msgs + co + aslot * kMsg) = v;
+    }
 
     // ---------------- iterations ----------------
     uint32_t iter = 0;

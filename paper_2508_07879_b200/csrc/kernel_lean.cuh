@@ -866,6 +866,10 @@ struct LatencyCtl {
   uint64_t idle_ns;                   // mode 2: retire after this long without a doorbell
   uint32_t* rec;                      // result records, rec_stride words per segment
   uint32_t rec_stride;
+  // degree-padded kernel only: this shot's priors of the absorbed variables (qb_decode_soft),
+  // [M] elements of soft_bytes in device-accessible memory, or nullptr
+  const void* soft;
+  uint32_t soft_bytes;
 };
 
 __device__ __forceinline__ uint32_t ld_volatile_global(const volatile uint32_t* p) {

@@ -163,6 +163,13 @@ struct qb_decoder {
   std::vector<uint32_t> soft_var;        // [M] variable whose prior soft[m] replaces, or ~0u
   uint32_t* d_aux_mask = nullptr;        // [est_w32] non-data variables (qb_set_auxiliary_vars)
   uint64_t* d_tcol = nullptr;            // [N] logical-test column per variable (fused campaign kernel)
+  // single-shot soft decode (qb_decode_soft): staging for one shot's [M] soft values
+  unsigned char* h_soft1 = nullptr;      // mapped pinned
+  unsigned char* d_soft1_map = nullptr;  // ... as the device sees it
+  unsigned char* d_soft1_dev = nullptr;  // device copy (memcpy protocol)
+  bool lat_is_ell = false;               // single shots run decode_ell_latency_kernel
+  bool db_soft = false;                  // the resident doorbell kernel reads soft values
+  cudaGraphExec_t lat_graph_soft[2] = {nullptr, nullptr};
   int64_t opt_campaign_fused = 1;        // QB_OPT_CAMPAIGN_FUSED
 
   // options
@@ -216,6 +223,10 @@ void drop_latency_graphs(qb_decoder* h) {
     if (g) cudaGraphExecDestroy(g);
     g = nullptr;
   }
+  for (auto& g : h->lat_graph_soft) {
+    if (g) cudaGraphExecDestroy(g);
+    g = nullptr;
+  }
 }
 
 void free_batch(qb_decoder* h) {
@@ -257,6 +268,8 @@ void destroy(qb_decoder* h) {
   cudaFree(h->d_counters);
   cudaFree(h->d_aux_mask);
   cudaFree(h->d_tcol);
+  cudaFree(h->d_soft1_dev);
+  if (h->h_soft1) cudaFreeHost(h->h_soft1);
   if (h->h_db) cudaFreeHost(h->h_db);
   if (h->h_rec) cudaFreeHost(h->h_rec);
   cudaFree(h->d_rec_dev);
@@ -785,6 +798,7 @@ void choose_plans(qb_decoder* h) {
     }
     // single shots: the degree-padded cluster kernel (mapped / doorbell / memcpy protocols)
     h->lat_lean_kernel = nullptr;
+    h->lat_is_ell = false;
     if (h->opt_kernel != 1 && h->opt_latency_shape != 1 && P.syn_w32 <= kInlineSynWords &&
         P.nseg <= kMaxSegments) {
       for (int idx = 0; idx < kNumEllLatVariants; ++idx) {
@@ -800,6 +814,7 @@ void choose_plans(qb_decoder* h) {
                                                    static_cast<uint32_t>(ev.dc), T);
         if (T > 1024 || smem > static_cast<size_t>(h->max_smem_optin)) continue;
         h->lat_lean_kernel = ell_lat_kernel(h->arith, idx);
+        h->lat_is_ell = true;
         h->lat_lean_block = T;
         h->lat_lean_smem = smem;
         CUDA_TRY(cudaFuncSetAttribute(h->lat_lean_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -814,6 +829,7 @@ void choose_plans(qb_decoder* h) {
   // per shot whatever the segment count, which is the generic kernel's shape
   h->lat = generic_plan(h);
   h->lat_lean_kernel = nullptr;
+  h->lat_is_ell = false;
   if (h->opt_latency_shape != 1 && P.seg_mmax <= 960 && P.seg_nmax <= 960 * 2 &&
       P.syn_w32 <= kInlineSynWords) {
     for (int npt : {1, 2}) {
@@ -1142,7 +1158,7 @@ void unpack_records(qb_decoder* h, uint64_t* estimate, uint64_t* residual, uint8
 }
 
 void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, uint64_t* residual,
-                 uint8_t* converged, uint32_t* iterations, bool debug) {
+                 uint8_t* converged, uint32_t* iterations, bool debug, const void* soft = nullptr) {
   const DecodeParams& P = h->P;
   if (!syndrome || !estimate || !converged || !iterations) {
     fail(QB_INVALID_ARGUMENT, "decode: NULL buffer");
@@ -1150,7 +1166,40 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
   const int io_mode = static_cast<int>(h->opt_latency_io);
   const bool lean = h->lat_lean_kernel != nullptr;
   const bool doorbell = io_mode == 2 && lean && !debug && P.syn_w32 <= 28;
-  if (!doorbell) stop_doorbell(h);
+  const size_t soft_row = static_cast<size_t>(P.M) * h->soft_bytes;
+  // memcpy protocol: [soft values | syndrome words] travel as ONE H2D copy (a second copy node
+  // in the graph measured +3 us, a third +10 us)
+  const size_t soft_pad = (soft_row + 15) & ~static_cast<size_t>(15);
+  const size_t syn_bytes = static_cast<size_t>(P.syn_w32) * 4;
+  if (soft) {
+    if (!(lean && h->lat_is_ell)) {
+      fail(QB_INVALID_ARGUMENT, "decode_soft: per-shot priors need a graph whose single shots run the "
+                                "degree-padded cluster kernel (e.g. the extended graph [H | I])");
+    }
+    if (!h->h_soft1) {
+      CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h->h_soft1),
+                             std::max(static_cast<size_t>(P.M) * 4, soft_pad + syn_bytes), cudaHostAllocMapped));
+      CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_soft1_map), h->h_soft1, 0));
+      CUDA_TRY(cudaMalloc(&h->d_soft1_dev, soft_pad + syn_bytes));
+    }
+    // mapped / doorbell protocols read the values over PCIe: integer modes are staged widened
+    // to int32 (a warp then fetches one full 128-byte line, as the float modes do; int8 rows
+    // read as 32-byte pieces measured +2.7 us per shot)
+    if (io_mode != 1 && h->soft_bytes < 4) {
+      int32_t* dst = reinterpret_cast<int32_t*>(h->h_soft1);
+      if (h->soft_bytes == 1) {
+        const int8_t* src = static_cast<const int8_t*>(soft);
+        for (uint32_t m = 0; m < P.M; ++m) dst[m] = src[m];
+      } else {
+        const int16_t* src = static_cast<const int16_t*>(soft);
+        for (uint32_t m = 0; m < P.M; ++m) dst[m] = src[m];
+      }
+    } else {
+      std::memcpy(h->h_soft1, soft, soft_row);
+    }
+  }
+  // a resident doorbell kernel was launched either with or without the soft pointer
+  if (!doorbell || (h->db_running && h->db_soft != (soft != nullptr))) stop_doorbell(h);
   uint32_t seq = ++h->seq;
   if (seq == kDoorbellExit || seq == 0) seq = h->seq = 1;
   ShotIO io{};
@@ -1168,6 +1217,8 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
     ctl.first_seq = seq;
     ctl.rec = mapped ? h->d_rec_map : h->d_rec_dev;
     ctl.rec_stride = h->rec_stride;
+    ctl.soft = soft ? (mapped ? h->d_soft1_map : h->d_soft1_dev) : nullptr;
+    ctl.soft_bytes = mapped ? 4u : h->soft_bytes;
     SynInline syn{};
     if (doorbell) {
       // ---- persistent cluster: ring the doorbell, wait for the records
@@ -1186,6 +1237,7 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
           ctl.idle_ns = static_cast<uint64_t>(h->opt_idle_ms) * 1000000ull;
           launch_lean_latency(h, io, ctl, syn);
           h->db_running = true;
+          h->db_soft = soft != nullptr;
         }
         for (uint32_t i = 0; i < P.syn_w32; ++i) db[sector_pos(i)] = syn32[i];
         std::atomic_thread_fence(std::memory_order_release);
@@ -1204,16 +1256,26 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
       spin_until(h, [&] { return records_ready(h, seq); }, false);
     } else {
       ctl.mode = 1;  // the paper's protocol: H2D copy, kernel, D2H copy, synchronize
-      std::memcpy(h->h_in, syndrome, P.syn_w32 * 4);
-      io.syn = h->d_in_dev;
+      if (soft) {
+        std::memcpy(h->h_soft1 + soft_pad, syndrome, syn_bytes);
+        io.syn = reinterpret_cast<const uint32_t*>(h->d_soft1_dev + soft_pad);
+      } else {
+        std::memcpy(h->h_in, syndrome, syn_bytes);
+        io.syn = h->d_in_dev;
+      }
       const bool timed = h->opt_latency_events != 0;
       if (timed && !h->ev0) {
         CUDA_TRY(cudaEventCreate(&h->ev0));
         CUDA_TRY(cudaEventCreate(&h->ev1));
       }
+      cudaGraphExec_t* graphs = soft ? h->lat_graph_soft : h->lat_graph;
       auto enqueue = [&] {
-        CUDA_TRY(cudaMemcpyAsync(h->d_in_dev, h->h_in, P.syn_w32 * 4, cudaMemcpyHostToDevice,
-                                 h->stream));
+        if (soft) {
+          CUDA_TRY(cudaMemcpyAsync(h->d_soft1_dev, h->h_soft1, soft_pad + syn_bytes,
+                                   cudaMemcpyHostToDevice, h->stream));
+        } else {
+          CUDA_TRY(cudaMemcpyAsync(h->d_in_dev, h->h_in, syn_bytes, cudaMemcpyHostToDevice, h->stream));
+        }
         launch_lean_latency(h, io, ctl, syn);
         CUDA_TRY(cudaMemcpyAsync(h->h_rec, h->d_rec_dev,
                                  static_cast<size_t>(h->rec_stride) * P.nseg * 4,
@@ -1222,7 +1284,7 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
       if (h->opt_latency_graph != 0 && !debug) {
         const uint32_t g = h->lat_graph_flip ^= 1u;
         seq = 0x7ffffff0u + g;  // the record tag baked into graph g
-        if (!h->lat_graph[g]) {
+        if (!graphs[g]) {
           ctl.first_seq = seq;
           io.seq = seq;
           cudaGraph_t graph = nullptr;
@@ -1235,13 +1297,13 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
             throw;
           }
           CUDA_TRY(cudaStreamEndCapture(h->stream, &graph));
-          const cudaError_t ie = cudaGraphInstantiate(&h->lat_graph[g], graph, 0);
+          const cudaError_t ie = cudaGraphInstantiate(&graphs[g], graph, 0);
           cudaGraphDestroy(graph);
           CUDA_TRY(ie);
           --h->launches;  // the capture enqueued nothing
         }
         if (timed) CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
-        CUDA_TRY(cudaGraphLaunch(h->lat_graph[g], h->stream));
+        CUDA_TRY(cudaGraphLaunch(graphs[g], h->stream));
         ++h->launches;
       } else {
         if (timed) CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
@@ -1944,12 +2006,23 @@ qb_status qb_decode(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate,
   return guarded(h, [&] { single_shot(h, syndrome, estimate, residual, converged, iterations, false); });
 }
 
-qb_status qb_latency_run(qb_decoder* h, const uint64_t* pool, uint64_t pool_size,
-                         uint64_t warmup, uint64_t measure, uint64_t* wall_ns,
-                         uint64_t* kernel_ns, uint64_t* digest) {
+qb_status qb_decode_soft(qb_decoder* h, const uint64_t* syndrome, const void* soft,
+                         uint64_t* estimate, uint64_t* residual, uint8_t* converged,
+                         uint32_t* iterations) {
+  if (!h) return QB_INVALID_ARGUMENT;
+  return guarded(h, [&] {
+    if (!soft) fail(QB_INVALID_ARGUMENT, "decode_soft: NULL soft buffer");
+    single_shot(h, syndrome, estimate, residual, converged, iterations, false, soft);
+  });
+}
+
+qb_status qb_latency_run_soft(qb_decoder* h, const uint64_t* pool, const void* soft_pool,
+                              uint64_t pool_size, uint64_t warmup, uint64_t measure,
+                              uint64_t* wall_ns, uint64_t* kernel_ns, uint64_t* digest) {
   if (!h) return QB_INVALID_ARGUMENT;
   return guarded(h, [&] {
     if (!pool || pool_size == 0) fail(QB_INVALID_ARGUMENT, "latency_run: empty pool");
+    const size_t soft_row = static_cast<size_t>(h->P.M) * h->soft_bytes;
     const DecodeParams& P = h->P;
     const size_t sw = P.syn_w32 / 2, ew = P.est_w32 / 2;
     std::vector<uint64_t> est(ew), res(sw);
@@ -1966,7 +2039,9 @@ qb_status qb_latency_run(qb_decoder* h, const uint64_t* pool, uint64_t pool_size
     for (uint64_t b = 0; b < warmup + measure; ++b) {
       const uint64_t* syn = pool + (b % pool_size) * sw;
       const auto t0 = std::chrono::steady_clock::now();
-      single_shot(h, syn, est.data(), res.data(), conv.data(), its.data(), false);
+      const void* soft = soft_pool ? static_cast<const unsigned char*>(soft_pool) + (b % pool_size) * soft_row
+                                   : nullptr;
+      single_shot(h, syn, est.data(), res.data(), conv.data(), its.data(), false, soft);
       const auto t1 = std::chrono::steady_clock::now();
       if (b < warmup) continue;
       const uint64_t k = b - warmup;
@@ -1990,6 +2065,12 @@ qb_status qb_latency_run(qb_decoder* h, const uint64_t* pool, uint64_t pool_size
     }
     if (digest) *digest = hsh;
   });
+}
+
+qb_status qb_latency_run(qb_decoder* h, const uint64_t* pool, uint64_t pool_size,
+                         uint64_t warmup, uint64_t measure, uint64_t* wall_ns,
+                         uint64_t* kernel_ns, uint64_t* digest) {
+  return qb_latency_run_soft(h, pool, nullptr, pool_size, warmup, measure, wall_ns, kernel_ns, digest);
 }
 
 qb_status qb_decode_debug(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate,

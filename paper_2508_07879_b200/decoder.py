@@ -338,6 +338,21 @@ class Decoder:
             raise ValueError("decode_batch_soft: a prior is not finite")
         return soft
 
+    def decode_soft_segments(self, syndrome: np.ndarray, soft: np.ndarray):
+        """qb_decode_soft: one shot through the latency path with per-shot priors."""
+        syndrome = self._check_syndrome(syndrome, None, "decode")
+        soft = self._check_soft(np.asarray(soft)[None, :], 1)[0]
+        est = np.zeros(self._ew, dtype=np.uint64)
+        res = np.zeros(self._sw, dtype=np.uint64)
+        conv = np.zeros(self.num_segments, dtype=np.uint8)
+        its = np.zeros(self.num_segments, dtype=np.uint32)
+        st = self._lib.qb_decode_soft(self._h, _ptr(syndrome, _lib.u64p), soft.ctypes.data,
+                                      _ptr(est, _lib.u64p), _ptr(res, _lib.u64p), _ptr(conv, _lib.u8p),
+                                      _ptr(its, _lib.u32p))
+        if st != _lib.QB_OK:
+            _raise(st, self._h)
+        return est, res, conv, its
+
     def decode_batch_soft_segments(self, syndromes: np.ndarray, soft: np.ndarray,
                                    want_residual: bool = True):
         """qb_decode_batch_soft on host arrays: syndromes (shots, ceil(M/64)) uint64 words and
@@ -377,18 +392,25 @@ class Decoder:
         if st != _lib.QB_OK:
             _raise(st, self._h)
 
-    def latency_run(self, pool: np.ndarray, warmup: int, measure: int):
+    def latency_run(self, pool: np.ndarray, warmup: int, measure: int,
+                    soft_pool: Optional[np.ndarray] = None):
         """qb_latency_run: the reference's run_bench protocol at batch 1
-        (proj/src/bench.cpp:182-337) -> (wall_ns[measure], kernel_ns[measure], digest)."""
+        (proj/src/bench.cpp:182-337) -> (wall_ns[measure], kernel_ns[measure], digest).
+        With `soft_pool` ((n, num_checks) values as decode_batch_soft takes them) every decode
+        is a qb_decode_soft (qb_latency_run_soft)."""
         pool = np.ascontiguousarray(pool, dtype=np.uint64)
         if pool.ndim != 2 or pool.shape[1] != self._sw:
             raise ValueError(f"latency_run: pool must be (n, {self._sw}) uint64 words")
+        soft_ptr = None
+        if soft_pool is not None:
+            soft_pool = self._check_soft(soft_pool, pool.shape[0])
+            soft_ptr = soft_pool.ctypes.data
         wall = np.zeros(measure, dtype=np.uint64)
         kern = np.zeros(measure, dtype=np.uint64)
         digest = C.c_uint64()
-        st = self._lib.qb_latency_run(self._h, _ptr(pool, _lib.u64p), pool.shape[0], warmup,
-                                      measure, _ptr(wall, _lib.u64p), _ptr(kern, _lib.u64p),
-                                      C.byref(digest))
+        st = self._lib.qb_latency_run_soft(self._h, _ptr(pool, _lib.u64p), soft_ptr, pool.shape[0],
+                                           warmup, measure, _ptr(wall, _lib.u64p),
+                                           _ptr(kern, _lib.u64p), C.byref(digest))
         if st != _lib.QB_OK:
             _raise(st, self._h)
         return wall, kern, int(digest.value)

@@ -115,6 +115,18 @@ class Decoder {  // proj/include/qldpc/decoder.hpp:77-108
   std::vector<DecodeOutcome> decode_batch(std::span<const Gf2Vector> syndromes);
   std::uint64_t last_kernel_ns() const;
 
+  /// Soft (noisy) syndromes on a graph [H | I] (extension; include/qldpc_b200.h, "soft
+  /// syndromes"): reliability[m] is this shot's prior (LLR) of the degree-1 measurement-error
+  /// variable soft_vars()[m] of check m; entries of checks without one are ignored.  Equal to a
+  /// reference Decoder built for the shot with priors[soft_vars()[m]] = the value as stored
+  /// (float(prior), or the quantised prior / quant_scale in the integer modes; a value that
+  /// would quantise to 0 is stored as +-1, which the reference would reject).
+  std::vector<std::uint32_t> soft_vars() const;  // 0xffffffff where a check has none
+  DecodeOutcome decode_soft(const Gf2Vector& syndrome, std::span<const double> reliability);
+  /// reliability = [syndromes.size()][num_checks()], row-major.
+  std::vector<DecodeOutcome> decode_batch_soft(std::span<const Gf2Vector> syndromes,
+                                               std::span<const double> reliability);
+
   void set_latency_io(LatencyIo mode);
   void* native_handle() const;  // qb_decoder*
 

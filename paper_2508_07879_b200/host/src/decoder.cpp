@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <bit>
+#include <cmath>
 #include <stdexcept>
 
 #include "qldpc_b200.h"
@@ -131,6 +132,34 @@ struct Decoder::Impl {
   std::vector<std::uint32_t> its;
 
   ~Impl() { qb_decoder_destroy(h); }
+
+  // reliabilities -> the C-ABI's soft format (float, or quantize_saturate as
+  // proj/src/decoder.cpp:500-509 with 0 stored as +-1)
+  std::vector<unsigned char> pack_soft(std::span<const double> rel) const {
+    for (double v : rel) {
+      if (!std::isfinite(v)) throw std::invalid_argument("decode_soft: a reliability is not finite");
+    }
+    std::vector<unsigned char> out;
+    if (cfg.arithmetic == Arithmetic::kFloat || cfg.arithmetic == Arithmetic::kHalf) {
+      out.resize(rel.size() * sizeof(float));
+      float* f = reinterpret_cast<float*>(out.data());
+      for (std::size_t i = 0; i < rel.size(); ++i) f[i] = static_cast<float>(rel[i]);
+      return out;
+    }
+    const bool i8 = cfg.arithmetic == Arithmetic::kInt8;
+    const long long kmax = i8 ? 127 : 32767;
+    const double scale = cfg.quant_scale != 0.0 ? cfg.quant_scale : (i8 ? 8.0 : 256.0);
+    out.resize(rel.size() * (i8 ? 1 : 2));
+    for (std::size_t i = 0; i < rel.size(); ++i) {
+      const double scaled = rel[i] * scale;
+      long long q = std::abs(scaled) >= 1e18 ? (scaled < 0 ? -kmax : kmax) : std::llround(scaled);
+      q = std::clamp(q, -kmax, kmax);
+      if (q == 0) q = std::signbit(scaled) ? -1 : 1;
+      if (i8) reinterpret_cast<std::int8_t*>(out.data())[i] = static_cast<std::int8_t>(q);
+      else reinterpret_cast<std::int16_t*>(out.data())[i] = static_cast<std::int16_t>(q);
+    }
+    return out;
+  }
 
   void run(const Gf2Vector& syndrome) {
     const qb_status st = qb_decode(h, syndrome.words().data(), est.data(), res.data(), conv.data(),
@@ -268,6 +297,73 @@ std::vector<DecodeOutcome> Decoder::decode_batch(std::span<const Gf2Vector> synd
   }
   const qb_status st = qb_decode_batch(I.h, shots, syn.data(), est.data(), res.data(), conv.data(),
                                        its.data());
+  if (st != QB_OK) raise(st, I.h);
+  for (std::size_t i = 0; i < shots; ++i) {
+    assign_bits(out[i].error_estimate, I.n, est.data() + i * ew);
+    assign_bits(out[i].syndrome_residual, I.m, res.data() + i * sw);
+    out[i].converged = true;
+    out[i].iterations_used = 0;
+    for (std::size_t s = 0; s < ns; ++s) {
+      out[i].converged = out[i].converged && conv[i * ns + s] != 0;
+      out[i].iterations_used = std::max<std::size_t>(out[i].iterations_used, its[i * ns + s]);
+    }
+  }
+  return out;
+}
+
+std::vector<std::uint32_t> Decoder::soft_vars() const {
+  std::vector<std::uint32_t> v(impl_->m);
+  const qb_status st = qb_soft_vars(impl_->h, v.data());
+  if (st != QB_OK) raise(st, impl_->h);
+  return v;
+}
+
+DecodeOutcome Decoder::decode_soft(const Gf2Vector& syndrome, std::span<const double> reliability) {
+  Impl& I = *impl_;
+  if (syndrome.size() != I.m || reliability.size() != I.m) {
+    throw std::invalid_argument("decode_soft: syndrome has " + std::to_string(syndrome.size()) +
+                                " bits and " + std::to_string(reliability.size()) +
+                                " reliabilities but the graph has " + std::to_string(I.m) + " checks");
+  }
+  const std::vector<unsigned char> soft = I.pack_soft(reliability);
+  const qb_status st = qb_decode_soft(I.h, syndrome.words().data(), soft.data(), I.est.data(),
+                                      I.res.data(), I.conv.data(), I.its.data());
+  if (st != QB_OK) raise(st, I.h);
+  DecodeOutcome out;
+  assign_bits(out.error_estimate, I.n, I.est.data());
+  assign_bits(out.syndrome_residual, I.m, I.res.data());
+  out.converged = std::all_of(I.conv.begin(), I.conv.end(), [](std::uint8_t c) { return c != 0; });
+  out.iterations_used = *std::max_element(I.its.begin(), I.its.end());
+  return out;
+}
+
+std::vector<DecodeOutcome> Decoder::decode_batch_soft(std::span<const Gf2Vector> syndromes,
+                                                      std::span<const double> reliability) {
+  Impl& I = *impl_;
+  for (std::size_t i = 0; i < syndromes.size(); ++i) {
+    if (syndromes[i].size() != I.m) {
+      throw std::invalid_argument("decode_batch_soft: syndrome " + std::to_string(i) + " has " +
+                                  std::to_string(syndromes[i].size()) +
+                                  " bits but the graph has " + std::to_string(I.m) + " checks");
+    }
+  }
+  if (reliability.size() != syndromes.size() * I.m) {
+    throw std::invalid_argument("decode_batch_soft: expected " + std::to_string(syndromes.size() * I.m) +
+                                " reliabilities, got " + std::to_string(reliability.size()));
+  }
+  const std::size_t shots = syndromes.size(), sw = (I.m + 63) / 64, ew = (I.n + 63) / 64;
+  const std::size_t ns = I.segs.size();
+  std::vector<DecodeOutcome> out(shots);
+  if (shots == 0) return out;
+  const std::vector<unsigned char> soft = I.pack_soft(reliability);
+  std::vector<std::uint64_t> syn(shots * sw), est(shots * ew), res(shots * sw);
+  std::vector<std::uint8_t> conv(shots * ns);
+  std::vector<std::uint32_t> its(shots * ns);
+  for (std::size_t i = 0; i < shots; ++i) {
+    std::copy(syndromes[i].words().begin(), syndromes[i].words().end(), syn.begin() + i * sw);
+  }
+  const qb_status st = qb_decode_batch_soft(I.h, shots, syn.data(), soft.data(), est.data(), res.data(),
+                                            conv.data(), its.data());
   if (st != QB_OK) raise(st, I.h);
   for (std::size_t i = 0; i < shots; ++i) {
     assign_bits(out[i].error_estimate, I.n, est.data() + i * ew);

@@ -3,6 +3,7 @@
 // (oracle/libmsa_oracle.so - test infrastructure, linked here only).  One
 // PASS/FAIL line per check; exit status 1 if any fails.  Style follows
 // proj/tests/acceptance.cpp; checks follow proj/tests/test_decoder.cpp.
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <random>
@@ -241,6 +242,76 @@ int main() {
       }
     }
     report("combined decode equals separate decodes; [[784,24,24]] equals the oracle in every I/O mode", ok);
+  }
+  // 6. soft syndromes (extension): [H | I] extension of bb72, per-shot reliabilities; the
+  //    oracle is one reference-style decoder per shot whose priors carry that shot's values
+  //    as the library stores them (float(prior) / quantised prior / scale)
+  {
+    std::mt19937 gen(83);
+    const std::size_t n = bb72.n, mz = bb72.mz, mx = bb72.mx;
+    std::vector<std::vector<uint32_t>> rows;
+    for (std::size_t r = 0; r < mz; ++r) {
+      std::vector<uint32_t> row;
+      for (uint32_t e = bb72.combined.check_offsets[r]; e < bb72.combined.check_offsets[r + 1]; ++e)
+        row.push_back(bb72.combined.edge_var[e]);
+      row.push_back((uint32_t)(n + r));
+      rows.push_back(row);
+    }
+    for (std::size_t r = 0; r < mx; ++r) {
+      std::vector<uint32_t> row;
+      for (uint32_t e = bb72.combined.check_offsets[mz + r]; e < bb72.combined.check_offsets[mz + r + 1]; ++e)
+        row.push_back(bb72.combined.edge_var[e] + (uint32_t)mz);  // second block sits after the first I
+      row.push_back((uint32_t)(2 * n + mz + r));
+      rows.push_back(row);
+    }
+    const std::size_t M = mz + mx, N = 2 * n + mz + mx;
+    TannerGraph ext = build_tanner_graph(M, N, rows);
+    const std::vector<Segment> segs = {{0, (uint32_t)mz, 0, (uint32_t)(n + mz)},
+                                       {(uint32_t)mz, (uint32_t)M, (uint32_t)(n + mz), (uint32_t)N}};
+    bool ok = true;
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    for (Arithmetic mode : {Arithmetic::kFloat, Arithmetic::kInt8, Arithmetic::kInt16}) {
+      DecoderConfig cfg;
+      cfg.max_iterations = 20;
+      cfg.arithmetic = mode;
+      cfg.priors.assign(N, 5.0);
+      Decoder dec(ext, segs, cfg);
+      const std::vector<uint32_t> sv = dec.soft_vars();
+      for (std::size_t m = 0; m < M; ++m) ok = ok && sv[m] == (m < mz ? n + m : 2 * n + mz + (m - mz));
+      std::vector<Gf2Vector> syn;
+      std::vector<double> rel;
+      for (int i = 0; i < 24; ++i) {
+        syn.push_back(random_syndrome(gen, M, 0.05));
+        for (std::size_t m = 0; m < M; ++m) rel.push_back(std::abs(1.0 + 0.45 * gauss(gen)) * 2.0 / (0.45 * 0.45));
+      }
+      std::vector<DecodeOutcome> batch = dec.decode_batch_soft(syn, rel);
+      const double scale = mode == Arithmetic::kInt8 ? 8.0 : 256.0, kmax = mode == Arithmetic::kInt8 ? 127 : 32767;
+      for (int i = 0; i < 24; ++i) {
+        DecoderConfig shot = cfg;
+        for (std::size_t m = 0; m < M; ++m) {
+          const double v = rel[i * M + m];
+          if (mode == Arithmetic::kFloat) {
+            shot.priors[sv[m]] = static_cast<double>(static_cast<float>(v));
+          } else {
+            double q = std::min(kmax, std::max(-kmax, (double)std::llround(v * scale)));
+            if (q == 0) q = 1;
+            shot.priors[sv[m]] = q / scale;
+          }
+        }
+        const DecodeOutcome want = oracle(ext, segs, shot, syn[i]);
+        ok = ok && same_outcome(batch[i], want);
+        for (LatencyIo io : {LatencyIo::kMapped, LatencyIo::kMemcpy, LatencyIo::kDoorbell}) {
+          dec.set_latency_io(io);
+          ok = ok && same_outcome(dec.decode_soft(syn[i], std::span<const double>(rel).subspan(i * M, M)), want);
+        }
+      }
+      ok = ok && throws_invalid([&] { dec.decode_soft(syn[0], std::span<const double>(rel).subspan(0, 5)); });
+      ok = ok && throws_invalid([&] { dec.decode_batch_soft(syn, std::span<const double>(rel).subspan(0, M)); });
+    }
+    Decoder plain(bb72.combined, bb72.segs, DecoderConfig{});
+    std::vector<double> ones(bb72.combined.num_checks, 1.0);
+    ok = ok && throws_invalid([&] { plain.decode_soft(Gf2Vector(bb72.combined.num_checks), ones); });
+    report("soft syndromes on [H | I]: batch and single-shot (3 I/O modes) equal one oracle decoder per shot", ok);
   }
   std::printf("%s\n", g_failures == 0 ? "ALL PASS" : "SOME FAILED");
   return g_failures == 0 ? 0 : 1;

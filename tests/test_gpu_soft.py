@@ -228,3 +228,41 @@ def test_device_campaigns_on_the_extended_graph(mode):
         assert np.array_equal(swhole, host), (swhole, host)
     finally:
         camp.close()
+
+
+@pytest.mark.parametrize("mode", ["float", "int8", "int16"])
+def test_single_shot_soft_decode_in_every_io_protocol(oracle, mode):
+    """qb_decode_soft: per-shot priors through the single-shot cluster kernel
+    (decode_ell_latency_kernel) with the syndrome in the kernel parameters, by memcpy and by
+    doorbell, interleaved with plain single shots on the same handle; outcomes equal the
+    oracle's per-shot-prior decode and the batch call's."""
+    code, h, g, segs = _ext("bb144")
+    p, mu, sigma = 0.006, 1.0, 0.45
+    rng = np.random.default_rng(19)
+    err, s, llr = _soft_shots(code, h, g, rng, 40, p, mu, sigma)
+    syn = gf2.pack_bits(s)
+    cfg = DecoderConfig(max_iterations=25, arithmetic=mode, priors=_priors(code, p, mu, sigma).tolist())
+    with Decoder(g, cfg, segments=segs) as dec:
+        sv = dec.soft_vars()
+        soft = dec.quantize_soft(llr)
+        want = oracle.decode_many_soft(g, cfg, syn, sv, _dequant(dec, soft), segs)
+        plain = oracle.decode_many(g, cfg, syn, segs)
+        batch = dec.decode_batch_soft_segments(syn, soft)
+        assert all(np.array_equal(a, b) for a, b in zip(batch, want))
+        for io_mode in (0, 1, 2):
+            dec.set_option(1, io_mode)
+            launches = dec.launch_count()
+            for k in range(len(syn)):
+                one = dec.decode_soft_segments(syn[k], soft[k])
+                assert all(np.array_equal(a, b[k]) for a, b in zip(one, want)), (io_mode, k)
+            if io_mode == 2:
+                assert dec.launch_count() - launches <= 2, "doorbell mode must not launch per shot"
+            for k in (0, 5):  # plain single shots in between (the decoder's own priors)
+                one = dec.decode_segments(syn[k])
+                assert all(np.array_equal(a, b[k]) for a, b in zip(one, plain)), (io_mode, k, "plain")
+            one = dec.decode_soft_segments(syn[7], soft[7])
+            assert all(np.array_equal(a, b[7]) for a, b in zip(one, want))
+    with Decoder(codes.make_code("bb72"), DecoderConfig()) as dec:
+        with pytest.raises(ValueError, match="degree-padded"):
+            dec.decode_soft_segments(np.zeros(gf2.num_words(dec.num_checks()), dtype=np.uint64),
+                                     np.ones(dec.num_checks(), dtype=np.float32))
