@@ -141,7 +141,10 @@ typedef enum {
   /* Lean batch kernels ((6,3)-regular codes): 1 (default) = the loader permutes the six
    * message slots inside every check's block so that the variable-side accesses of a
    * warp spread over the shared-memory banks (results are unaffected: the check
-   * update is symmetric in its slots); 0 = slots in row order. */
+   * update is symmetric in its slots); 0 = slots in row order; 2 = as 1, then refined by
+   * simulated annealing (200 moves per edge, fixed seed: ~90 ms per thread shape on
+   * [[784,24,24]], 1.72 -> 1.43 shared-memory wavefronts per variable-side access; for
+   * long campaigns: +2.5 % / +3.5 % on the int8 / half kernels, +0.5-0.8 % on float). */
   QB_OPT_SLOT_SPREAD = 14,
   /* qb_decode_batch (host buffers): shots per pipeline chunk (H2D copy, kernel and D2H
    * copy of consecutive chunks overlap on three streams); 0 = auto (2^15).  Also the

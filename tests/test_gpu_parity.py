@@ -653,3 +653,28 @@ def test_degree_padded_batch_kernel_messages_match_oracle_bitwise(oracle, mode):
             _, _, _, _, oq, orr = oracle.decode(g, cfg, syn1[k], segs)
             assert np.array_equal(_bits(q), _bits(oq)), ("q", k)
             assert np.array_equal(_bits(r), _bits(orr)), ("r", k)
+
+
+@pytest.mark.parametrize("mode", REF_MODES)
+def test_annealed_slot_permutation_leaves_results_unchanged(oracle, mode):
+    """QB_OPT_SLOT_SPREAD = 2 (slot permutation refined by simulated annealing) only moves
+    messages inside their check's block: outcomes and per-edge messages of the batch kernels
+    stay those of the oracle."""
+    code = codes.make_code("bb144")
+    g = code.combined_graph
+    rng = np.random.default_rng(77)
+    _, _, syn1 = error_syndromes(code, rng, 64, 0.03)
+    syn = np.repeat(syn1, 2, axis=0)
+    cfg = DecoderConfig(max_iterations=30, arithmetic=mode)
+    oe, ores, oc, oi = oracle.decode_many(g, cfg, syn1, code.segments)
+    with Decoder(code, cfg) as dec:
+        dec.set_option(14, 2)
+        assert dec.get_option(14) == 2
+        for k in (0, 17, 63):
+            est, res, conv, its, q, r = dec.decode_batch_debug(syn, 2 * k + 1)
+            assert np.array_equal(est[::2], oe) and np.array_equal(res[1::2], ores)
+            assert np.array_equal(its[::2], oi) and np.array_equal(conv[1::2], oc)
+            _, _, _, _, oq, orr = oracle.decode(g, cfg, syn1[k], code.segments)
+            assert np.array_equal(_bits(q), _bits(oq)) and np.array_equal(_bits(r), _bits(orr))
+        with pytest.raises(ValueError):
+            dec.set_option(14, 3)
