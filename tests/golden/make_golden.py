@@ -77,8 +77,50 @@ def graph_fixture(ref, name, graph, cfg_kwargs, syndromes):
     save(name, **out)
 
 
+def soft_fixture(ref, code_name, shots, p, mu, sigma, seed):
+    """Soft (noisy) syndromes on the extended graph diag([Hz | I], [Hx | I]): the reference
+    has priors per Decoder only, so every shot is decoded by its own unmodified reference
+    Decoder whose priors carry that shot's reliabilities (ref_decode_many_soft).  Stored:
+    the syndromes, the reliabilities as doubles AND in each mode's stored form (what the
+    CUDA library is handed), and the reference's outcomes per mode."""
+    from paper_2508_07879_b200 import codes
+    code = codes.make_code(code_name)
+    h, _ = codes.extended_graph(code)
+    g = codes.build_tanner_graph(h)
+    n, mz, mx = code.n, code.hz.rows, code.hx.rows
+    rng = np.random.default_rng(seed)
+    data = np.zeros(g.num_vars, dtype=bool)
+    data[:n] = True
+    data[n + mz:2 * n + mz] = True
+    err = ((rng.random((shots, g.num_vars)) < p) & data[None, :]).astype(np.uint8)
+    lm = (1.0 - 2.0 * h.mat_vec(err)) * mu + sigma * rng.standard_normal((shots, g.num_checks))
+    syn = gf2.pack_bits((lm < 0).astype(np.uint8))
+    llr = 2.0 * mu * np.abs(lm) / sigma ** 2
+    meas = np.concatenate([np.arange(n, n + mz), np.arange(2 * n + mz, 2 * n + mz + mx)]).astype(np.uint32)
+    llr_d = float(np.log((1 - p) / p))
+    rg = ref.graph_from_coo(h.rows, h.cols, h.coo())
+    out = {"code": code_name, "syndromes": syn, "llr": llr, "soft_vars": meas, "p": p, "mu": mu,
+           "sigma": sigma, "prior_data": llr_d, "max_iterations": 30}
+    for mode, scale, kmax in (("float", 0.0, 0), ("int8", 8.0, 127), ("int16", 256.0, 32767)):
+        if mode == "float":
+            stored = llr.astype(np.float32)
+            as_prior = stored.astype(np.float64)
+        else:
+            q = np.clip(np.floor(llr * scale + 0.5), 1, kmax)   # llround of a positive value, 0 -> 1
+            stored = q.astype(np.int8 if mode == "int8" else np.int16)
+            as_prior = q / scale
+        cfg = DecoderConfig(max_iterations=30, arithmetic=mode, priors=[llr_d] * g.num_vars)
+        est, res, conv, its = ref.decode_many_soft(rg, cfg, syn, meas, as_prior)
+        out.update({f"{mode}_soft": stored, f"{mode}_estimate": est, f"{mode}_residual": res,
+                    f"{mode}_converged": conv, f"{mode}_iterations": its})
+    save(f"soft_{code_name}_p{p}", **out)
+
+
 def main():
     ref = Ref()
+    if "--soft-only" in sys.argv:
+        soft_fixture(ref, "bb144", 96, 0.01, 1.0, 0.45, 20260823)
+        return
     # 1. the reference's toy 3x6 fixture, every syndrome (test_decoder.cpp:269-294)
     toy = ref.toy_graph()
     all8 = np.stack([gf2.pack_bits(np.array([(m >> k) & 1 for k in range(3)], dtype=np.uint8))
@@ -102,6 +144,8 @@ def main():
     css_fixture(ref, "bb144", 0.01, 64, 10, False, 1)
     css_fixture(ref, "bb784", 0.01, 48, 50, True, 1)
     css_fixture(ref, "bb784", 0.03, 32, 10, False, 12345)
+    # 3b. soft syndromes: one reference Decoder per shot on [H | I]
+    soft_fixture(ref, "bb144", 96, 0.01, 1.0, 0.45, 20260823)
     # 4. node-operation KATs evaluated by the reference itself
     q = np.array([2.0, -3.0, 1.5])
     save("node_ops",

@@ -266,3 +266,31 @@ def test_single_shot_soft_decode_in_every_io_protocol(oracle, mode):
         with pytest.raises(ValueError, match="degree-padded"):
             dec.decode_soft_segments(np.zeros(gf2.num_words(dec.num_checks()), dtype=np.uint64),
                                      np.ones(dec.num_checks(), dtype=np.float32))
+
+
+@pytest.mark.parametrize("mode", ["float", "int8", "int16"])
+def test_soft_decode_matches_the_golden_fixture_of_the_compiled_reference(mode):
+    """tests/golden/soft_bb144_p0.01.npz holds the outcomes of one UNMODIFIED reference Decoder
+    per shot (generated in the authoring container, tests/golden/make_golden.py): the batch
+    kernel and the single-shot kernel, handed the stored reliabilities, reproduce them."""
+    import os
+    d = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "soft_bb144_p0.01.npz"))
+    code = codes.make_code(str(d["code"]))
+    h, segs = codes.extended_graph(code)
+    g = codes.build_tanner_graph(h)
+    cfg = DecoderConfig(max_iterations=int(d["max_iterations"]), arithmetic=mode,
+                        priors=[float(d["prior_data"])] * g.num_vars)
+    syn, soft = d["syndromes"], d[f"{mode}_soft"]
+    with Decoder(g, cfg, segments=segs) as dec:
+        assert np.array_equal(dec.soft_vars(), d["soft_vars"])
+        assert np.array_equal(dec.quantize_soft(d["llr"]), soft)
+        est, res, conv, its = dec.decode_batch_soft_segments(syn, soft)
+        assert np.array_equal(est, d[f"{mode}_estimate"]) and np.array_equal(res, d[f"{mode}_residual"])
+        assert np.array_equal(conv.min(axis=1), d[f"{mode}_converged"])
+        assert np.array_equal(its.max(axis=1), d[f"{mode}_iterations"])
+        for io_mode in (0, 2):
+            dec.set_option(1, io_mode)
+            for k in range(0, len(syn), 5):
+                e1, r1, c1, i1 = dec.decode_soft_segments(syn[k], soft[k])
+                assert np.array_equal(e1, d[f"{mode}_estimate"][k]) and np.array_equal(r1, d[f"{mode}_residual"][k])
+                assert c1.min() == d[f"{mode}_converged"][k] and i1.max() == d[f"{mode}_iterations"][k]

@@ -243,3 +243,26 @@ def test_per_shot_priors_oracle_equals_one_reference_decoder_per_shot(oracle, re
     # and the per-shot values matter: a constant prior gives different outcomes
     fe, _, _, _ = oracle.decode_many(g, cfg, syn, None, per_segment=False)
     assert not np.array_equal(fe, oe)
+
+
+@pytest.mark.parametrize("mode", ["float", "int8", "int16"])
+def test_oracle_matches_golden_soft_fixture(oracle, mode):
+    """tests/golden/soft_bb144_p0.01.npz: soft syndromes on diag([Hz | I], [Hx | I]), every
+    shot decoded by its own unmodified reference Decoder (priors per Decoder,
+    decoder.hpp:31-32) - the oracle's per-shot-prior entry point reproduces it."""
+    from paper_2508_07879_b200 import DecoderConfig, codes
+    d = np.load(os.path.join(GOLDEN, "soft_bb144_p0.01.npz"))
+    code = codes.make_code(str(d["code"]))
+    h, _ = codes.extended_graph(code)
+    g = codes.build_tanner_graph(h)
+    stored = d[f"{mode}_soft"].astype(np.float64)
+    if mode != "float":
+        stored = stored / (8.0 if mode == "int8" else 256.0)
+    cfg = DecoderConfig(max_iterations=int(d["max_iterations"]), arithmetic=mode,
+                        priors=[float(d["prior_data"])] * g.num_vars)
+    est, res, conv, its = oracle.decode_many_soft(g, cfg, d["syndromes"], d["soft_vars"], stored,
+                                                  None, per_segment=False)
+    assert np.array_equal(est, d[f"{mode}_estimate"]) and np.array_equal(res, d[f"{mode}_residual"])
+    assert np.array_equal(conv[:, 0], d[f"{mode}_converged"])
+    assert np.array_equal(its[:, 0], d[f"{mode}_iterations"])
+    assert 0 < d[f"{mode}_converged"].mean() and d[f"{mode}_iterations"].max() > 3
