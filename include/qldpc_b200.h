@@ -107,7 +107,8 @@ typedef enum {
    * 0 = auto, else one of the instantiations 1, 2, 3, 4, 6, 8, 11 (see kLeanVariants). */
   QB_OPT_BATCH_VARIANT = 5,
   /* Single-shot cluster kernel: 1 or 2 checks (and twice as many variables)
-   * per thread; 0 = auto. */
+   * per thread, 3 = one check and one variable per thread; 0 = auto (3 for float
+   * decoders of small codes, else 1). */
   QB_OPT_LATENCY_NODES_PER_THREAD = 6,
   /* (6,3)-regular kernels: 1 (default) lets uniform-prior decoders use the
    * instantiation with the prior as a kernel constant and (fp32) without the

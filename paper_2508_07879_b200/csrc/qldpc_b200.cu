@@ -499,8 +499,9 @@ KernelFn lean_h2_kernel_tf(int variant) {
 
 template <class A, bool kFast>
 LatKernelFn lean_latency_kernel_tf(int npt) {
-  return npt == 1 ? decode_lean_latency_kernel<A, 1, 2, kFast>
-                  : decode_lean_latency_kernel<A, 2, 4, kFast>;
+  return npt == 3   ? decode_lean_latency_kernel<A, 1, 1, kFast>  // one variable per thread
+         : npt == 1 ? decode_lean_latency_kernel<A, 1, 2, kFast>
+                    : decode_lean_latency_kernel<A, 2, 4, kFast>;
 }
 
 LatKernelFn lean_latency_kernel(int arith, int npt, bool fast) {
@@ -884,9 +885,14 @@ void choose_plans(qb_decoder* h) {
   h->lat_is_ell = false;
   if (h->opt_latency_shape != 1 && P.seg_mmax <= 960 && P.seg_nmax <= 960 * 2 &&
       P.syn_w32 <= kInlineSynWords) {
-    for (int npt : {1, 2}) {
-      if (h->opt_latency_npt && npt != h->opt_latency_npt) continue;
-      const uint32_t T = regular_group_threads(P, npt, 2 * npt);
+    // shape 3 = one check and ONE variable per thread: the shortest dependent chain per
+    // iteration; pays on small codes in float mode ([[144,12,12]]: 4.19 -> 3.62 us for 10
+    // iterations as a 2-CTA cluster of 160 threads, 4.83 -> 4.26 as one CTA of 288), loses on
+    // [[784,24,24]], where it means 25 warps per barrier (6.66 -> 7.10)
+    const bool small_float = h->arith == QB_ARITH_FLOAT && regular_group_threads(P, 1, 1) <= 320;
+    for (int npt : {3, 1, 2}) {
+      if (h->opt_latency_npt ? npt != h->opt_latency_npt : (npt == 3 && !small_float)) continue;
+      const uint32_t T = npt == 3 ? regular_group_threads(P, 1, 1) : regular_group_threads(P, npt, 2 * npt);
       if (T > 1024) continue;
       h->lat_lean_kernel =
           lean_latency_kernel(h->arith, npt, h->fast_ok && h->opt_fast != 0);
@@ -1979,8 +1985,8 @@ qb_status set_option_unchecked(qb_decoder* h, int option, int64_t value) {
         h->opt_fast = value;
         break;
       case QB_OPT_LATENCY_NODES_PER_THREAD:
-        if (value != 0 && value != 1 && value != 2) {
-          fail(QB_INVALID_ARGUMENT, "QB_OPT_LATENCY_NODES_PER_THREAD: 0, 1 or 2");
+        if (value < 0 || value > 3) {
+          fail(QB_INVALID_ARGUMENT, "QB_OPT_LATENCY_NODES_PER_THREAD: 0, 1, 2 or 3");
         }
         h->opt_latency_npt = value;
         break;

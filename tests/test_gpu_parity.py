@@ -329,7 +329,7 @@ def test_regular_and_cluster_kernels_match_oracle(oracle, name, mode):
             for shape in (1, 2):
                 dec.set_option(OPT_LATENCY_SHAPE, shape)
                 assert dec.get_option(INFO_LATENCY_CLUSTER) == (1 if shape == 2 else 0)
-                for npt in (1, 2):
+                for npt in (1, 2, 3):
                     dec.set_option(OPT_LATENCY_NPT, npt)
                     assert_matches_oracle(oracle, g, cfg, syn[:6], code.segments, dec=dec,
                                           messages=True)
