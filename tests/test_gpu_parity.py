@@ -678,3 +678,32 @@ def test_annealed_slot_permutation_leaves_results_unchanged(oracle, mode):
             assert np.array_equal(_bits(q), _bits(oq)) and np.array_equal(_bits(r), _bits(orr))
         with pytest.raises(ValueError):
             dec.set_option(14, 3)
+
+
+@pytest.mark.parametrize("l,m,lean", [(32, 30, True), (31, 32, False)])
+def test_largest_segments_of_the_regular_kernels_and_the_first_size_beyond(oracle, l, m, lean):
+    """Maximum sizes: 960 checks per segment is the largest graph the (6,3)-regular item and
+    cluster kernels take (message blocks of one segment in one CTA's shared memory, syndrome
+    in the kernel parameters); one size up (992) the generic CSR kernel must take over.  Both
+    decode a batch and single shots exactly as the oracle, float and int8."""
+    code = codes.build_bb_code(l, m, [(3, 0), (0, 1), (0, 2)], [(0, 3), (1, 0), (2, 0)], f"bb{2 * l * m}")
+    g = code.combined_graph
+    assert g.num_checks == 2 * l * m
+    rng = np.random.default_rng(l * m)
+    _, _, syn = error_syndromes(code, rng, 40, 0.01)
+    for mode in ("float", "int8"):
+        cfg = DecoderConfig(max_iterations=20, arithmetic=mode)
+        oe, ores, oc, oi = oracle.decode_many(g, cfg, syn, code.segments)
+        with Decoder(code, cfg) as dec:
+            assert dec.get_option(INFO_BATCH_REGULAR) == (1 if lean else 0)
+            assert dec.get_option(INFO_LATENCY_LEAN) == (1 if lean else 0)
+            est, res, conv, its = dec.decode_batch_segments(syn)
+            assert np.array_equal(est, oe) and np.array_equal(res, ores)
+            assert np.array_equal(conv, oc) and np.array_equal(its, oi)
+            for io_mode in ((0, 1, 2) if lean else (0, 1)):
+                dec.set_option(OPT_LATENCY_IO, io_mode)
+                for k in (0, 13, 39):
+                    e1, r1, c1, i1 = dec.decode_segments(syn[k])
+                    assert np.array_equal(e1, oe[k]) and np.array_equal(r1, ores[k])
+                    assert np.array_equal(c1, oc[k]) and np.array_equal(i1, oi[k])
+    assert oi.max() > 2 and oc.min() in (0, 1)
