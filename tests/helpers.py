@@ -68,3 +68,25 @@ def skip_sampler_flips(seed: int, trial: int, p: float, num_vars: int) -> list:
         if not pos < num_vars:
             return out
         out.append(int(pos))
+
+
+def random_regular63_matrix(rng: np.random.Generator, checks: int) -> codes.SparseMatrix:
+    """Random (6,3)-regular parity-check matrix with `checks` rows and 2 * checks columns and no
+    repeated entry (configuration model + repair swaps): a graph with the degrees of the
+    bivariate-bicycle codes but none of their structure."""
+    n = 2 * checks
+    stubs = np.repeat(np.arange(n), 3)
+    rng.shuffle(stubs)
+    rows = stubs.reshape(checks, 6)
+    for _ in range(10000):
+        bad = [m for m in range(checks) if len(set(rows[m].tolist())) < 6]
+        if not bad:
+            break
+        for m in bad:
+            vals = rows[m].tolist()
+            j = next(k for k in range(6) if vals.count(vals[k]) > 1)
+            m2, j2 = int(rng.integers(0, checks)), int(rng.integers(0, 6))
+            rows[m, j], rows[m2, j2] = rows[m2, j2], rows[m, j]
+    else:
+        raise RuntimeError("could not repair the configuration-model graph")
+    return codes.SparseMatrix.from_rows(checks, n, [sorted(r.tolist()) for r in rows])

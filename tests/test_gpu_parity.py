@@ -9,7 +9,7 @@ import pytest
 
 from paper_2508_07879_b200 import (Decoder, DecoderConfig, codes, decode, decode_batch,
                                    decode_css, gf2)
-from tests.helpers import (error_syndromes, random_ldpc_matrix, random_syndrome,
+from tests.helpers import (error_syndromes, random_ldpc_matrix, random_regular63_matrix, random_syndrome,
                            random_syndromes)
 
 pytestmark = pytest.mark.gpu
@@ -707,3 +707,34 @@ def test_largest_segments_of_the_regular_kernels_and_the_first_size_beyond(oracl
                     assert np.array_equal(e1, oe[k]) and np.array_equal(r1, ores[k])
                     assert np.array_equal(c1, oc[k]) and np.array_equal(i1, oi[k])
     assert oi.max() > 2 and oc.min() in (0, 1)
+
+
+@pytest.mark.parametrize("mode", REF_MODES)
+def test_unstructured_regular_graphs_on_the_regular_kernels(oracle, mode):
+    """The (6,3)-regular kernels assume the degrees, not the bivariate-bicycle structure: random
+    regular graphs (one segment, and two different graphs as two segments of unequal size) go
+    through the item kernel, its slot permutation and the cluster kernel, and decode as the
+    oracle does - outcomes and, for one shot of the batch, every edge message."""
+    rng = np.random.default_rng(20260824)
+    h1 = random_regular63_matrix(rng, 100)
+    h2 = random_regular63_matrix(rng, 61)
+    both = codes.block_diag(h1, h2)
+    cases = [(h1, None), (both, np.array([[0, 100, 0, 200], [100, 161, 200, 322]], dtype=np.uint32))]
+    for h, segs in cases:
+        g = codes.build_tanner_graph(h)
+        err = (rng.random((33, g.num_vars)) < 0.03).astype(np.uint8)
+        syn1 = gf2.pack_bits(h.mat_vec(err))
+        syn = np.repeat(syn1, 2, axis=0)  # both lanes of a packed pair stop together
+        for iters, early in ((25, True), (6, False)):
+            cfg = DecoderConfig(max_iterations=iters, early_termination=early, arithmetic=mode)
+            oe, ores, oc, oi = oracle.decode_many(g, cfg, syn1, segs)
+            with Decoder(g, cfg, segments=segs) as dec:
+                assert dec.get_option(INFO_BATCH_REGULAR) == 1 and dec.get_option(INFO_LATENCY_LEAN) == 1
+                for spread in (0, 1, 2):
+                    dec.set_option(14, spread)
+                    est, res, conv, its, q, r = dec.decode_batch_debug(syn, 2 * 17 + 1)
+                    assert np.array_equal(est[::2], oe) and np.array_equal(res[1::2], ores)
+                    assert np.array_equal(conv[::2], oc) and np.array_equal(its[1::2], oi)
+                    _, _, _, _, oq, orr = oracle.decode(g, cfg, syn1[17], segs)
+                    assert np.array_equal(_bits(q), _bits(oq)) and np.array_equal(_bits(r), _bits(orr))
+                assert_matches_oracle(oracle, g, cfg, syn1[:5], segs, dec=dec, messages=True)
