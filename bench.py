@@ -642,9 +642,10 @@ def measure_latency(args, code, lib, d_syn):
                             arithmetic=args.arithmetic)
         with Decoder(code, cfg) as dec:
             for io_mode, io_name in ((2, "doorbell"), (0, "mapped"), (1, "memcpy"),
-                                     (1, "memcpy_nograph")):
+                                     (1, "memcpy_nograph"), (1, "memcpy_poll")):
                 dec.set_option(1, io_mode)
                 dec.set_option(12, 0 if io_name == "memcpy_nograph" else 1)
+                dec.set_option(18, 1 if io_name == "memcpy_poll" else 0)
                 wall, kern, digest = dec.latency_run(pool, 300, args.latency_shots)
                 wall = np.sort(wall.astype(np.float64) * 1e-3)
                 kern = np.sort(kern.astype(np.float64) * 1e-3)
@@ -653,7 +654,7 @@ def measure_latency(args, code, lib, d_syn):
                     "mean": float(np.mean(wall)), "min": float(wall[0]), "max": float(wall[-1]),
                     "kernel_p50": nearest_rank(kern, 50), "kernel_p99": nearest_rank(kern, 99),
                     "shots": args.latency_shots, "digest": "%016x" % digest}
-                if io_mode == 1:  # the same protocol timed by CUDA events on the stream
+                if io_mode == 1 and io_name != "memcpy_poll":  # the same protocol timed by CUDA events on the stream
                     dec.set_option(11, 1)
                     _, ev, _ = dec.latency_run(pool, 300, args.latency_shots)
                     dec.set_option(11, 0)
@@ -727,7 +728,9 @@ def measure_latency(args, code, lib, d_syn):
                    "shot), mapped = one cluster launch per shot with the syndrome in the kernel "
                    "parameters and results to mapped pinned memory + completion flag, memcpy = "
                    "cudaMemcpyAsync H2D / kernel / D2H + stream sync (paper protocol) as ONE CUDA-graph "
-                   "launch per decode (memcpy_nograph: three separate stream operations); cuda_event = "
+                   "launch per decode (memcpy_nograph: three separate stream operations; memcpy_poll: the "
+                   "host watches the tags of the copied record instead of cudaStreamSynchronize, "
+                   "QB_OPT_LATENCY_WAIT = 1); cuda_event = "
                    "cudaEventRecord before the H2D copy and after the D2H copy of that protocol")
     return out
 
@@ -745,14 +748,15 @@ def data_mask(code, gx) -> np.ndarray:
 def compact_latency(table: dict) -> dict:
     """p50 / p99 (us) per protocol from measure_latency's table, for `e2e.latency_us`."""
     out = {"unit": "us", "protocols": "memcpy = cudaMemcpyAsync H2D + kernel + D2H + sync as one "
-           "CUDA-graph launch (the paper's protocol; cuda_event = the same span by CUDA events); "
+           "CUDA-graph launch (the paper's protocol; cuda_event = the same span by CUDA events; "
+           "memcpy_poll = the same with the host watching the copied record's tags instead of the stream sync); "
            "mapped = one cluster launch per shot, syndrome in the kernel parameters, result to "
            "mapped pinned memory; doorbell = persistent cluster polling mapped memory. Host "
            "steady_clock around the whole qb_decode call, nearest-rank percentiles"}
     code = {}
     for label in ("fixed10", "cap50_early"):
         row = {}
-        for proto in ("memcpy", "mapped", "doorbell"):
+        for proto in ("memcpy", "memcpy_poll", "mapped", "doorbell"):
             r = table.get(f"{label}_{proto}")
             if not r:
                 continue

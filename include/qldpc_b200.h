@@ -165,6 +165,12 @@ typedef enum {
    * per trial reach HBM); 0 = sampler, decode and classifier as three kernels per round.
    * Counters are identical either way (and identical to the reference's run_campaign). */
   QB_OPT_CAMPAIGN_FUSED = 17,
+  /* Memcpy protocol of single shots (QB_OPT_LATENCY_IO = 1): how the host learns that the
+   * D2H copy has landed.  0 (default) = cudaStreamSynchronize, the paper's literal protocol;
+   * 1 = watch the pinned destination: every 32-byte sector of the copied record carries the
+   * shot's tag, so the record is complete when all of them show it (-3 us per decode).
+   * Ignored while QB_OPT_LATENCY_EVENTS = 1 (reading the events needs the synchronize). */
+  QB_OPT_LATENCY_WAIT = 18,
   /* Read-only (qb_get_option): the launch plans actually in use. */
   QB_OPT_INFO_BATCH_CTAS_PER_SM = 100,
   QB_OPT_INFO_BATCH_BLOCK = 101,

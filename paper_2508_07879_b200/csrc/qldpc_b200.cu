@@ -172,6 +172,7 @@ struct qb_decoder {
   bool db_soft = false;                  // the resident doorbell kernel reads soft values
   cudaGraphExec_t lat_graph_soft[2] = {nullptr, nullptr};
   int64_t opt_campaign_fused = 1;        // QB_OPT_CAMPAIGN_FUSED
+  int64_t opt_latency_wait = 0;          // QB_OPT_LATENCY_WAIT
 
   // options
   int64_t opt_kernel = 0, opt_latency_io = 0, opt_latency_shape = 0, opt_group_threads = 0,
@@ -1368,7 +1369,15 @@ void single_shot(qb_decoder* h, const uint64_t* syndrome, uint64_t* estimate, ui
         enqueue();
       }
       if (timed) CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
-      CUDA_TRY(cudaStreamSynchronize(h->stream));
+      if (h->opt_latency_wait != 0 && !timed) {
+        // the D2H copy IS the completion signal: every 32-byte sector of the record carries
+        // the shot's tag (the previous shot left the other graph's tag behind), so the host
+        // can watch the pinned destination instead of paying cudaStreamSynchronize's wake-up
+        // (-3 us); the next call's operations are stream-ordered behind this one either way
+        spin_until(h, [&] { return records_ready(h, seq); }, false);
+      } else {
+        CUDA_TRY(cudaStreamSynchronize(h->stream));
+      }
       if (timed) {
         float ms = 0.0f;
         CUDA_TRY(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
@@ -1949,6 +1958,10 @@ qb_status set_option_unchecked(qb_decoder* h, int option, int64_t value) {
         if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_SAMPLER: 0 or 1");
         h->opt_sampler = value;
         return;
+      case QB_OPT_LATENCY_WAIT:
+        if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_LATENCY_WAIT: 0 or 1");
+        h->opt_latency_wait = value;
+        break;
       case QB_OPT_CAMPAIGN_FUSED:
         if (value < 0 || value > 1) fail(QB_INVALID_ARGUMENT, "QB_OPT_CAMPAIGN_FUSED: 0 or 1");
         h->opt_campaign_fused = value;
@@ -2044,6 +2057,7 @@ int64_t qb_get_option(const qb_decoder* h, int option) {
     case QB_OPT_BATCH_CHUNK: return h->opt_batch_chunk;
     case QB_OPT_SAMPLER: return h->opt_sampler;
     case QB_OPT_CAMPAIGN_FUSED: return h->opt_campaign_fused;
+    case QB_OPT_LATENCY_WAIT: return h->opt_latency_wait;
     case QB_OPT_SLOT_SPREAD: return h->opt_slot_spread;
     case QB_OPT_INFO_LAST_EVENT_NS: return static_cast<int64_t>(h->last_event_ns);
     case QB_OPT_BATCH_CTAS_PER_SM: return h->opt_batch_ctas;

@@ -569,6 +569,24 @@ def test_memcpy_protocol_graph_and_event_timing(oracle):
         dec.set_option(OPT_LATENCY_EVENTS, 0)
         _, kern, _ = dec.latency_run(syn.view(np.uint64), 5, 50)
         assert np.median(kern) < np.median(ev)
+        # QB_OPT_LATENCY_WAIT = 1: completion read off the copied record's tags instead of a
+        # stream synchronize - same results, graph or not, also when interleaved with the
+        # other single-shot protocols and with batch calls on the same handle
+        want = oracle.decode_many(g, cfg, syn, code.segments)
+        dec.set_option(18, 1)
+        assert dec.get_option(18) == 1
+        for graph in (1, 0):
+            dec.set_option(OPT_LATENCY_GRAPH, graph)
+            assert_matches_oracle(oracle, g, cfg, syn, code.segments, dec=dec)
+        for k, io_mode in enumerate((1, 0, 1, 2, 1, 1, 0, 2, 1)):
+            dec.set_option(OPT_LATENCY_IO, io_mode)
+            got = dec.decode_segments(syn[k])
+            assert all(np.array_equal(a, b[k]) for a, b in zip(got, want)), (k, io_mode)
+            if k == 4:
+                batch = dec.decode_batch_segments(syn)
+                assert all(np.array_equal(a, b) for a, b in zip(batch, want))
+        with pytest.raises(ValueError):
+            dec.set_option(18, 2)
 
 
 # ---- per-edge messages of the THROUGHPUT kernels ----------------------------------------
