@@ -626,6 +626,29 @@ def measure_e2e(args, dec, lib, d_syn, shots, sw, ew, nseg):
            "gpu_launches_per_step": (dec.launch_count() - l0) // (2 + len(times))}
     for p in (h_syn, h_est, h_conv, h_its):
         lib.qb_host_free(p)
+    # what the host link of this box delivers (pinned, 64 MiB per copy, one direction at a
+    # time): the e2e rate needs d2h_bytes_per_step / step time of it in the D2H direction
+    try:
+        nb = 64 << 20
+        hbuf = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+        dbuf = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        link = {}
+        for name, dst, src in (("h2d_gbs", dbuf, hbuf), ("d2h_gbs", hbuf, dbuf)):
+            dst.copy_(src, non_blocking=True)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(4):
+                dst.copy_(src, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            link[name] = 4 * nb / (e0.elapsed_time(e1) * 1e-3) / 1e9
+        link["d2h_needed_gbs"] = out["d2h_bytes_per_step"] / dt / 1e9
+        link["h2d_needed_gbs"] = out["h2d_bytes_per_step"] / dt / 1e9
+        link["note"] = "measured pinned-memory copy rates of this box beside what the e2e rate moves"
+        out["host_link"] = link
+    except Exception as exc:  # the measurement is explanatory only
+        out["host_link"] = {"error": str(exc)}
     return out
 
 
