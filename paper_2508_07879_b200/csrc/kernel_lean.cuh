@@ -726,7 +726,15 @@ decode_lean_kernel(const __grid_constant__ DecodeParams P, const __grid_constant
         }
       } else {
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) cn6_block(P, A{}, msgs + co[k], (synbits >> k) & 1u);
+        for (int k = 0; k < CPT; ++k) {
+          // warps whose 32 slots of the LAST round lie beyond the segment's checks skip it
+          // (T * CPT covers up to 1.2 Ms + 96 slots: on [[784,24,24]] two of five warps; the
+          // branch is uniform per warp).  +2 % (float) / +5 % (int16) at 10 fixed iterations;
+          // the same test on the last round of the variable stage made things slower.
+          if (k + 1 < CPT || (tid & ~31u) + static_cast<uint32_t>(CPT - 1) * T < Ms) {
+            cn6_block(P, A{}, msgs + co[k], (synbits >> k) & 1u);
+          }
+        }
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < VPT; ++k) {
