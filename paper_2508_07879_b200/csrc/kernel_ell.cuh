@@ -542,13 +542,16 @@ decode_ell_kernel(const __grid_constant__ DecodeParams P, const __grid_constant_
       uint32_t achg = 0;
 #pragma unroll
       for (int k = 0; k < CPT; ++k) {
-        cn_ell<DC>(P, A{}, msgs + co[k], (synbits >> k) & 1u);
-        const uint32_t aslot = (absorb >> (8 * k)) & 0xffu;
-        if (aslot != kNoAbsorb) {  // posterior of the absorbed variable from the r just produced
-          const unsigned char* slot = msgs + co[k] + aslot * kMsg;
-          const uint32_t e = absorbed_decision(A{}, *reinterpret_cast<const Msg*>(slot),
-                                               *reinterpret_cast<const Msg*>(slot + DC * kMsg));
-          achg |= (e ^ ((aprev >> k) & 1u)) << k;  // it flips the parity of its one check
+        // (warps without a check in the last round skip it, as in decode_lean_kernel)
+        if (k + 1 < CPT || (tid & ~31u) + static_cast<uint32_t>(CPT - 1) * T < Ms) {
+          cn_ell<DC>(P, A{}, msgs + co[k], (synbits >> k) & 1u);
+          const uint32_t aslot = (absorb >> (8 * k)) & 0xffu;
+          if (aslot != kNoAbsorb) {  // posterior of the absorbed variable from the r just produced
+            const unsigned char* slot = msgs + co[k] + aslot * kMsg;
+            const uint32_t e = absorbed_decision(A{}, *reinterpret_cast<const Msg*>(slot),
+                                                 *reinterpret_cast<const Msg*>(slot + DC * kMsg));
+            achg |= (e ^ ((aprev >> k) & 1u)) << k;  // it flips the parity of its one check
+          }
         }
       }
       aprev ^= achg;

@@ -320,14 +320,17 @@ decode_ell_h2_kernel(const __grid_constant__ DecodeParams P, const __grid_consta
       uint32_t achg_a = 0, achg_b = 0;
 #pragma unroll
       for (int k = 0; k < CPT; ++k) {
-        cn_ell_h2<DC, kI8>(P, msgs + co[k], synpair[k]);
-        const uint32_t aslot = (absorb >> (8 * k)) & 0xffu;
-        if (aslot != kNoAbsorb) {  // posteriors of the absorbed variable from the r just produced
-          const unsigned char* slot = msgs + co[k] + aslot * kMsg;
-          const uint32_t sg = h22u(__hadd2(*reinterpret_cast<const __half2*>(slot),
-                                           *reinterpret_cast<const __half2*>(slot + DC * kMsg)));
-          achg_a |= (((sg >> 15) & 1u) ^ ((aprev_a >> k) & 1u)) << k;
-          achg_b |= ((sg >> 31) ^ ((aprev_b >> k) & 1u)) << k;
+        // (warps without a check in the last round skip it, as in decode_lean_kernel)
+        if (k + 1 < CPT || (tid & ~31u) + static_cast<uint32_t>(CPT - 1) * T < Ms) {
+          cn_ell_h2<DC, kI8>(P, msgs + co[k], synpair[k]);
+          const uint32_t aslot = (absorb >> (8 * k)) & 0xffu;
+          if (aslot != kNoAbsorb) {  // posteriors of the absorbed variable from the r just produced
+            const unsigned char* slot = msgs + co[k] + aslot * kMsg;
+            const uint32_t sg = h22u(__hadd2(*reinterpret_cast<const __half2*>(slot),
+                                             *reinterpret_cast<const __half2*>(slot + DC * kMsg)));
+            achg_a |= (((sg >> 15) & 1u) ^ ((aprev_a >> k) & 1u)) << k;
+            achg_b |= ((sg >> 31) ^ ((aprev_b >> k) & 1u)) << k;
+          }
         }
       }
       if (!live_a) achg_a = 0;
