@@ -756,3 +756,48 @@ def test_unstructured_regular_graphs_on_the_regular_kernels(oracle, mode):
                     _, _, _, _, oq, orr = oracle.decode(g, cfg, syn1[17], segs)
                     assert np.array_equal(_bits(q), _bits(oq)) and np.array_equal(_bits(r), _bits(orr))
                 assert_matches_oracle(oracle, g, cfg, syn1[:5], segs, dec=dec, messages=True)
+
+
+@pytest.mark.parametrize("mode", REF_MODES)
+@pytest.mark.parametrize("alpha", [1.0, 0.5])
+def test_exact_zeros_ties_and_signed_zero_messages(oracle, mode, alpha):
+    """Zeros and ties in the check update (proj/tests/test_decoder.cpp:207-221 tests the
+    reference's two-minimum trick on them): with alpha a power of two and small integer
+    priors of both signs the sums cancel exactly, so messages of +0.0 / -0.0 / 0 and tied
+    minima occur at once.  Outcomes and every edge message (bit patterns: the sign of a zero
+    included) must equal the oracle's - single-shot kernels, batch kernels, and the generic
+    CSR kernel."""
+    rng = np.random.default_rng(97)
+    code = codes.make_code("bb72")
+    cases = [(code.combined_graph, code.segments, 24),
+             (codes.build_tanner_graph(codes.toy_code_3x6()), None, 8),
+             (codes.build_tanner_graph(random_ldpc_matrix(rng, 9, 16)), None, 16)]
+    zeros_seen = 0
+    for g, segs, shots in cases:
+        pri = rng.choice(np.array([-2.0, -1.0, 1.0, 1.0, 2.0, 3.0]), size=g.num_vars)
+        syn = gf2.pack_bits((rng.random((shots, g.num_checks)) < 0.3).astype(np.uint8))
+        for iters, early in ((9, True), (6, False)):
+            cfg = DecoderConfig(max_iterations=iters, early_termination=early, alpha=alpha,
+                                arithmetic=mode, priors=pri.tolist(),
+                                quant_scale=0.0 if mode == "float" else 1.0)
+            with Decoder(g, cfg, segments=segs) as dec:
+                assert_matches_oracle(oracle, g, cfg, syn, segs, dec=dec, messages=True)
+                dec.set_option(0, 1)  # the generic kernel, same handle
+                assert_matches_oracle(oracle, g, cfg, syn[:4], segs, dec=dec, messages=True)
+                dec.set_option(0, 0)
+                oe, ores, oc, oi = oracle.decode_many(g, cfg, syn, segs)
+                est, res, conv, its = dec.decode_batch_segments(syn)
+                assert np.array_equal(est, oe) and np.array_equal(res, ores)
+                assert np.array_equal(conv, oc) and np.array_equal(its, oi)
+                if dec.get_option(INFO_BATCH_REGULAR) == 1:
+                    # the regular batch kernels' own messages, general-prior instantiations
+                    # (pairs of identical shots: both lanes of a packed pair stop together)
+                    syn2 = np.repeat(syn, 2, axis=0)
+                    for k in (0, 5):
+                        q, r = dec.decode_batch_debug(syn2, 2 * k + 1)[4:]
+                        _, _, _, _, oq, orr = oracle.decode(g, cfg, syn[k], segs)
+                        assert np.array_equal(_bits(q), _bits(oq)) and np.array_equal(_bits(r), _bits(orr))
+            for s in syn[:6]:
+                _, _, _, _, oq, orr = oracle.decode(g, cfg, s, segs)
+                zeros_seen += int((np.asarray(oq) == 0).sum() + (np.asarray(orr) == 0).sum())
+    assert zeros_seen > 0, "the construction must produce zero messages"
