@@ -801,3 +801,42 @@ def test_exact_zeros_ties_and_signed_zero_messages(oracle, mode, alpha):
                 _, _, _, _, oq, orr = oracle.decode(g, cfg, s, segs)
                 zeros_seen += int((np.asarray(oq) == 0).sum() + (np.asarray(orr) == 0).sum())
     assert zeros_seen > 0, "the construction must produce zero messages"
+
+
+@pytest.mark.parametrize("mode", REF_MODES)
+@pytest.mark.parametrize("alpha", [0.5, 1.0, 0.25])
+def test_uniform_prior_fast_paths_with_zero_messages(oracle, mode, alpha):
+    """The uniform-prior instantiations (first iteration by table / from the syndrome) when
+    the arithmetic produces exact zeros: gamma = 1 and alpha = 0.5 give q = 0.5 - 0.5 = +0.0
+    already in the first iteration, whose magnitude then wins every minimum and whose sign
+    travels through the products.  Batch kernels (messages of selected shots) and single-shot
+    kernels against the oracle, bit patterns included."""
+    code = codes.make_code("bb144")
+    g = code.combined_graph
+    rng = np.random.default_rng(int(alpha * 100))
+    _, _, syn1 = error_syndromes(code, rng, 48, 0.04)
+    syn = np.repeat(syn1, 2, axis=0)
+    for iters, early in ((12, True), (5, False)):
+        cfg = DecoderConfig(max_iterations=iters, early_termination=early, alpha=alpha, arithmetic=mode,
+                            quant_scale=0.0 if mode == "float" else 2.0)
+        oe, ores, oc, oi = oracle.decode_many(g, cfg, syn1, code.segments)
+        with Decoder(code, cfg) as dec:
+            for k in (0, 7, 30, 47):
+                est, res, conv, its, q, r = dec.decode_batch_debug(syn, 2 * k)
+                assert np.array_equal(est[::2], oe) and np.array_equal(res[1::2], ores)
+                assert np.array_equal(conv[::2], oc) and np.array_equal(its[1::2], oi)
+                _, _, _, _, oq, orr = oracle.decode(g, cfg, syn1[k], code.segments)
+                assert np.array_equal(_bits(q), _bits(oq)), (k, "q")
+                assert np.array_equal(_bits(r), _bits(orr)), (k, "r")
+            assert_matches_oracle(oracle, g, cfg, syn1[:8], code.segments, dec=dec, messages=True)
+    if alpha == 0.5:  # after the first iteration a variable with two unsatisfied checks sends 0
+        one = DecoderConfig(max_iterations=1, early_termination=False, alpha=alpha, arithmetic=mode,
+                            quant_scale=0.0 if mode == "float" else 2.0)
+        zeros = 0
+        with Decoder(code, one) as dec:
+            for k in range(12):
+                _, _, _, _, oq, _ = oracle.decode(g, one, syn1[k], code.segments)
+                zeros += int((np.asarray(oq) == 0).sum())
+                q = dec.decode_batch_debug(syn, 2 * k + 1)[4]
+                assert np.array_equal(_bits(q), _bits(oq))
+        assert zeros > 0, "alpha = 0.5 must produce zero messages in the first iteration"
