@@ -41,6 +41,74 @@ namespace {
 
 thread_local std::string g_create_error;
 
+// Pinned (mapped) host memory is slow to allocate and free (1.5 - 2 ms per call) and the
+// reference's usage constructs decoders freely (one per decode() call, decoder.cpp:598-602):
+// every handle takes ONE slab for its four small staging buffers, and slabs of destroyed
+// handles wait in a process-wide free list for the next handle on that device.
+struct PinnedSlab {
+  void* p;
+  size_t bytes;
+  int device;
+};
+std::mutex g_slab_mu;
+std::vector<PinnedSlab> g_slabs;
+constexpr size_t kMaxIdleSlabs = 16;
+
+void* slab_acquire(size_t bytes, int device, size_t* got) {
+  {
+    std::lock_guard<std::mutex> lk(g_slab_mu);
+    for (size_t i = 0; i < g_slabs.size(); ++i) {
+      if (g_slabs[i].device == device && g_slabs[i].bytes >= bytes && g_slabs[i].bytes <= 4 * bytes + 4096) {
+        const PinnedSlab sl = g_slabs[i];
+        g_slabs.erase(g_slabs.begin() + static_cast<long>(i));
+        *got = sl.bytes;
+        return sl.p;
+      }
+    }
+  }
+  const size_t want = (bytes + 4095) & ~static_cast<size_t>(4095);
+  void* p = nullptr;
+  const cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocMapped);
+  if (e != cudaSuccess) return nullptr;
+  *got = want;
+  return p;
+}
+
+void slab_release(void* p, size_t bytes, int device) {
+  if (!p) return;
+  {
+    std::lock_guard<std::mutex> lk(g_slab_mu);
+    if (g_slabs.size() < kMaxIdleSlabs) {
+      g_slabs.push_back({p, bytes, device});
+      return;
+    }
+  }
+  cudaFreeHost(p);
+}
+
+// cudaGetDeviceProperties costs milliseconds; the two fields the loader needs do not change
+bool device_limits(int device, int* sm_count, int* smem_optin) {
+  static std::mutex mu;
+  static std::vector<std::array<int, 3>> seen;  // {device, sm_count, smem_optin}
+  std::lock_guard<std::mutex> lk(mu);
+  for (const auto& d : seen) {
+    if (d[0] == device) {
+      *sm_count = d[1];
+      *smem_optin = d[2];
+      return true;
+    }
+  }
+  int sm = 0, optin = 0;
+  if (cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess) {
+    return false;
+  }
+  seen.push_back({device, sm, optin});
+  *sm_count = sm;
+  *smem_optin = optin;
+  return true;
+}
+
 struct StatusError {
   qb_status code;
   std::string msg;
@@ -204,6 +272,8 @@ struct qb_decoder {
   uint32_t lat_graph_flip = 0;
   bool regular63 = false;  // every check degree 6, every variable degree 3
   uint32_t max_dc = 0, max_dv = 0;  // largest check / variable degree of the graph
+  void* h_slab = nullptr;          // the pinned slab behind h_in / h_out / h_db / h_rec
+  size_t h_slab_bytes = 0;
   uint8_t* d_edge_slot = nullptr;  // [E] slot permutation of the lean batch kernels
   int64_t slot_table_for = -1;     // ... computed for this thread count (0 = natural order)
   std::vector<uint32_t> h_var_edges, h_check_off;  // host copies for the slot optimiser
@@ -273,11 +343,8 @@ void destroy(qb_decoder* h) {
   cudaFree(h->d_tcol);
   cudaFree(h->d_soft1_dev);
   if (h->h_soft1) cudaFreeHost(h->h_soft1);
-  if (h->h_db) cudaFreeHost(h->h_db);
-  if (h->h_rec) cudaFreeHost(h->h_rec);
   cudaFree(h->d_rec_dev);
-  if (h->h_in) cudaFreeHost(h->h_in);
-  if (h->h_out) cudaFreeHost(h->h_out);
+  slab_release(h->h_slab, h->h_slab_bytes, h->device);  // h_in, h_out, h_db, h_rec
   free_batch(h);
   for (int k = 0; k < kPipeSlots; ++k) {
     if (h->pipe_stream[k]) cudaStreamDestroy(h->pipe_stream[k]);
@@ -1601,12 +1668,14 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
 
     // ---- device
     CUDA_TRY(cudaSetDevice(device));
-    cudaDeviceProp prop{};
-    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    int sm_count = 0, smem_optin = 0;
+    if (!device_limits(device, &sm_count, &smem_optin)) {
+      fail(QB_RUNTIME_ERROR, "cudaDeviceGetAttribute failed for device " + std::to_string(device));
+    }
     h = new qb_decoder();
     h->device = device;
-    h->sm_count = prop.multiProcessorCount;
-    h->max_smem_optin = static_cast<int>(prop.sharedMemPerBlockOptin);
+    h->sm_count = sm_count;
+    h->max_smem_optin = smem_optin;
     h->arith = arith;
     int lo = 0, hi = 0;
     CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -1871,20 +1940,27 @@ qb_status qb_decoder_create(const qb_graph* graph, const qb_segment* segments,
     h->off_ns = h->off_iters + align8(P.nseg * 4);
     h->off_flag = h->off_ns + 8;
     h->out_bytes = h->off_flag + 8;
-    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h->h_in), P.syn_w32 * 4,
-                           cudaHostAllocMapped | cudaHostAllocWriteCombined));
-    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h->h_out), h->out_bytes, cudaHostAllocMapped));
-    std::memset(h->h_out, 0, h->out_bytes);
-    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_in_map), h->h_in, 0));
-    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_out_map), h->h_out, 0));
-    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h->h_db), 64 * 4, cudaHostAllocMapped));
-    std::memset(h->h_db, 0, 64 * 4);
-    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_db), h->h_db, 0));
     h->rec_stride = sector_words(record_data_words(P.seg_nmax, P.seg_mmax));
     const size_t rec_bytes = static_cast<size_t>(h->rec_stride) * P.nseg * 4;
-    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h->h_rec), rec_bytes, cudaHostAllocMapped));
-    std::memset(h->h_rec, 0, rec_bytes);
-    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_rec_map), h->h_rec, 0));
+    {
+      // one pinned slab: [syndrome in | outputs of the generic path | doorbell | records]
+      auto r256 = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
+      const size_t o_out = r256(P.syn_w32 * 4), o_db = o_out + r256(h->out_bytes), o_rec = o_db + 256;
+      h->h_slab = slab_acquire(o_rec + r256(rec_bytes), device, &h->h_slab_bytes);
+      if (!h->h_slab) fail(QB_RUNTIME_ERROR, "cudaHostAlloc failed for the single-shot staging buffers");
+      unsigned char* base = static_cast<unsigned char*>(h->h_slab);
+      unsigned char* dbase = nullptr;
+      CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dbase), base, 0));
+      h->h_in = reinterpret_cast<decltype(h->h_in)>(base);
+      h->h_out = reinterpret_cast<decltype(h->h_out)>(base + o_out);
+      h->h_db = reinterpret_cast<decltype(h->h_db)>(base + o_db);
+      h->h_rec = reinterpret_cast<decltype(h->h_rec)>(base + o_rec);
+      h->d_in_map = reinterpret_cast<decltype(h->d_in_map)>(dbase);
+      h->d_out_map = reinterpret_cast<decltype(h->d_out_map)>(dbase + o_out);
+      h->d_db = reinterpret_cast<decltype(h->d_db)>(dbase + o_db);
+      h->d_rec_map = reinterpret_cast<decltype(h->d_rec_map)>(dbase + o_rec);
+      std::memset(base, 0, o_rec + r256(rec_bytes));
+    }
     CUDA_TRY(cudaMalloc(&h->d_rec_dev, rec_bytes));
     CUDA_TRY(cudaMemset(h->d_rec_dev, 0, rec_bytes));
     CUDA_TRY(cudaMalloc(&h->d_in_dev, P.syn_w32 * 4));
