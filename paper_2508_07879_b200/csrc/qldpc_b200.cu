@@ -749,6 +749,35 @@ void optimise_edge_slots(qb_decoder* h, uint32_t T) {
   h->slot_table_for = key;
   std::vector<uint8_t> slot(E, 0);
   for (uint32_t e = 0; e < E; ++e) slot[e] = static_cast<uint8_t>(e % 6);
+  // The table is a function of the graph, its segments and the thread shape only, and costs
+  // ~1 ms to compute on [[784,24,24]] (90 ms with annealing): decoders built again and again
+  // for the same code (the reference's callers do that) find it in a small process-wide cache.
+  struct SlotCacheEntry {
+    uint64_t hash;
+    uint32_t E, nseg, T;
+    int64_t spread;
+    std::vector<uint8_t> slot;
+  };
+  static std::mutex cache_mu;
+  static std::vector<SlotCacheEntry> cache;
+  uint64_t hash = 14695981039346656037ull;
+  if (h->regular63 && T >= 32) {
+    auto mix = [&hash](uint32_t v) {
+      hash = (hash ^ v) * 1099511628211ull;
+    };
+    for (uint32_t v : h->h_var_edges) mix(v);
+    for (uint32_t sgi = 0; sgi < P.nseg; ++sgi) {
+      mix(P.segs[sgi].c0);
+      mix(P.segs[sgi].v0);
+    }
+    std::lock_guard<std::mutex> lk(cache_mu);
+    for (const SlotCacheEntry& c : cache) {
+      if (c.hash == hash && c.E == E && c.nseg == P.nseg && c.T == T && c.spread == h->opt_slot_spread) {
+        CUDA_TRY(cudaMemcpy(h->d_edge_slot, c.slot.data(), E, cudaMemcpyHostToDevice));
+        return;
+      }
+    }
+  }
   if (h->regular63 && T >= 32) {
     constexpr uint32_t kStrideWords = 14;
     std::vector<uint32_t> group_of(E, 0);
@@ -858,6 +887,11 @@ void optimise_edge_slots(qb_decoder* h, uint32_t T) {
     }
   }
   CUDA_TRY(cudaMemcpy(h->d_edge_slot, slot.data(), E, cudaMemcpyHostToDevice));
+  if (h->regular63 && T >= 32) {
+    std::lock_guard<std::mutex> lk(cache_mu);
+    if (cache.size() >= 8) cache.erase(cache.begin());
+    cache.push_back({hash, E, P.nseg, T, h->opt_slot_spread, std::move(slot)});
+  }
 }
 
 void choose_plans(qb_decoder* h);
