@@ -139,13 +139,14 @@ typedef enum {
    * ticket per tile), 1 .. 16; 0 = auto (16 for large batches, smaller when that
    * would leave resident CTAs without work). */
   QB_OPT_BATCH_TILE = 13,
-  /* Lean batch kernels ((6,3)-regular codes): 1 (default) = the loader permutes the six
-   * message slots inside every check's block so that the variable-side accesses of a
-   * warp spread over the shared-memory banks (results are unaffected: the check
-   * update is symmetric in its slots); 0 = slots in row order; 2 = as 1, then refined by
-   * simulated annealing (200 moves per edge, fixed seed: ~90 ms per thread shape on
-   * [[784,24,24]], 1.72 -> 1.43 shared-memory wavefronts per variable-side access; for
-   * long campaigns: +2.5 % / +3.5 % on the int8 / half kernels, +0.5-0.8 % on float). */
+  /* Lean batch kernels ((6,3)-regular codes): the loader permutes the six message slots
+   * inside every check's block so that the variable-side accesses of a warp spread over the
+   * shared-memory banks (results are unaffected: the check update is symmetric in its
+   * slots).  0 = slots in row order; 1 = greedy assignment + one pass of improving swaps
+   * (~1 ms); 2 (default) = as 1, then refined by simulated annealing (200 moves per edge,
+   * fixed seed: ~25 ms on [[784,24,24]], paid once per graph and thread shape in a process -
+   * the tables are cached; 1.72 -> 1.43 shared-memory wavefronts per variable-side access:
+   * +1 % on float, +2 % / +3 % / +3.6 % on int8 / half / int16 at 10 fixed iterations). */
   QB_OPT_SLOT_SPREAD = 14,
   /* qb_decode_batch (host buffers): shots per pipeline chunk (H2D copy, kernel and D2H
    * copy of consecutive chunks overlap on three streams); 0 = auto (2^15).  Also the

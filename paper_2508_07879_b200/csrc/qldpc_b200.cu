@@ -266,7 +266,7 @@ struct qb_decoder {
   int64_t opt_batch_tile = 0;  // shots per TMA syndrome tile, 0 = auto
   int64_t opt_sampler = 0;      // qb_generate_syndromes: 0 = the reference's stream, 1 = geometric skips
   int64_t opt_batch_chunk = 0;  // qb_decode_batch: shots per pipeline chunk, 0 = auto (2^15)
-  int64_t opt_slot_spread = 1;  // lean batch kernels: bank-spreading slot permutation
+  int64_t opt_slot_spread = 2;  // lean batch kernels: bank-spreading slot permutation (2 = annealed)
   int64_t opt_latency_graph = 1;
   cudaGraphExec_t lat_graph[2] = {nullptr, nullptr};
   uint32_t lat_graph_flip = 0;
