@@ -231,7 +231,12 @@ decode_lean_campaign_kernel(const __grid_constant__ DecodeParams P, const __grid
         for (int k = 0; k < VPT; ++k) eb |= vn3_first_tab<kStride>(P, msgs, smem_raw, eo[k], syn2) << k;
       } else {
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) cn6_block(P, A{}, msgs + co[k], (synbits >> k) & 1u);
+        for (int k = 0; k < CPT; ++k) {
+          // (warps without a check in the last round skip it, as in decode_lean_kernel)
+          if (k + 1 < CPT || (tid & ~31u) + static_cast<uint32_t>(CPT - 1) * T < Ms) {
+            cn6_block(P, A{}, msgs + co[k], (synbits >> k) & 1u);
+          }
+        }
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < VPT; ++k) {
